@@ -1,0 +1,181 @@
+/*
+ * dlmpc.h -- C ABI of the B200 DLMPC ADMM hot path (libdlmpc.so).
+ *
+ * This is the device boundary that replaces the reference's per-iteration
+ * execution layer (L3 in SURVEY.md §1):
+ *
+ *   reference interface                                   replaced by
+ *   ---------------------------------------------------   ---------------------------
+ *   admm_solve loop          admm.py:315-347              dlmpc_solve
+ *   Executor.run_iteration   strategies.py:249-260        dlmpc_iterate
+ *   precompute_row_data      sls_core.py:330-349          dlmpc_set_x
+ *   PhiTriple (state arrays) sls_core.py:415-438          dlmpc_get / dlmpc_put / dlmpc_zero
+ *   AdmmWorkspace.__init__   admm.py:106-127              dlmpc_create
+ *   dlmpc_simulate loop      admm.py:486-520              dlmpc_simulate
+ *   extract_control          admm.py:350-360              (inside dlmpc_simulate)
+ *   step_dynamics            admm.py:363-369              (inside dlmpc_simulate)
+ *
+ * All pointers in the structs below are HOST pointers that must stay valid
+ * only for the duration of the call; the library copies what it needs into
+ * device memory it owns. No torch types cross this boundary. A handle is
+ * bound to one device and one CUDA stream and is not thread-safe.
+ *
+ * Status codes map one to one to the Python exceptions of errors.py
+ * (reference errors.py:8-62): DLMPC_NOT_CONVERGED -> NotConverged,
+ * DLMPC_ROW_INFEASIBLE -> RowInfeasible; every other nonzero code is a
+ * DeviceError / ValueError with dlmpc_last_error() text.
+ */
+#ifndef DLMPC_H
+#define DLMPC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  DLMPC_OK = 0,
+  DLMPC_NOT_CONVERGED = 1,   /* iteration cap reached (admm.py:342-343)        */
+  DLMPC_ROW_INFEASIBLE = 2,  /* zero state on a row whose bounds exclude zero  */
+  DLMPC_BAD_ARGUMENT = 3,
+  DLMPC_CUDA_ERROR = 4,
+  DLMPC_NO_DEVICE = 5
+};
+
+/* which array dlmpc_get/dlmpc_put address (internal column layout, n_cols x s_pad) */
+enum {
+  DLMPC_PSI = 0,       /* ψ, current iterate                          */
+  DLMPC_LAM = 1,       /* λ, current iterate                          */
+  DLMPC_PSI_PREV = 2,  /* ψ before the last iteration (psi_prev_c)    */
+  DLMPC_PHI = 3,       /* φ of the last iteration (phi_c)             */
+  DLMPC_LAM_PREV = 4,  /* λ before the last iteration                 */
+  DLMPC_S_ROW = 5,     /* per-row Φ scale of the last iteration (n_rows, internal order) */
+  DLMPC_X = 6,         /* measured state currently loaded (n_x)       */
+  DLMPC_ADA = 7        /* per-subsystem ||a||^2 for the loaded state  */
+};
+
+/*
+ * Problem description. Internal layouts (built by devlayout.py):
+ *  - rows are grouped by owning subsystem: subsystem i owns internal rows
+ *    [row_start[i], row_start[i+1]) in ascending reference-row order;
+ *  - column c (= global state c, owner col_owner[c]) stores its support as
+ *    the concatenation, over ball members i of the owner (ascending), of the
+ *    rows of i; entry (row of i with local index l, column c) lives at
+ *    c*s_pad + ball_off[e] + l where e is the (i -> owner) edge of the ball CSR;
+ *  - the Ψ operator of every column class is stored padded for the FP64
+ *    tensor-core fragments (see devlayout.py).
+ */
+typedef struct dlmpc_problem {
+  int32_t n_sub, n_rows, n_cols, n_inputs, s_pad, horizon;
+  int32_t exact;          /* 1: reference arithmetic bit for bit; 0: fast path  */
+  int32_t contiguous;     /* 1: every ball is a contiguous id range (chains)    */
+  double rho;
+  /* subsystems */
+  const int64_t* row_start;      /* [n_sub+1] */
+  const int64_t* ball_ptr;       /* [n_sub+1] */
+  const int32_t* ball_idx;       /* [nnz_ball] ascending per node            */
+  const int32_t* ball_off;       /* [nnz_ball] offset of node i's rows inside column support of ball_idx[e] */
+  const int32_t* state_start;    /* [n_sub] */
+  const int32_t* state_count;    /* [n_sub] */
+  const int32_t* sub_first_bad;  /* [n_sub] lowest reference row of the node whose bounds exclude 0, or -1 */
+  /* rows, internal order */
+  const double* row_w;           /* [n_rows] */
+  const double* row_lo;
+  const double* row_hi;
+  /* columns */
+  const int32_t* col_owner;      /* [n_cols] */
+  const int32_t* col_len;        /* [n_cols] */
+  const int32_t* col_class;      /* [n_cols] */
+  const int32_t* col_vec;        /* [n_cols] index into q_pool / rhs_pool */
+  const int32_t* col_irow;       /* [n_sub*s_pad] internal row per support slot (NULL if contiguous) */
+  /* column classes (fast path operators) */
+  int32_t n_classes;
+  const int32_t* class_s;        /* [n_classes] support length                   */
+  const int32_t* class_n0;       /* null-space dimension                         */
+  const int32_t* class_ldn;      /* leading dimension of the padded operator     */
+  const int64_t* class_null_off; /* offset (doubles) into null_pool              */
+  const double* null_pool;       /* per class: [round8(s) x ldn], zero padded     */
+  int32_t n_vec;
+  const double* q_pool;          /* [n_vec x s_pad] particular solutions          */
+  /* exact path operators (reference support order) */
+  const int32_t* class_m;        /* rows of the reduced operator g               */
+  const int64_t* class_g_off;    /* offset into g_pool ([m x s] row-major)        */
+  const int64_t* class_p_off;    /* offset into p_pool ([s x m] row-major)        */
+  const double* g_pool;
+  const double* p_pool;
+  int32_t m_pad;
+  const double* rhs_pool;        /* [n_vec x m_pad] reduced rhs                   */
+  const int32_t* ref_pos;        /* [n_sub*s_pad] internal slot of reference slot p */
+  /* tiles of the column stage */
+  int32_t n_tiles, tile_cols;    /* tile_cols in {8,16,32}                        */
+  const int32_t* tile_class;     /* [n_tiles] */
+  const int32_t* tile_first;     /* [n_tiles] first index into tile_colv          */
+  const int32_t* tile_count;     /* [n_tiles] */
+  const int32_t* tile_colv;      /* [n_cols] columns sorted by class              */
+  /* plant (CSR, reference column order) for the on-device closed loop */
+  const int64_t* a_ptr; const int32_t* a_idx; const double* a_val;   /* n_cols rows  */
+  const int64_t* b_ptr; const int32_t* b_idx; const double* b_val;   /* n_cols rows  */
+  const int32_t* input_owner;    /* [n_inputs] */
+  const int32_t* input_local;    /* [n_inputs] local row index of input k at t=0 */
+} dlmpc_problem;
+
+typedef struct dlmpc_handle dlmpc_handle;
+
+/* Upload a problem and allocate all device state (zeroed). */
+int dlmpc_create(const dlmpc_problem* prob, int device, dlmpc_handle** out);
+void dlmpc_destroy(dlmpc_handle* h);
+const char* dlmpc_last_error(const dlmpc_handle* h);
+/* Library-wide error text for failures before a handle exists. */
+const char* dlmpc_global_error(void);
+
+/* Load a measured state: ||a||^2 per subsystem on device and the row
+ * feasibility check of sls_core.py:346-348. *bad_row = first infeasible
+ * reference row or -1; returns DLMPC_ROW_INFEASIBLE in that case. */
+int dlmpc_set_x(dlmpc_handle* h, const double* x, int64_t* bad_row);
+
+/* ADMM from the current iterate until both residuals are within tolerance
+ * (admm.py:336-343). hist receives 2*iters doubles (pri, dual). */
+int dlmpc_solve(dlmpc_handle* h, int max_iters, double eps_pri, double eps_dual,
+                int* iters, double* hist);
+
+/* Exactly n iterations, no convergence stop (Executor.run_iteration x n). */
+int dlmpc_iterate(dlmpc_handle* h, int n, double* hist);
+
+/* Closed loop of t_sim MPC steps fully on device (admm.py:486-520):
+ * row data, solve, control extraction and plant step per step in one
+ * persistent launch. states: (t_sim+1) x n_cols, inputs: t_sim x n_inputs,
+ * step_iters: t_sim. On failure *fail_step is the step, *bad_row the row
+ * (RowInfeasible) and fail_hist receives the failing step's history
+ * (2*max_iters doubles, *fail_iters entries valid). cold_start zeroes the
+ * iterate first (a fresh PhiTriple, admm.py:466). */
+int dlmpc_simulate(dlmpc_handle* h, const double* x0, int t_sim, int warm_start, int cold_start,
+                   int max_iters, double eps_pri, double eps_dual,
+                   double* states, double* inputs, int* step_iters,
+                   int* fail_step, int64_t* bad_row, int* fail_iters, double* fail_hist);
+
+/* Same closed loop with x0 and all outputs already in device memory
+ * (device pointers); nothing is copied and the call does not synchronise. */
+int dlmpc_simulate_device(dlmpc_handle* h, const double* x0_dev, int t_sim, int warm_start,
+                          int cold_start, int max_iters, double eps_pri, double eps_dual,
+                          double* states_dev, double* inputs_dev, int* step_iters_dev,
+                          int* status_dev);
+
+/* Copy an internal-layout array to/from host memory. */
+int dlmpc_get(dlmpc_handle* h, int which, double* dst);
+int dlmpc_put(dlmpc_handle* h, int which, const double* src);
+int dlmpc_zero(dlmpc_handle* h);
+
+/* Device time (ms, CUDA events on the handle's stream) of the last
+ * solve / iterate / simulate launch, and the number of kernels it launched. */
+int dlmpc_last_timing(const dlmpc_handle* h, float* ms, int* launches);
+/* The CUDA stream of the handle (cudaStream_t as void*). */
+void* dlmpc_stream(dlmpc_handle* h);
+int dlmpc_synchronize(dlmpc_handle* h);
+/* Shape info: n_rows, n_cols, s_pad, n_sub, grid CTAs, tile_cols, smem bytes. */
+int dlmpc_info(const dlmpc_handle* h, int64_t* out7);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DLMPC_H */
