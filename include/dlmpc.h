@@ -79,6 +79,10 @@ typedef struct dlmpc_problem {
   const int32_t* state_start;    /* [n_sub] */
   const int32_t* state_count;    /* [n_sub] */
   const int32_t* sub_first_bad;  /* [n_sub] lowest reference row of the node whose bounds exclude 0, or -1 */
+  int32_t d_pad;                 /* padded row-support length (>= max supp_len)  */
+  const int32_t* supp_col;       /* [n_sub*d_pad] row-support columns, ascending  */
+  const int32_t* supp_off;       /* [n_sub*d_pad] block offset of the node's rows in each of those columns */
+  const int32_t* supp_len;       /* [n_sub] row-support length (= d_row of the node's rows) */
   /* rows, internal order */
   const double* row_w;           /* [n_rows] */
   const double* row_lo;
@@ -89,26 +93,27 @@ typedef struct dlmpc_problem {
   const int32_t* col_class;      /* [n_cols] */
   const int32_t* col_vec;        /* [n_cols] index into q_pool / rhs_pool */
   const int32_t* col_irow;       /* [n_sub*s_pad] internal row per support slot (NULL if contiguous) */
+  const int64_t* col_rowbase;    /* [n_cols] internal row of support slot 0 (contiguous supports) */
   /* column classes (fast path operators) */
   int32_t n_classes;
   const int32_t* class_s;        /* [n_classes] support length                   */
   const int32_t* class_n0;       /* null-space dimension                         */
   const int32_t* class_ldn;      /* leading dimension of the padded operator     */
-  const int64_t* class_null_off; /* offset (doubles) into null_pool              */
+  const int64_t* class_null_off; /* [n_classes+1] offsets (doubles) into null_pool */
   const double* null_pool;       /* per class: [round8(s) x ldn], zero padded     */
   int32_t n_vec;
   const double* q_pool;          /* [n_vec x s_pad] particular solutions          */
   /* exact path operators (reference support order) */
   const int32_t* class_m;        /* rows of the reduced operator g               */
-  const int64_t* class_g_off;    /* offset into g_pool ([m x s] row-major)        */
-  const int64_t* class_p_off;    /* offset into p_pool ([s x m] row-major)        */
+  const int64_t* class_g_off;    /* [n_classes+1] offsets into g_pool ([m x s])   */
+  const int64_t* class_p_off;    /* [n_classes+1] offsets into p_pool ([s x m])   */
   const double* g_pool;
   const double* p_pool;
   int32_t m_pad;
   const double* rhs_pool;        /* [n_vec x m_pad] reduced rhs                   */
   const int32_t* ref_pos;        /* [n_sub*s_pad] internal slot of reference slot p */
   /* tiles of the column stage */
-  int32_t n_tiles, tile_cols;    /* tile_cols in {8,16,32}                        */
+  int32_t n_tiles, tile_cols;    /* tile_cols in {8,16}                           */
   const int32_t* tile_class;     /* [n_tiles] */
   const int32_t* tile_first;     /* [n_tiles] first index into tile_colv          */
   const int32_t* tile_count;     /* [n_tiles] */
@@ -172,6 +177,11 @@ int dlmpc_last_timing(const dlmpc_handle* h, float* ms, int* launches);
 /* The CUDA stream of the handle (cudaStream_t as void*). */
 void* dlmpc_stream(dlmpc_handle* h);
 int dlmpc_synchronize(dlmpc_handle* h);
+/* Per-CTA per-phase device nanoseconds accumulated by a profiling build
+ * (-DDLMPC_PHASE_TIMING; zeros otherwise): out[grid*8]; reset clears them.
+ * Phases: 0 Φ, 1 Ψ prologue, 2 GEMM 1, 3 GEMM 2, 4 epilogue, 5 residual
+ * publish, 6 grid barrier. */
+int dlmpc_phase_times(dlmpc_handle* h, uint64_t* out, int reset);
 /* Shape info: n_rows, n_cols, s_pad, n_sub, grid CTAs, tile_cols, smem bytes. */
 int dlmpc_info(const dlmpc_handle* h, int64_t* out7);
 

@@ -1,0 +1,854 @@
+// dlmpc_device.cuh -- device code of the DLMPC ADMM hot path (sm_100a).
+//
+// Three persistent cooperative kernels, one launch per solve / closed loop:
+//
+//  dlmpc_patch<TC>     fast path for layouts whose d-hop balls are contiguous
+//                      subsystem-id ranges (chains, banded graphs). Each CTA
+//                      owns contiguous work units of subsystems. Per ADMM
+//                      iteration and unit it (1) recomputes the Φ scale s_r of
+//                      every row its columns touch -- own rows plus a d-hop
+//                      halo -- into shared memory (the paper's column patch,
+//                      §III-D; reference admm.py:155-170, 227-253), (2) runs
+//                      the Ψ projection of its columns as two FP64 tensor-core
+//                      GEMMs against the class null-space basis staged in
+//                      shared memory once per launch, then the Λ update and
+//                      the residual maxima (admm.py:174-217), writing (ψ',λ')
+//                      to the other ping-pong buffer. ONE grid barrier per
+//                      iteration, which also publishes the global (pri, dual).
+//  dlmpc_twophase<TC>  fast path for arbitrary graphs: a grid-wide Φ stage
+//                      writes s_r to global memory, barrier, column stage.
+//  dlmpc_exact         the reference's arithmetic bit for bit (dense
+//                      projector, numpy pairwise sums, no FMA), two-phase.
+//
+// φ is never stored: φ(r,c) = (ψ-λ)(r,c) + s_r·x_c is rebuilt where needed.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace cg = cooperative_groups;
+
+namespace dlmpc {
+
+// Optional per-phase timers (profiling build only: -DDLMPC_PHASE_TIMING).
+// Thread 0 of every CTA accumulates globaltimer deltas per phase into
+// P.phase_ns[blockIdx.x * 8 + phase].
+#ifdef DLMPC_PHASE_TIMING
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t;
+}
+#define PT_DECL unsigned long long pt_t0 = 0;
+#define PT_START if (threadIdx.x == 0) pt_t0 = gtimer();
+#define PT_LAP(P, ph) if (threadIdx.x == 0) { unsigned long long t1_ = gtimer(); (P).phase_ns[blockIdx.x * 8 + (ph)] += t1_ - pt_t0; pt_t0 = t1_; }
+#else
+#define PT_DECL
+#define PT_START
+#define PT_LAP(P, ph)
+#endif
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kBadNone = 0x7f7f7f7f;   // cudaMemset(0x7f) pattern = "no infeasible row"
+constexpr int kMG1 = 4;                // m-tiles per GEMM-1 work unit
+constexpr int kMG2 = 2;                // m-tiles per GEMM-2 work unit
+
+struct DevProblem {
+  int n_sub, n_rows, n_cols, n_inputs, s_pad, exact, contiguous, d_row;
+  double rho;
+  const int64_t* row_start; const int64_t* ball_ptr; const int* ball_idx; const int* ball_off;
+  const int* state_start; const int* state_count; const int* sub_first_bad;
+  int d_pad; const int* supp_col; const int* supp_off; const int* supp_len;
+  const double* row_w; const double* row_lo; const double* row_hi;
+  const int* col_owner; const int* col_len; const int* col_class; const int* col_vec; const int* col_irow;
+  const int64_t* col_rowbase;
+  int n_classes; const int* class_s; const int* class_n0; const int* class_ldn;
+  const int64_t* class_null_off; const double* null_pool; const double* q_pool;
+  const int* class_m; const int64_t* class_g_off; const int64_t* class_p_off;
+  const double* g_pool; const double* p_pool; int m_pad; const double* rhs_pool; const int* ref_pos;
+  int n_tiles, tile_cols; const int* tile_class; const int* tile_first; const int* tile_count;
+  const int* tile_colv;
+  const int64_t* a_ptr; const int* a_idx; const double* a_val;
+  const int64_t* b_ptr; const int* b_idx; const double* b_val;
+  const int* input_owner; const int* input_local;
+  // patch work units (built by the library at create time)
+  const int* cta_unit_ptr;     // [grid+1]
+  const int* unit_sub_lo;      // own subsystems [lo, hi)
+  const int* unit_sub_hi;
+  const int* unit_patch_lo;    // halo subsystems [lo, hi) whose rows the unit's columns touch
+  const int* unit_patch_hi;
+  const int* unit_chunk_ptr;   // [n_units+1]
+  const int* chunk_class; const int* chunk_col0; const int* chunk_n;
+  // mutable device state
+  double* psi[2]; double* lam[2]; double* s_row; double* ada; double* x[2]; double* u;
+  unsigned long long* resid;   // [2 * cap] residual maxima per iteration (ordered bits)
+  int* ctl;                    // 0 status, 1 fail step, 2/3 bad-row slots, 4 cur buffer, 5 fail iters
+  unsigned long long* phase_ns;   // [grid * 8] (profiling build only)
+  // shared-memory plan (offsets in doubles)
+  int opr_cap;                 // doubles of the per-CTA operator region at smem offset 0
+  int s8_max, n08_max, ldk, ldy, split_max, patch_cap, cache_phi;
+  int off_k, off_y, off_yp, off_red, off_meta, off_patch, off_phimeta, off_ex;
+};
+
+struct RunArgs {
+  int t_sim, closed_loop, warm_start, cold_start, max_iters, stop_on_conv;
+  double eps_pri, eps_dual;
+  double* hist;        // [2*max_iters] history of the current / failing step
+  int* step_iters;     // [t_sim]
+  double* states;      // [(t_sim+1) * n_cols] (closed loop)
+  double* inputs;      // [t_sim * n_inputs]
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+template <bool EXACT>
+__device__ __forceinline__ double make_phi(double v, double s, double xc) {
+  return EXACT ? __dadd_rn(v, __dmul_rn(s, xc)) : fma(s, xc, v);
+}
+
+// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum_DOUBLE) of rounded products f(i); the reference's Ψ
+// reductions `.sum(axis=2)` (admm.py:184, 186) use it.
+template <class F>
+__device__ double pairwise_sum(const F& f, int lo, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, f(lo + i));
+    return r;
+  }
+  if (n <= 128) {
+    double r0 = f(lo), r1 = f(lo + 1), r2 = f(lo + 2), r3 = f(lo + 3);
+    double r4 = f(lo + 4), r5 = f(lo + 5), r6 = f(lo + 6), r7 = f(lo + 7);
+    int i = 8;
+    const int stop = n - (n % 8);
+    for (; i < stop; i += 8) {
+      r0 = __dadd_rn(r0, f(lo + i));     r1 = __dadd_rn(r1, f(lo + i + 1));
+      r2 = __dadd_rn(r2, f(lo + i + 2)); r3 = __dadd_rn(r3, f(lo + i + 3));
+      r4 = __dadd_rn(r4, f(lo + i + 4)); r5 = __dadd_rn(r5, f(lo + i + 5));
+      r6 = __dadd_rn(r6, f(lo + i + 6)); r7 = __dadd_rn(r7, f(lo + i + 7));
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                           __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+    for (; i < n; ++i) res = __dadd_rn(res, f(lo + i));
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_sum(f, lo, n2), pairwise_sum(f, lo + n2, n - n2));
+}
+
+struct ProdRow {   // row[j] * v[j]
+  const double* row; const double* v;
+  __device__ double operator()(int j) const { return __dmul_rn(row[j], v[j]); }
+};
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double m = 0.0;
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < kWarps ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  }
+  return m;   // valid in thread 0
+}
+
+__device__ __forceinline__ void publish_residuals(const DevProblem& P, int it, double pri_m,
+                                                  double dual_m, double* red) {
+  const double bp = block_max(pri_m, red);
+  const double bd = block_max(dual_m, red);
+  if (threadIdx.x == 0) {
+    atomicMax(P.resid + 2 * it, static_cast<unsigned long long>(__double_as_longlong(bp)));
+    atomicMax(P.resid + 2 * it + 1, static_cast<unsigned long long>(__double_as_longlong(bd)));
+  }
+}
+
+// ||a||^2 per subsystem (reference sls_core.py:338-339: all rows of a
+// subsystem share the support, hence a_pad and a_dot_a) and the RowInfeasible
+// scan of sls_core.py:346-348. Strict ascending order, no FMA, in all modes.
+__device__ void row_data_stage(const DevProblem& P, const double* x, int* bad_slot) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, GT = gridDim.x * blockDim.x;
+  for (int i = gt; i < P.n_sub; i += GT) {
+    const int D = P.supp_len[i];
+    const int* sc = P.supp_col + static_cast<size_t>(i) * P.d_pad;
+    double acc = 0.0;
+    for (int k = 0; k < D; ++k) {
+      const double xc = ld_cg(x + sc[k]);
+      const double pr = __dmul_rn(xc, xc);
+      acc = k == 0 ? pr : __dadd_rn(acc, pr);
+    }
+    if (D < P.d_row) acc = __dadd_rn(acc, 0.0);   // the padded slots of a_pad
+    P.ada[i] = acc;
+    if (acc == 0.0 && P.sub_first_bad[i] >= 0) atomicMin(bad_slot, P.sub_first_bad[i]);
+  }
+}
+
+// Φ scale of the rows of subsystem i (one warp; lanes = rows). Lane k first
+// holds the k-th (column, block offset, x_c) of the shared row support; the
+// row lanes then read their ψ,λ entries 8 support columns at a time.
+// Calls `out(row_local, s)` for every row.
+template <bool EXACT, class Out>
+__device__ __forceinline__ void phi_rows_of(const DevProblem& P, int i, const double* psi,
+                                            const double* lam, const double* x, const Out& out) {
+  const int lane = threadIdx.x & 31;
+  const int D = P.supp_len[i];
+  const int* sc = P.supp_col + static_cast<size_t>(i) * P.d_pad;
+  const int* so = P.supp_off + static_cast<size_t>(i) * P.d_pad;
+  const long long r0 = P.row_start[i];
+  const int nr = static_cast<int>(P.row_start[i + 1] - r0);
+  const double ada = ld_cg(P.ada + i);
+  const double rho = P.rho;
+  for (int l0 = 0; l0 < nr; l0 += 32) {
+    const int l = l0 + lane;
+    const bool row_ok = l < nr;
+    double w = 0.0, lo = 0.0, hi = 0.0;
+    if (row_ok) { w = P.row_w[r0 + l]; lo = P.row_lo[r0 + l]; hi = P.row_hi[r0 + l]; }
+    double acc = 0.0;
+    bool first = true;
+    for (int k0 = 0; k0 < D; k0 += 32) {
+      const int kn = min(32, D - k0);
+      long long base_k = 0;
+      double x_k = 0.0;
+      if (lane < kn) {
+        const int c = sc[k0 + lane];
+        base_k = static_cast<long long>(c) * P.s_pad + so[k0 + lane];
+        x_k = ld_cg(x + c);
+      }
+      for (int u0 = 0; u0 < kn; u0 += 8) {
+        double pv[8], lv[8], xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const long long bk = __shfl_sync(0xffffffffu, base_k, (u0 + u) & 31);
+          xv[u] = __shfl_sync(0xffffffffu, x_k, (u0 + u) & 31);
+          pv[u] = 0.0; lv[u] = 0.0;
+          if (row_ok && u0 + u < kn) {
+            pv[u] = ld_cg(psi + bk + l);
+            lv[u] = ld_cg(lam + bk + l);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (u0 + u < kn) {
+            const double v = __dsub_rn(pv[u], lv[u]);
+            if (EXACT) {
+              const double pr = __dmul_rn(v, xv[u]);
+              acc = first ? pr : __dadd_rn(acc, pr);
+              first = false;
+            } else {
+              acc = fma(v, xv[u], acc);
+            }
+          }
+        }
+      }
+    }
+    if (!row_ok) continue;
+    if (EXACT && D < P.d_row) acc = __dadd_rn(acc, 0.0);
+    // y0 = ρc/(ρ + 2w·ada); clip; s = (y - c)/ada   (admm.py:162-166)
+    const double y0 = __ddiv_rn(__dmul_rn(rho, acc), __dadd_rn(rho, __dmul_rn(__dmul_rn(2.0, w), ada)));
+    const double y = fmin(fmax(y0, lo), hi);
+    out(l, ada > 0.0 ? __ddiv_rn(__dsub_rn(y, acc), ada) : 0.0);
+  }
+}
+
+// Grid-wide Φ stage of the two-phase kernels: s_r -> global s_row.
+template <bool EXACT>
+__device__ void phi_stage_global(const DevProblem& P, int b, const double* x) {
+  const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5), GW = gridDim.x * kWarps;
+  for (int i = gw; i < P.n_sub; i += GW) {
+    double* dst = P.s_row + P.row_start[i];
+    phi_rows_of<EXACT>(P, i, P.psi[b], P.lam[b], x, [dst](int l, double s) { dst[l] = s; });
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fast column chunk: TC columns of one class. The caller fills the per-column
+// metadata (smem) -- m_pos[t] = column base offset c*s_pad, m_s[t] = offset
+// of support slot 0 in the s source, m_q[t] = q offset, m_x[t] = x_c -- for
+// t < nt, and the s source is `s_src` (shared patch or global s_row); with
+// `irow` non-null, the global generic layout maps support slots to rows.
+// shared: kt [TC][ldk] (K, then O), yb [n08][ldy], yp [split][n08][TC].
+// ---------------------------------------------------------------------------
+template <int TC, bool S_GLOBAL, bool OPS>
+__device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi, const double* lam,
+                           double* psi_n, double* lam_n, const double* s_src, const int* irow_tab,
+                           double* smem, double& pri_m, double& dual_m) {
+  constexpr int NTN = TC / 8;
+  constexpr int WPC = kWarps / TC;   // warps per column in the element loops
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  double* kt = smem + P.off_k;
+  double* yb = smem + P.off_y;
+  double* yp = smem + P.off_yp;
+  const long long* m_pos = reinterpret_cast<const long long*>(smem + P.off_meta);
+  const long long* m_s = m_pos + TC;
+  const long long* m_q = m_pos + 2 * TC;
+  const double* m_x = smem + P.off_meta + 3 * TC;
+  const int ldk = P.ldk, ldy = P.ldy;
+  const int S = P.class_s[k], S8 = (S + 7) & ~7;
+  const int n0 = P.class_n0[k], n08 = (n0 + 7) & ~7;
+  const int ldn = P.class_ldn[k];
+  // the class operator: staged at smem offset 0 (LDS) or read from global
+  const double* nop = OPS ? smem : P.null_pool + P.class_null_off[k];
+  PT_DECL
+  PT_START
+  const int t_el = warp / WPC;                  // this warp's column in element loops
+  const int p_el0 = (warp % WPC) * 32 + lane;   // first support slot
+  constexpr int PSTEP = 32 * WPC;
+  // prologue: K[t][p] = φ + λ (admm.py:183), zero padded to TC x S8
+  {
+    const int t = t_el;
+    const bool col_ok = t < nt;
+    const long long pos0 = col_ok ? m_pos[t] : 0, s0 = col_ok ? m_s[t] : 0;
+    const double xc = col_ok ? m_x[t] : 0.0;
+    for (int pb = p_el0; pb < S8; pb += 4 * PSTEP) {
+      double ps[4], lm[4], sr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int p = pb + u * PSTEP;
+        ps[u] = lm[u] = sr[u] = 0.0;
+        if (col_ok && p < S) {
+          ps[u] = ld_cg(psi + pos0 + p);
+          lm[u] = ld_cg(lam + pos0 + p);
+          sr[u] = !S_GLOBAL ? s_src[s0 + p] : ld_cg(s_src + (irow_tab ? irow_tab[s0 + p] : s0 + p));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int p = pb + u * PSTEP;
+        if (p < S8) {
+          double kv = 0.0;
+          if (col_ok && p < S) kv = __dadd_rn(make_phi<false>(__dsub_rn(ps[u], lm[u]), sr[u], xc), lm[u]);
+          kt[t * ldk + p] = kv;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  PT_LAP(P, 1)
+  // GEMM 1: Y[a][t] = sum_p N[p][a] K[t][p]  (M = n0, N = TC, K = S), split-K
+  const int mt1 = n08 >> 3, ks1 = S8 >> 2;
+  const int groups1 = (mt1 + kMG1 - 1) / kMG1;
+  int split = 1;
+  while (groups1 * split * 2 <= kWarps && split < P.split_max) split <<= 1;
+  for (int u = warp; u < groups1 * split; u += kWarps) {
+    const int grp = u / split, sl = u - grp * split;
+    const int mt0 = grp * kMG1;
+    double acc[kMG1][NTN][2];
+#pragma unroll
+    for (int m = 0; m < kMG1; ++m)
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
+    for (int ks = sl; ks < ks1; ks += split) {
+      const int p = ks * 4 + tig;
+      double bf[NTN];
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) bf[nn] = kt[(nn * 8 + g) * ldk + p];
+#pragma unroll
+      for (int m = 0; m < kMG1; ++m) {
+        if (mt0 + m < mt1) {
+          const double af = nop[p * ldn + (mt0 + m) * 8 + g];
+#pragma unroll
+          for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
+        }
+      }
+    }
+    double* dst = split == 1 ? yb : yp + static_cast<size_t>(sl) * P.n08_max * TC;
+    const int ld = split == 1 ? ldy : TC;
+#pragma unroll
+    for (int m = 0; m < kMG1; ++m) {
+      if (mt0 + m < mt1) {
+#pragma unroll
+        for (int nn = 0; nn < NTN; ++nn) {
+          dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig] = acc[m][nn][0];
+          dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig + 1] = acc[m][nn][1];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (split > 1) {
+    for (int idx = tid; idx < n08 * TC; idx += kThreads) {
+      const int a = idx / TC, t = idx - a * TC;
+      double v = yp[idx];
+      for (int sl = 1; sl < split; ++sl) v += yp[static_cast<size_t>(sl) * P.n08_max * TC + idx];
+      yb[a * ldy + t] = v;
+    }
+    __syncthreads();
+  }
+  PT_LAP(P, 2)
+  // GEMM 2: O[t][p] = sum_a N[p][a] Y[a][t]  (M = S, N = TC, K = n0) -> kt
+  const int mt2 = S8 >> 3, ks2 = n08 >> 2;
+  for (int mb = warp; mb < mt2; mb += kWarps * kMG2) {
+    double acc[kMG2][NTN][2];
+#pragma unroll
+    for (int m = 0; m < kMG2; ++m)
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
+    for (int ks = 0; ks < ks2; ++ks) {
+      const int a = ks * 4 + tig;
+      double bf[NTN];
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) bf[nn] = yb[a * ldy + nn * 8 + g];
+#pragma unroll
+      for (int m = 0; m < kMG2; ++m) {
+        const int mt = mb + m * kWarps;
+        if (mt < mt2) {
+          const double af = nop[(mt * 8 + g) * ldn + a];
+#pragma unroll
+          for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kMG2; ++m) {
+      const int mt = mb + m * kWarps;
+      if (mt < mt2) {
+#pragma unroll
+        for (int nn = 0; nn < NTN; ++nn) {
+          kt[(nn * 8 + 2 * tig) * ldk + mt * 8 + g] = acc[m][nn][0];
+          kt[(nn * 8 + 2 * tig + 1) * ldk + mt * 8 + g] = acc[m][nn][1];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  PT_LAP(P, 3)
+  // epilogue: ψ' = q + O, λ' = λ + (φ - ψ'), residuals (admm.py:186, 207, 216-217)
+  {
+    const int t = t_el;
+    if (t < nt) {
+      const long long pos0 = m_pos[t], s0 = m_s[t], q0 = m_q[t];
+      const double xc = m_x[t];
+      for (int pb = p_el0; pb < S; pb += 4 * PSTEP) {
+        double ps[4], lm[4], sr[4], qv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int p = pb + u * PSTEP;
+          ps[u] = lm[u] = sr[u] = qv[u] = 0.0;
+          if (p < S) {
+            ps[u] = ld_cg(psi + pos0 + p);
+            lm[u] = ld_cg(lam + pos0 + p);
+            sr[u] = !S_GLOBAL ? s_src[s0 + p] : ld_cg(s_src + (irow_tab ? irow_tab[s0 + p] : s0 + p));
+            qv[u] = P.q_pool[q0 + p];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int p = pb + u * PSTEP;
+          if (p < S) {
+            const double phi = make_phi<false>(__dsub_rn(ps[u], lm[u]), sr[u], xc);
+            const double pn = qv[u] + kt[t * ldk + p];
+            const double d = __dsub_rn(phi, pn);
+            psi_n[pos0 + p] = pn;
+            lam_n[pos0 + p] = __dadd_rn(lm[u], d);
+            pri_m = fmax(pri_m, fabs(d));
+            dual_m = fmax(dual_m, fabs(__dsub_rn(pn, ps[u])));
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  PT_LAP(P, 4)
+}
+
+// Make class k's null-space operator resident at smem offset 0 if it fits
+// (cooperative copy, once per class change -- with the class-aware CTA
+// assignment, once per launch). Returns whether it is in shared memory.
+__device__ __forceinline__ bool stage_operator(const DevProblem& P, int k, double* smem, int& cur) {
+  const long long n = static_cast<long long>((P.class_s[k] + 7) & ~7) * P.class_ldn[k];
+  if (n > P.opr_cap) return false;
+  if (k != cur) {
+    __syncthreads();
+    const double2* src = reinterpret_cast<const double2*>(P.null_pool + P.class_null_off[k]);
+    double2* dst = reinterpret_cast<double2*>(smem);
+    for (long long q = threadIdx.x; q < n / 2; q += kThreads) dst[q] = __ldg(src + q);
+    __syncthreads();
+    cur = k;
+  }
+  return true;
+}
+
+template <int TC, bool S_GLOBAL>
+__device__ __forceinline__ void run_chunk(const DevProblem& P, int k, int nt, const double* psi,
+                                          const double* lam, double* psi_n, double* lam_n,
+                                          const double* s_src, const int* irow_tab, double* smem,
+                                          int& cur, double& pri_m, double& dual_m) {
+  if (stage_operator(P, k, smem, cur))
+    fast_chunk<TC, S_GLOBAL, true>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m);
+  else
+    fast_chunk<TC, S_GLOBAL, false>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m);
+}
+
+// Column stage of the two-phase fast kernel (class-sorted tiles, generic graphs).
+template <int TC>
+__device__ void column_stage_tiles(const DevProblem& P, int b, const double* x, int it, double* smem,
+                                   int& cur) {
+  long long* m_pos = reinterpret_cast<long long*>(smem + P.off_meta);
+  double* m_x = smem + P.off_meta + 3 * TC;
+  double pri_m = 0.0, dual_m = 0.0;
+  for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
+    const int k = P.tile_class[tile], first = P.tile_first[tile], nt = P.tile_count[tile];
+    if (threadIdx.x < TC) {
+      const int t = threadIdx.x;
+      long long pos = 0, s0 = 0, q0 = 0;
+      double xc = 0.0;
+      if (t < nt) {
+        const int c = P.tile_colv[first + t];
+        pos = static_cast<long long>(c) * P.s_pad;
+        s0 = P.contiguous ? P.col_rowbase[c] : static_cast<long long>(P.col_owner[c]) * P.s_pad;
+        q0 = static_cast<long long>(P.col_vec[c]) * P.s_pad;
+        xc = ld_cg(x + c);
+      }
+      m_pos[t] = pos; m_pos[TC + t] = s0; m_pos[2 * TC + t] = q0; m_x[t] = xc;
+    }
+    __syncthreads();
+    run_chunk<TC, true>(P, k, nt, P.psi[b], P.lam[b], P.psi[b ^ 1], P.lam[b ^ 1], P.s_row,
+                        P.contiguous ? nullptr : P.col_irow, smem, cur, pri_m, dual_m);
+  }
+  publish_residuals(P, it, pri_m, dual_m, smem + P.off_red);
+}
+
+// Per-step Φ metadata of a CTA's single unit, cached in shared memory (the
+// support descriptors, x on the support, row costs/bounds and ||a||^2 are
+// constant for a whole MPC step): each iteration's Φ then needs one L2 round
+// trip (the ψ,λ reads) instead of three.
+// layout at off_phimeta: base [np*d_pad] (int64), xk [np*d_pad], ada [np],
+//                        w/lo/hi [3*prows], len [np] (int32 in a double slot)
+__device__ void cache_phi_meta(const DevProblem& P, const double* x, double* smem) {
+  const int un0 = P.cta_unit_ptr[blockIdx.x];
+  if (un0 == P.cta_unit_ptr[blockIdx.x + 1]) return;
+  const int plo = P.unit_patch_lo[un0], phi_ = P.unit_patch_hi[un0];
+  const int np = phi_ - plo;
+  const long long prow0 = P.row_start[plo];
+  const int prows = static_cast<int>(P.row_start[phi_] - prow0);
+  double* base = smem + P.off_phimeta;
+  long long* bk = reinterpret_cast<long long*>(base);
+  double* xk = base + static_cast<size_t>(np) * P.d_pad;
+  double* ada = xk + static_cast<size_t>(np) * P.d_pad;
+  double* rw = ada + np;
+  int* len = reinterpret_cast<int*>(rw + 3 * prows);
+  for (int q = threadIdx.x; q < np * P.d_pad; q += kThreads) {
+    const int i = plo + q / P.d_pad, k = q % P.d_pad;
+    if (k < P.supp_len[i]) {
+      const size_t e = static_cast<size_t>(i) * P.d_pad + k;
+      const int c = P.supp_col[e];
+      bk[q] = static_cast<long long>(c) * P.s_pad + P.supp_off[e];
+      xk[q] = ld_cg(x + c);
+    }
+  }
+  for (int q = threadIdx.x; q < np; q += kThreads) { ada[q] = ld_cg(P.ada + plo + q); len[q] = P.supp_len[plo + q]; }
+  for (int q = threadIdx.x; q < prows; q += kThreads) {
+    rw[q] = P.row_w[prow0 + q]; rw[prows + q] = P.row_lo[prow0 + q]; rw[2 * prows + q] = P.row_hi[prow0 + q];
+  }
+  __syncthreads();
+}
+
+// Φ scale of the rows of patch subsystem q from the cached metadata (fast path).
+template <class Out>
+__device__ __forceinline__ void phi_rows_cached(const DevProblem& P, int q, int np, int prows,
+                                                int r_off, int nr, const double* psi, const double* lam,
+                                                const double* smem, const Out& out) {
+  const int lane = threadIdx.x & 31;
+  const double* base = smem + P.off_phimeta;
+  const long long* bk = reinterpret_cast<const long long*>(base) + static_cast<size_t>(q) * P.d_pad;
+  const double* xk = base + static_cast<size_t>(np) * P.d_pad + static_cast<size_t>(q) * P.d_pad;
+  const double* ada_p = base + 2 * static_cast<size_t>(np) * P.d_pad;
+  const double* rw = ada_p + np;
+  const int D = reinterpret_cast<const int*>(rw + 3 * prows)[q];
+  const double ada = ada_p[q];
+  const double rho = P.rho;
+  for (int l0 = 0; l0 < nr; l0 += 32) {
+    const int l = l0 + lane;
+    if (l >= nr) break;
+    double acc = 0.0;
+    for (int k0 = 0; k0 < D; k0 += 8) {
+      double pv[8], lv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        pv[u] = lv[u] = 0.0;
+        if (k0 + u < D) {
+          const long long b = bk[k0 + u] + l;
+          pv[u] = ld_cg(psi + b);
+          lv[u] = ld_cg(lam + b);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (k0 + u < D) acc = fma(__dsub_rn(pv[u], lv[u]), xk[k0 + u], acc);
+    }
+    const int rr = r_off + l;
+    const double w = rw[rr], lo = rw[prows + rr], hi = rw[2 * prows + rr];
+    const double y0 = __ddiv_rn(__dmul_rn(rho, acc), __dadd_rn(rho, __dmul_rn(__dmul_rn(2.0, w), ada)));
+    const double y = fmin(fmax(y0, lo), hi);
+    out(l, ada > 0.0 ? __ddiv_rn(__dsub_rn(y, acc), ada) : 0.0);
+  }
+}
+
+// One ADMM iteration of the patch kernel for this CTA's units.
+template <int TC>
+__device__ void patch_iteration(const DevProblem& P, int b, const double* x, int it, double* smem,
+                                int& cur) {
+  double* s_patch = smem + P.off_patch;
+  long long* m_pos = reinterpret_cast<long long*>(smem + P.off_meta);
+  double* m_x = smem + P.off_meta + 3 * TC;
+  const int warp = threadIdx.x >> 5;
+  const double* psi = P.psi[b];
+  const double* lam = P.lam[b];
+  double pri_m = 0.0, dual_m = 0.0;
+  PT_DECL
+  for (int un = P.cta_unit_ptr[blockIdx.x]; un < P.cta_unit_ptr[blockIdx.x + 1]; ++un) {
+    PT_START
+    const int own_lo = P.unit_sub_lo[un], own_hi = P.unit_sub_hi[un];
+    const int plo = P.unit_patch_lo[un], phi_ = P.unit_patch_hi[un];
+    const long long prow0 = P.row_start[plo];
+    const int prows = static_cast<int>(P.row_start[phi_] - prow0);
+    // Φ scale of every row the unit's columns touch (own rows + d-hop halo)
+    for (int i = plo + warp; i < phi_; i += kWarps) {
+      const int r_off = static_cast<int>(P.row_start[i] - prow0);
+      double* dst = s_patch + r_off;
+      double* gdst = (i >= own_lo && i < own_hi) ? P.s_row + P.row_start[i] : nullptr;
+      auto out = [dst, gdst](int l, double s) {
+        dst[l] = s;
+        if (gdst) gdst[l] = s;
+      };
+      if (P.cache_phi)
+        phi_rows_cached(P, i - plo, phi_ - plo, prows, r_off, static_cast<int>(P.row_start[i + 1] - P.row_start[i]),
+                        psi, lam, smem, out);
+      else
+        phi_rows_of<false>(P, i, psi, lam, x, out);
+    }
+    __syncthreads();
+    PT_LAP(P, 0)
+    for (int ch = P.unit_chunk_ptr[un]; ch < P.unit_chunk_ptr[un + 1]; ++ch) {
+      const int k = P.chunk_class[ch], c0 = P.chunk_col0[ch], nt = P.chunk_n[ch];
+      if (threadIdx.x < TC) {
+        const int t = threadIdx.x;
+        long long pos = 0, s0 = 0, q0 = 0;
+        double xc = 0.0;
+        if (t < nt) {
+          const int c = c0 + t;
+          pos = static_cast<long long>(c) * P.s_pad;
+          s0 = P.col_rowbase[c] - prow0;
+          q0 = static_cast<long long>(P.col_vec[c]) * P.s_pad;
+          xc = ld_cg(x + c);
+        }
+        m_pos[t] = pos; m_pos[TC + t] = s0; m_pos[2 * TC + t] = q0; m_x[t] = xc;
+      }
+      __syncthreads();
+      run_chunk<TC, false>(P, k, nt, psi, lam, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, nullptr, smem, cur,
+                           pri_m, dual_m);
+    }
+  }
+  PT_START
+  publish_residuals(P, it, pri_m, dual_m, smem + P.off_red);
+  PT_LAP(P, 5)
+}
+
+// Exact column stage: one column per CTA at a time, the reference's dense
+// projector with numpy's pairwise order (admm.py:183-186).
+__device__ void column_stage_exact(const DevProblem& P, int b, const double* x, int it, double* smem) {
+  const int tid = threadIdx.x;
+  const int sp = P.s_pad;
+  double* phi_s = smem + P.off_ex;   // internal order
+  double* lam_s = phi_s + sp;
+  double* psi_s = lam_s + sp;
+  double* kref = psi_s + sp;          // reference order
+  double* pnew = kref + sp;           // internal order
+  double* res_s = pnew + sp;          // [m_pad]
+  const double* psi = P.psi[b];
+  const double* lam = P.lam[b];
+  double* psi_n = P.psi[b ^ 1];
+  double* lam_n = P.lam[b ^ 1];
+  double pri_m = 0.0, dual_m = 0.0;
+  for (int c = blockIdx.x; c < P.n_cols; c += gridDim.x) {
+    const int owner = P.col_owner[c];
+    const int k = P.col_class[c];
+    const int S = P.class_s[k], m = P.class_m[k];
+    const double* gk = P.g_pool + P.class_g_off[k];
+    const double* pk = P.p_pool + P.class_p_off[k];
+    const double* rhs = P.rhs_pool + static_cast<size_t>(P.col_vec[c]) * P.m_pad;
+    const int* rp = P.ref_pos + static_cast<size_t>(owner) * sp;
+    const double xc = ld_cg(x + c);
+    for (int p = tid; p < S; p += kThreads) {
+      const size_t pos = static_cast<size_t>(c) * sp + p;
+      const double ps = ld_cg(psi + pos), lm = ld_cg(lam + pos);
+      const long long ir = P.contiguous ? P.col_rowbase[c] + p : P.col_irow[static_cast<size_t>(owner) * sp + p];
+      phi_s[p] = make_phi<true>(__dsub_rn(ps, lm), ld_cg(P.s_row + ir), xc);
+      lam_s[p] = lm;
+      psi_s[p] = ps;
+    }
+    __syncthreads();
+    for (int q = tid; q < S; q += kThreads) kref[q] = __dadd_rn(phi_s[rp[q]], lam_s[rp[q]]);
+    __syncthreads();
+    for (int i = tid; i < m; i += kThreads)
+      res_s[i] = __dsub_rn(rhs[i], pairwise_sum(ProdRow{gk + static_cast<size_t>(i) * S, kref}, 0, S));
+    __syncthreads();
+    for (int q = tid; q < S; q += kThreads)
+      pnew[rp[q]] = __dadd_rn(kref[q], pairwise_sum(ProdRow{pk + static_cast<size_t>(q) * m, res_s}, 0, m));
+    __syncthreads();
+    for (int p = tid; p < S; p += kThreads) {
+      const size_t pos = static_cast<size_t>(c) * sp + p;
+      const double pn = pnew[p];
+      const double d = __dsub_rn(phi_s[p], pn);
+      psi_n[pos] = pn;
+      lam_n[pos] = __dadd_rn(lam_s[p], d);
+      pri_m = fmax(pri_m, fabs(d));
+      dual_m = fmax(dual_m, fabs(__dsub_rn(pn, psi_s[p])));
+    }
+    __syncthreads();
+  }
+  publish_residuals(P, it, pri_m, dual_m, smem + P.off_red);
+}
+
+// u_k = ascending dot of φ_r[input row k, t=0] with x (admm.py:350-360);
+// φ is rebuilt from the iterate the last Φ stage read (buffer pb).
+template <bool EXACT>
+__device__ void control_stage(const DevProblem& P, int pb, const double* x) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, GT = gridDim.x * blockDim.x;
+  for (int k = gt; k < P.n_inputs; k += GT) {
+    const int i = P.input_owner[k], l = P.input_local[k];
+    const double s = ld_cg(P.s_row + P.row_start[i] + l);
+    const int D = P.supp_len[i];
+    const int* sc = P.supp_col + static_cast<size_t>(i) * P.d_pad;
+    const int* so = P.supp_off + static_cast<size_t>(i) * P.d_pad;
+    double acc = 0.0;
+    for (int q = 0; q < D; ++q) {
+      const int c = sc[q];
+      const size_t pos = static_cast<size_t>(c) * P.s_pad + so[q] + l;
+      const double xc = ld_cg(x + c);
+      const double phi = make_phi<EXACT>(__dsub_rn(ld_cg(P.psi[pb] + pos), ld_cg(P.lam[pb] + pos)), s, xc);
+      const double pr = __dmul_rn(phi, xc);
+      acc = q == 0 ? pr : __dadd_rn(acc, pr);
+    }
+    P.u[k] = acc;
+  }
+}
+
+// x+ = A x + B u on the plant's CSR rows (admm.py:363-369: scipy csr_matvec
+// accumulates from 0 in stored order without FMA, then the two vectors add).
+__device__ void plant_stage(const DevProblem& P, const double* x, double* xn) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, GT = gridDim.x * blockDim.x;
+  for (int r = gt; r < P.n_cols; r += GT) {
+    double ax = 0.0, bu = 0.0;
+    for (long long q = P.a_ptr[r]; q < P.a_ptr[r + 1]; ++q)
+      ax = __dadd_rn(ax, __dmul_rn(P.a_val[q], ld_cg(x + P.a_idx[q])));
+    for (long long q = P.b_ptr[r]; q < P.b_ptr[r + 1]; ++q)
+      bu = __dadd_rn(bu, __dmul_rn(P.b_val[q], ld_cg(P.u + P.b_idx[q])));
+    xn[r] = __dadd_rn(ax, bu);
+  }
+}
+
+__device__ void zero_iterate(const DevProblem& P, int b) {
+  const size_t n = static_cast<size_t>(P.n_cols) * P.s_pad;
+  const size_t gt = blockIdx.x * blockDim.x + threadIdx.x, GT = gridDim.x * blockDim.x;
+  for (size_t q = gt; q < n; q += GT) { P.psi[b][q] = 0.0; P.lam[b][q] = 0.0; }
+}
+
+enum Mode { kPatch = 0, kTwoPhase = 1, kExact = 2 };
+
+template <int TC, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, RunArgs R) {
+  constexpr bool EXACT = MODE == kExact;
+  extern __shared__ __align__(16) double smem[];
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x;
+  const bool leader = blockIdx.x == 0 && tid == 0;
+  int cur = -1;   // class whose operator is staged at smem offset 0
+  int b = P.ctl[4];
+  const size_t gt = blockIdx.x * blockDim.x + tid, GT = gridDim.x * blockDim.x;
+  for (int step = 0; step < R.t_sim; ++step) {
+    const double* x = P.x[R.closed_loop ? (step & 1) : 0];
+    int* bad_slot = P.ctl + 2 + (step & 1);
+    for (size_t q = gt; q < static_cast<size_t>(2 * R.max_iters); q += GT) P.resid[q] = 0ull;
+    if (R.closed_loop) {
+      row_data_stage(P, x, bad_slot);
+      if ((R.cold_start && step == 0) || !R.warm_start) zero_iterate(P, b);
+    }
+    grid.sync();
+    if (R.closed_loop) {
+      const int bad = *reinterpret_cast<volatile int*>(bad_slot);
+      if (bad != kBadNone) {
+        if (leader) { P.ctl[0] = 2; P.ctl[1] = step; P.ctl[5] = 0; P.ctl[4] = b; }
+        return;
+      }
+      if (leader) P.ctl[2 + ((step + 1) & 1)] = kBadNone;
+    }
+    if (MODE == kPatch && P.cache_phi) cache_phi_meta(P, x, smem);
+    int it = 0;
+    bool conv = false;
+    while (it < R.max_iters) {
+      PT_DECL
+      if (MODE == kPatch) {
+        patch_iteration<TC>(P, b, x, it, smem, cur);
+        PT_START
+      } else {
+        PT_START
+        phi_stage_global<EXACT>(P, b, x);
+        PT_LAP(P, 0)
+        grid.sync();
+        PT_LAP(P, 6)
+        if (EXACT) column_stage_exact(P, b, x, it, smem);
+        else column_stage_tiles<TC>(P, b, x, it, smem, cur);
+        PT_START
+      }
+      grid.sync();
+      PT_LAP(P, 6)
+      b ^= 1;
+      const double pri = __longlong_as_double(static_cast<long long>(__ldcg(P.resid + 2 * it)));
+      const double dual = P.rho * __longlong_as_double(static_cast<long long>(__ldcg(P.resid + 2 * it + 1)));
+      if (leader) { R.hist[2 * it] = pri; R.hist[2 * it + 1] = dual; }
+      ++it;
+      if (R.stop_on_conv && pri <= R.eps_pri && dual <= R.eps_dual) { conv = true; break; }
+    }
+    if (leader) R.step_iters[step] = it;
+    if (R.stop_on_conv && !conv) {
+      if (leader) { P.ctl[0] = 1; P.ctl[1] = step; P.ctl[5] = it; P.ctl[4] = b; }
+      return;
+    }
+    if (R.closed_loop) {
+      if (step == 0) {
+        for (size_t q = gt; q < static_cast<size_t>(P.n_cols); q += GT) R.states[q] = x[q];
+      }
+      control_stage<EXACT>(P, b ^ 1, x);
+      grid.sync();
+      double* xn = P.x[(step + 1) & 1];
+      plant_stage(P, x, xn);
+      for (size_t q = gt; q < static_cast<size_t>(P.n_cols); q += GT)
+        R.states[static_cast<size_t>(step + 1) * P.n_cols + q] = xn[q];
+      for (size_t q = gt; q < static_cast<size_t>(P.n_inputs); q += GT)
+        R.inputs[static_cast<size_t>(step) * P.n_inputs + q] = P.u[q];
+      grid.sync();
+    }
+  }
+  if (leader) { P.ctl[0] = 0; P.ctl[4] = b; }
+}
+
+// Row data for the solve API (dlmpc_set_x): a plain launch.
+__global__ void set_x_kernel(DevProblem P) { row_data_stage(P, P.x[0], P.ctl + 2); }
+
+// φ of the last iteration, internal column layout (for dlmpc_get(DLMPC_PHI)).
+template <bool EXACT>
+__global__ void phi_materialize_kernel(DevProblem P, int pb, double* out) {
+  const size_t n = static_cast<size_t>(P.n_cols) * P.s_pad;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
+    const int c = static_cast<int>(q / P.s_pad), p = static_cast<int>(q % P.s_pad);
+    double v = 0.0;
+    if (p < P.col_len[c]) {
+      const long long ir = P.contiguous ? P.col_rowbase[c] + p
+                                        : P.col_irow[static_cast<size_t>(P.col_owner[c]) * P.s_pad + p];
+      v = make_phi<EXACT>(__dsub_rn(P.psi[pb][q], P.lam[pb][q]), P.s_row[ir], P.x[0][c]);
+    }
+    out[q] = v;
+  }
+}
+
+}  // namespace dlmpc

@@ -14,7 +14,8 @@ import numpy as np
 
 from .errors import DeviceError, NotConverged, RowInfeasible
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdlmpc.so")
+_LIB_PATH = os.environ.get("DLMPC_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                          "libdlmpc.so")
 
 DLMPC_OK, DLMPC_NOT_CONVERGED, DLMPC_ROW_INFEASIBLE = 0, 1, 2
 DLMPC_BAD_ARGUMENT, DLMPC_CUDA_ERROR, DLMPC_NO_DEVICE = 3, 4, 5
@@ -31,9 +32,10 @@ class _Problem(C.Structure):
         ("rho", C.c_double),
         ("row_start", _i64p), ("ball_ptr", _i64p), ("ball_idx", _i32p), ("ball_off", _i32p),
         ("state_start", _i32p), ("state_count", _i32p), ("sub_first_bad", _i32p),
+        ("d_pad", C.c_int32), ("supp_col", _i32p), ("supp_off", _i32p), ("supp_len", _i32p),
         ("row_w", _f64p), ("row_lo", _f64p), ("row_hi", _f64p),
         ("col_owner", _i32p), ("col_len", _i32p), ("col_class", _i32p), ("col_vec", _i32p),
-        ("col_irow", _i32p),
+        ("col_irow", _i32p), ("col_rowbase", _i64p),
         ("n_classes", C.c_int32), ("class_s", _i32p), ("class_n0", _i32p), ("class_ldn", _i32p),
         ("class_null_off", _i64p), ("null_pool", _f64p),
         ("n_vec", C.c_int32), ("q_pool", _f64p),
@@ -51,7 +53,8 @@ class _Problem(C.Structure):
 EXPORTS = ("dlmpc_create", "dlmpc_destroy", "dlmpc_last_error", "dlmpc_global_error",
            "dlmpc_set_x", "dlmpc_solve", "dlmpc_iterate", "dlmpc_simulate",
            "dlmpc_simulate_device", "dlmpc_get", "dlmpc_put", "dlmpc_zero",
-           "dlmpc_last_timing", "dlmpc_stream", "dlmpc_synchronize", "dlmpc_info")
+           "dlmpc_last_timing", "dlmpc_stream", "dlmpc_synchronize", "dlmpc_info",
+           "dlmpc_phase_times")
 
 _lib = None
 
@@ -91,6 +94,7 @@ def load_library():
     lib.dlmpc_stream.restype = vp
     lib.dlmpc_synchronize.argtypes = [vp]
     lib.dlmpc_info.argtypes = [vp, _i64p]
+    lib.dlmpc_phase_times.argtypes = [vp, _P(C.c_uint64), C.c_int]
     _lib = lib
     return lib
 
@@ -129,7 +133,8 @@ class DeviceSession:
         p.state_start, p.state_count, p.sub_first_bad = i32("state_start"), i32("state_count"), i32("sub_first_bad")
         p.row_w, p.row_lo, p.row_hi = f64("row_w"), f64("row_lo"), f64("row_hi")
         p.col_owner, p.col_len, p.col_class, p.col_vec = i32("col_owner"), i32("col_len"), i32("col_class"), i32("col_vec")
-        p.col_irow = i32("col_irow")
+        p.col_irow, p.col_rowbase = i32("col_irow"), i64("col_rowbase")
+        p.d_pad, p.supp_col, p.supp_off, p.supp_len = L.d_pad, i32("supp_col"), i32("supp_off"), i32("supp_len")
         p.n_classes = L.n_classes
         p.class_s, p.class_n0, p.class_ldn = i32("class_s"), i32("class_n0"), i32("class_ldn")
         p.class_null_off, p.null_pool = i64("class_null_off"), f64("null_pool")
@@ -257,6 +262,14 @@ class DeviceSession:
         ms, n = C.c_float(0), C.c_int32(0)
         self._lib.dlmpc_last_timing(self._h, C.byref(ms), C.byref(n))
         return float(ms.value), int(n.value)
+
+    def phase_times(self, reset=True):
+        """Per-CTA per-phase ns (profiling build), shape (grid, 8)."""
+        g = self.info()["grid"]
+        out = np.zeros(8 * g, dtype=np.uint64)
+        self._check(self._lib.dlmpc_phase_times(self._h, out.ctypes.data_as(_P(C.c_uint64)), int(reset)),
+                    "dlmpc_phase_times")
+        return out.reshape(g, 8)
 
     def info(self):
         out = np.zeros(7, dtype=np.int64)

@@ -22,7 +22,7 @@ layouts every iteration (sls_core.py:352-472). The device keeps ONE copy:
   distinct (class, rhs); Ψ = q + N(Nᵀ k) is the reference projection
   k + P(rhs - g k) (admm.py:186) in exact arithmetic. The exact path stores
   the reference's own g, P (reference support order) and reduced rhs.
-* **Tiles**: columns sorted by class, cut into tiles of `tile_cols` (8/16/32)
+* **Tiles**: columns sorted by class, cut into tiles of `tile_cols` (8/16)
   columns; one CTA works a tile at a time.
 """
 
@@ -31,7 +31,7 @@ from __future__ import annotations
 import numpy as np
 
 from .sls_core import ColumnClasses, ProblemSpec
-from .system_model import LocalityMask, LtiSystem, phi_row_owners
+from .system_model import LocalityMask, LtiSystem
 
 SM_COUNT_B200 = 148
 
@@ -51,7 +51,7 @@ def _ld_frag(n):
 
 def choose_tile_cols(n_cols, sm_count=SM_COUNT_B200):
     """Largest tile that still gives every SM work; >= 8 (one MMA n-tile)."""
-    for tc in (32, 16):
+    for tc in (16,):
         if n_cols >= 2 * tc * sm_count:
             return tc
     return 8
@@ -61,19 +61,18 @@ class DeviceLayout:
     """All arrays of `dlmpc_problem` (include/dlmpc.h) plus the index maps
     between the internal layout and the reference's padded layouts."""
 
-    def __init__(self, system: LtiSystem, spec: ProblemSpec, mask: LocalityMask,
+    def __init__(self, system: LtiSystem | None, spec: ProblemSpec, mask: LocalityMask,
                  classes: ColumnClasses, exact: bool = False, tile_cols: int | None = None):
         if mask.compact is None:
             raise ValueError("the device layout needs a mask built by build_locality_mask")
         cm = mask.compact
-        part = system.partition
         t = int(spec.horizon)
         if cm["horizon"] != t:
             raise ValueError("mask horizon does not match the spec")
         self.exact = bool(exact)
         self.rho = float(spec.rho)
-        n_sub = part.subsystem_count
-        n_x, n_u = part.n_states, part.n_inputs
+        n_sub = int(cm["state_start"].size)
+        n_x, n_u = int(cm["n_x"]), int(cm["n_u"])
         self.n_sub, self.n_cols, self.n_inputs, self.horizon = n_sub, n_x, n_u, t
         s_cnt, u_cnt = cm["state_count"], cm["input_count"]
         rows_per = cm["rows_per_sub"]
@@ -81,7 +80,7 @@ class DeviceLayout:
         self.row_start = np.concatenate([[0], np.cumsum(rows_per)]).astype(np.int64)
 
         # internal <-> reference row order
-        owner_ref = phi_row_owners(part, t).astype(np.int64)
+        owner_ref = cm["row_owner"].astype(np.int64)
         self.int_to_ref = np.argsort(owner_ref, kind="stable").astype(np.int64)
         self.ref_to_int = np.empty_like(self.int_to_ref)
         self.ref_to_int[self.int_to_ref] = np.arange(self.n_rows)
@@ -114,6 +113,20 @@ class DeviceLayout:
         self.contiguous = bool(np.all(gaps[~row_bound[1:]] == 1)) if ball_idx.size > 1 else True
         self.state_start = cm["state_start"].astype(np.int32)
         self.state_count = s_cnt.astype(np.int32)
+        # row-support descriptor per subsystem: (column, block offset) pairs in
+        # ascending column order -- the reference's ascending_dot order.
+        cnt_e = s_cnt[ball_idx]
+        self.supp_len = np.add.reduceat(cnt_e, ball_ptr[:-1]).astype(np.int32)
+        self.d_pad = _round(int(self.supp_len.max()), 4)
+        e_rep = np.repeat(np.arange(ball_idx.size), cnt_e)
+        k_in_e = np.arange(e_rep.size) - np.repeat(np.cumsum(cnt_e) - cnt_e, cnt_e)
+        sub_of = src[e_rep]
+        first_of_sub = np.cumsum(np.r_[0, self.supp_len[:-1].astype(np.int64)])
+        slot = np.arange(e_rep.size) - first_of_sub[sub_of]
+        self.supp_col = np.zeros((n_sub, self.d_pad), dtype=np.int32)
+        self.supp_off = np.zeros((n_sub, self.d_pad), dtype=np.int32)
+        self.supp_col[sub_of, slot] = (cm["state_start"][ball_idx[e_rep]] + k_in_e).astype(np.int32)
+        self.supp_off[sub_of, slot] = self.ball_off[e_rep]
 
         # per-row costs and bounds, internal order
         w, lo, hi = spec.row_arrays()
@@ -135,6 +148,7 @@ class DeviceLayout:
         col_owner = cm["col_owner"].astype(np.int64)
         self.col_owner = col_owner.astype(np.int32)
         self.col_len = sup_len[col_owner].astype(np.int32)
+        self.col_rowbase = self.row_start[ball_idx[ball_ptr[:-1]]][col_owner].astype(np.int64)
 
         # reference slot -> internal slot, per subsystem
         rptr, rows = mask._rows_of()
@@ -237,12 +251,17 @@ class DeviceLayout:
         self.tile_count = np.array(tcount, dtype=np.int32)
         self.n_tiles = len(tcls)
 
-        # plant CSR (sorted, as scipy stores it)
-        a = system.a.tocsr(); a.sort_indices()
-        b = system.b.tocsr(); b.sort_indices()
+        # plant CSR (sorted, as scipy stores it); absent for solve-only sessions
+        if system is not None:
+            a = system.a.tocsr(); a.sort_indices()
+            b = system.b.tocsr(); b.sort_indices()
+        else:
+            import scipy.sparse as _sp
+            a, b = _sp.csr_matrix((n_x, n_x)), _sp.csr_matrix((n_x, max(n_u, 0)))
+        self.has_plant = system is not None
         self.a_ptr, self.a_idx, self.a_val = a.indptr.astype(np.int64), a.indices.astype(np.int32), a.data.astype(np.float64)
         self.b_ptr, self.b_idx, self.b_val = b.indptr.astype(np.int64), b.indices.astype(np.int32), b.data.astype(np.float64)
-        iown = part.input_owner().astype(np.int64)
+        iown = np.repeat(np.arange(n_sub, dtype=np.int64), cm["input_count"])
         self.input_owner = iown.astype(np.int32)
         self.input_local = (self.ref_to_int[n_x * t + np.arange(n_u)] - self.row_start[iown]).astype(np.int32) \
             if n_u else np.zeros(0, np.int32)

@@ -153,13 +153,17 @@ def row_index_map(partition: SubsystemPartition, horizon: int,
                                             w.tolist(), lo.tolist(), hi.tolist())]
 
 
-@dataclass(frozen=True)
 class DynamicsOperator:
-    """z @ response == rhs encodes x_0 = I and x_{t+1} = A x_t + B u_t."""
+    """z @ response == rhs encodes x_0 = I and x_{t+1} = A x_t + B u_t
+    (reference sls_core.py:164-190). `rhs` -- identity block on top, zeros
+    below, (n_states*horizon, n_cols) -- is materialised only on access: at
+    N = 10^4 the dense array alone would take 32 GB."""
 
-    z: sp.csr_matrix          # (n_states*horizon, n_rows)
-    rhs: np.ndarray           # (n_states*horizon, n_cols)
-    horizon: int
+    def __init__(self, z: sp.csr_matrix, horizon: int, n_cols: int):
+        self.z = z
+        self.horizon = int(horizon)
+        self._n_cols = int(n_cols)
+        self._rhs = None
 
     @property
     def n_rows(self) -> int:
@@ -167,7 +171,19 @@ class DynamicsOperator:
 
     @property
     def n_cols(self) -> int:
-        return self.rhs.shape[1]
+        return self._n_cols
+
+    @property
+    def rhs(self) -> np.ndarray:
+        if self._rhs is None:
+            r = np.zeros((self.z.shape[0], self._n_cols))
+            r[np.arange(self._n_cols), np.arange(self._n_cols)] = 1.0
+            self._rhs = r
+        return self._rhs
+
+    def rhs_entries(self, rows: np.ndarray, col: int) -> np.ndarray:
+        """rhs[rows, col] without materialising rhs."""
+        return (np.asarray(rows) == col).astype(np.float64)
 
     def residual(self, dense_response: np.ndarray) -> np.ndarray:
         return self.z @ dense_response - self.rhs
@@ -195,9 +211,7 @@ def build_dynamics_operator(system: LtiSystem, horizon: int) -> DynamicsOperator
         vals.append(-b.data.astype(np.float64))
     z = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
                       shape=(n_x * t, n_rows))
-    rhs = np.zeros((n_x * t, n_x))
-    rhs[np.arange(n_x), np.arange(n_x)] = 1.0
-    return DynamicsOperator(z, rhs, t)
+    return DynamicsOperator(z, t, n_x)
 
 
 @dataclass(frozen=True)
@@ -232,26 +246,50 @@ class ColumnClass:
 
 
 class ColumnClasses:
-    """Columns grouped into operator classes, plus per-column rhs data.
+    """Columns grouped into operator classes, plus the per-column reduced rhs.
 
-    Attributes: `classes` (list of ColumnClass), `col_class` (n_cols,) class
-    id per column, `rhs` (list per column of the reduced rhs vector),
-    `particular` (list per column of P @ rhs), `touch` (per column, absolute
-    operator rows touched), `keep_rows` (per column, absolute kept rows).
+    `classes[k]` is a ColumnClass (None for a class whose reduction failed),
+    `col_class[c]` the class of column c, `rhs[c]` the reduced right-hand side
+    (the reference's ColumnPrecomp.rhs), `touch[c]` the operator rows touched.
     """
 
-    def __init__(self, classes, col_class, rhs0, touch):
+    def __init__(self, classes, col_class, rhs, touch=None):
         self.classes = classes
-        self.col_class = col_class
-        self.rhs0 = rhs0
+        self.col_class = np.asarray(col_class, dtype=np.int64)
+        self.rhs = rhs
         self.touch = touch
 
     def reduced_rhs(self, c):
-        return self.rhs0[c][self.classes[self.col_class[c]].keep]
+        return self.rhs[c]
 
     def particular(self, c):
-        cl = self.classes[self.col_class[c]]
-        return cl.projector @ self.reduced_rhs(c)
+        return self.classes[self.col_class[c]].projector @ self.rhs[c]
+
+    @classmethod
+    def from_precomps(cls, col_solvers):
+        """Classes recovered from a plain list of ColumnPrecomp (bit-identical
+        `g` and `projector` -> one class)."""
+        key_to_class, classes, col_class = {}, [], []
+        for pre in col_solvers:
+            g = np.ascontiguousarray(pre.g)
+            pj = np.ascontiguousarray(pre.projector)
+            key = hashlib.blake2b(np.asarray(g.shape, np.int64).tobytes() + g.tobytes() + pj.tobytes(),
+                                  digest_size=16).digest()
+            if key not in key_to_class:
+                key_to_class[key] = len(classes)
+                null = sla.null_space(g) if g.shape[1] > g.shape[0] else np.zeros((g.shape[1], 0))
+                classes.append(ColumnClass(touch_rel=None, g0=g, keep=np.arange(g.shape[0]), g=g,
+                                           projector=pj, null=np.ascontiguousarray(null),
+                                           columns=None))
+            col_class.append(key_to_class[key])
+        return cls(classes, col_class, [np.asarray(p.rhs, dtype=np.float64) for p in col_solvers])
+
+
+class ColumnSolverList(list):
+    """`precompute_column_solvers` result: the reference's per-column list,
+    carrying the class table the device path uploads (`.classes`)."""
+
+    classes: "ColumnClasses"
 
 
 def _support_sets(mask: LocalityMask):
@@ -284,9 +322,12 @@ def build_column_classes(op: DynamicsOperator, mask: LocalityMask) -> ColumnClas
     # one restricted operator per support set
     g0_of, touch_of = [], []
     for s in sups:
-        sub = z_csc[:, s]
-        touch = np.unique(sub.tocoo().row)
-        g0_of.append(np.ascontiguousarray(sub.toarray()[touch]))
+        sub = z_csc[:, s].tocoo()
+        touch = np.unique(sub.row)
+        g0 = np.zeros((touch.size, len(s)))
+        # same values the reference reads from sub.toarray()[touch] (no duplicates in z)
+        g0[np.searchsorted(touch, sub.row), sub.col] = sub.data
+        g0_of.append(g0)
         touch_of.append(touch)
     # bit-identical g0 -> one class
     key_to_class, set_class = {}, np.empty(len(sups), dtype=np.int64)
@@ -310,7 +351,7 @@ def build_column_classes(op: DynamicsOperator, mask: LocalityMask) -> ColumnClas
         rank = int(np.count_nonzero(diag > tol))
         if rank == 0:
             c0 = int(members[0])
-            rhs0 = op.rhs[touch_of[owners[c0]], c0]
+            rhs0 = op.rhs_entries(touch_of[owners[c0]], c0)
             failing.append((c0, float(np.max(np.abs(rhs0), initial=0.0))))
             classes.append(None)
             continue
@@ -321,24 +362,28 @@ def build_column_classes(op: DynamicsOperator, mask: LocalityMask) -> ColumnClas
         classes.append(ColumnClass(touch_rel=None, g0=g0, keep=keep, g=g,
                                    projector=projector, null=np.ascontiguousarray(null),
                                    columns=members))
-    rhs0 = [None] * n_cols
+    rhs = [None] * n_cols
     touch = [None] * n_cols
+    checked = {}   # (class, rhs0 bytes) -> residual: the check depends on nothing else
     for c in range(n_cols):
         tch = touch_of[owners[c]]
         touch[c] = tch
-        rhs0[c] = op.rhs[tch, c]
+        rhs0 = op.rhs_entries(tch, c)
         cl = classes[col_class[c]]
         if cl is None:
             continue
-        rhs = rhs0[c][cl.keep]
-        particular = cl.projector @ rhs
-        resid = float(np.max(np.abs(cl.g0 @ particular - rhs0[c])))
-        if resid > CONSISTENCY_TOL * max(1.0, float(np.max(np.abs(rhs0[c]), initial=0.0))):
+        rhs[c] = rhs0[cl.keep]
+        key = (int(col_class[c]), rhs0.tobytes())
+        if key not in checked:
+            particular = cl.projector @ rhs[c]
+            checked[key] = float(np.max(np.abs(cl.g0 @ particular - rhs0)))
+        resid = checked[key]
+        if resid > CONSISTENCY_TOL * max(1.0, float(np.max(np.abs(rhs0), initial=0.0))):
             failing.append((c, resid))
     if failing:
         c, res = min(failing)
         raise LocalityInfeasible(c, res)
-    return ColumnClasses(classes, col_class, rhs0, touch)
+    return ColumnClasses(classes, col_class, rhs, touch)
 
 
 def precompute_column_solvers(op: DynamicsOperator, mask: LocalityMask, classes=None):
@@ -348,11 +393,12 @@ def precompute_column_solvers(op: DynamicsOperator, mask: LocalityMask, classes=
     `projector` arrays (read-only views of one factorisation)."""
     cc = classes if classes is not None else build_column_classes(op, mask)
     owners, sups = _support_sets(mask)
-    out = []
+    out = ColumnSolverList()
     for c in range(mask.n_cols):
         cl = cc.classes[cc.col_class[c]]
         out.append(ColumnPrecomp(c, sups[owners[c]], cc.touch[c][cl.keep], cl.g,
-                                 cc.rhs0[c][cl.keep], cl.projector))
+                                 cc.rhs[c], cl.projector))
+    out.classes = cc
     return out
 
 

@@ -1,0 +1,22 @@
+"""Per-phase device time breakdown (profiling build of the library).
+usage: DLMPC_LIB=paper_2103_14990_b200/libdlmpc_timing.so python tools/phase_profile.py N [t_sim] [twophase]"""
+import os, sys
+sys.path.insert(0, '.')
+import numpy as np
+import paper_2103_14990_b200 as pb
+n = int(sys.argv[1]); t_sim = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+if len(sys.argv) > 3 and sys.argv[3] == "twophase":
+    os.environ["DLMPC_FORCE_TWOPHASE"] = "1"
+system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=n, d=3, horizon=10, t_sim=t_sim, seed=1))
+sess = pb.DlmpcSession(system, spec, mask, "b200")
+sess.simulate(x0, t_sim)
+sess.device.phase_times(reset=True)
+traj, ms = sess.simulate(x0, t_sim)
+it = sum(traj.step_iterations)
+pt = sess.device.phase_times(reset=True).astype(np.float64) / it / 1e3   # us per iteration per CTA
+names = ["phi", "prologue", "gemm1", "gemm2", "epilogue", "publish", "barrier", "-"]
+print(f"N={n} {sess.device.info()} iters {it} device {ms:.3f} ms = {1e3*ms/it:.2f} us/iter")
+for k, nm in enumerate(names[:7]):
+    col = pt[:, k]
+    print(f"  {nm:9s} max {col.max():7.2f} us  mean {col.mean():7.2f} us  min {col.min():7.2f}")
+print(f"  sum(max) {pt[:, :7].max(axis=0).sum():.2f}  per-CTA total max {pt[:, :7].sum(axis=1).max():.2f}")
