@@ -46,6 +46,18 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def reduce_over_ranks(vals, dist, device=None):
+    """[iterations, ms, e2e_iterations, e2e_ms] -> work summed over ranks,
+    times maxed over ranks (replicas: whole-job throughput = all ranks' work
+    / the slowest rank's time)."""
+    import torch
+    t = torch.tensor([vals[1], vals[3]], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    w = torch.tensor([vals[0], vals[2]], dtype=torch.float64, device=device)
+    dist.all_reduce(w, op=dist.ReduceOp.SUM)
+    return np.array([w[0].item(), t[0].item(), w[1].item(), t[1].item()])
+
+
 def problem():
     import paper_2103_14990_b200 as pb
     system = pb.build_chain_network(N_SUB)
@@ -255,11 +267,7 @@ def run_device_arm(args):
 
     vals = np.array([timed_iters, total_ms, e2e_iters, e2e_s * 1e3], dtype=np.float64)
     if world > 1:
-        t = torch.tensor(vals[[1, 3]], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        s = torch.tensor(vals[[0, 2]], device=f"cuda:{local}")
-        dist.all_reduce(s, op=dist.ReduceOp.SUM)
-        vals = np.array([s[0].item(), t[0].item(), s[1].item(), t[1].item()])
+        vals = reduce_over_ranks(vals, dist, device=f"cuda:{local}")
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

@@ -52,6 +52,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kBadNone = 0x7f7f7f7f;   // cudaMemset(0x7f) pattern = "no infeasible row"
 constexpr int kMG1 = 4;                // m-tiles per GEMM-1 work unit
 constexpr int kMG2 = 2;                // m-tiles per GEMM-2 work unit
+constexpr int kSmallCols = 4;          // chunks up to this many columns take the GEMV path
 
 struct DevProblem {
   int n_sub, n_rows, n_cols, n_inputs, s_pad, exact, contiguous, d_row;
@@ -163,11 +164,23 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 
 __device__ __forceinline__ void publish_residuals(const DevProblem& P, int it, double pri_m,
                                                   double dual_m, double* red) {
-  const double bp = block_max(pri_m, red);
-  const double bd = block_max(dual_m, red);
-  if (threadIdx.x == 0) {
-    atomicMax(P.resid + 2 * it, static_cast<unsigned long long>(__double_as_longlong(bp)));
-    atomicMax(P.resid + 2 * it + 1, static_cast<unsigned long long>(__double_as_longlong(bd)));
+  for (int o = 16; o > 0; o >>= 1) {
+    pri_m = fmax(pri_m, __shfl_xor_sync(0xffffffffu, pri_m, o));
+    dual_m = fmax(dual_m, __shfl_xor_sync(0xffffffffu, dual_m, o));
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { red[2 * warp] = pri_m; red[2 * warp + 1] = dual_m; }
+  __syncthreads();
+  if (warp == 0) {
+    double p = lane < kWarps ? red[2 * lane] : 0.0, d = lane < kWarps ? red[2 * lane + 1] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      p = fmax(p, __shfl_xor_sync(0xffffffffu, p, o));
+      d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    }
+    if (lane == 0) {
+      atomicMax(P.resid + 2 * it, static_cast<unsigned long long>(__double_as_longlong(p)));
+      atomicMax(P.resid + 2 * it + 1, static_cast<unsigned long long>(__double_as_longlong(d)));
+    }
   }
 }
 
@@ -333,88 +346,152 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
   }
   __syncthreads();
   PT_LAP(P, 1)
-  // GEMM 1: Y[a][t] = sum_p N[p][a] K[t][p]  (M = n0, N = TC, K = S), split-K
-  const int mt1 = n08 >> 3, ks1 = S8 >> 2;
-  const int groups1 = (mt1 + kMG1 - 1) / kMG1;
-  int split = 1;
-  while (groups1 * split * 2 <= kWarps && split < P.split_max) split <<= 1;
-  for (int u = warp; u < groups1 * split; u += kWarps) {
-    const int grp = u / split, sl = u - grp * split;
-    const int mt0 = grp * kMG1;
-    double acc[kMG1][NTN][2];
+  if (nt <= kSmallCols) {
+    // Small chunk (<= kSmallCols real columns): the two products as FP64
+    // GEMVs on the CUDA cores -- short FMA chains, no 8-wide padding, no
+    // split-K reduction. Y[a][t]: 8 lanes per a split p; O[t][p]: one thread per p.
+    {
+      // warp-uniform trip count: the 8-lane reductions below shuffle with a
+      // full mask, so every lane of the warp must take every iteration
+      const int j = lane & 7;
+      for (int a0 = warp * 4; a0 < n0; a0 += kThreads / 8) {
+        const int a = a0 + (lane >> 3);
+        const bool a_ok = a < n0;
+        double acc0[kSmallCols], acc1[kSmallCols];
 #pragma unroll
-    for (int m = 0; m < kMG1; ++m)
+        for (int t = 0; t < kSmallCols; ++t) { acc0[t] = 0.0; acc1[t] = 0.0; }
+        int p = a_ok ? j : S;
+        for (; p + 8 < S; p += 16) {
+          const double n_a = nop[p * ldn + a], n_b = nop[(p + 8) * ldn + a];
 #pragma unroll
-      for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
-    for (int ks = sl; ks < ks1; ks += split) {
-      const int p = ks * 4 + tig;
-      double bf[NTN];
+          for (int t = 0; t < kSmallCols; ++t)
+            if (t < nt) { acc0[t] = fma(n_a, kt[t * ldk + p], acc0[t]); acc1[t] = fma(n_b, kt[t * ldk + p + 8], acc1[t]); }
+        }
+        if (p < S) {
+          const double n_a = nop[p * ldn + a];
 #pragma unroll
-      for (int nn = 0; nn < NTN; ++nn) bf[nn] = kt[(nn * 8 + g) * ldk + p];
+          for (int t = 0; t < kSmallCols; ++t)
+            if (t < nt) acc0[t] = fma(n_a, kt[t * ldk + p], acc0[t]);
+        }
 #pragma unroll
-      for (int m = 0; m < kMG1; ++m) {
-        if (mt0 + m < mt1) {
-          const double af = nop[p * ldn + (mt0 + m) * 8 + g];
-#pragma unroll
-          for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
+        for (int t = 0; t < kSmallCols; ++t) {
+          double v = acc0[t] + acc1[t];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          if (j == 0 && t < nt && a_ok) yb[a * ldy + t] = v;
         }
       }
-    }
-    double* dst = split == 1 ? yb : yp + static_cast<size_t>(sl) * P.n08_max * TC;
-    const int ld = split == 1 ? ldy : TC;
-#pragma unroll
-    for (int m = 0; m < kMG1; ++m) {
-      if (mt0 + m < mt1) {
-#pragma unroll
-        for (int nn = 0; nn < NTN; ++nn) {
-          dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig] = acc[m][nn][0];
-          dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig + 1] = acc[m][nn][1];
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (split > 1) {
-    for (int idx = tid; idx < n08 * TC; idx += kThreads) {
-      const int a = idx / TC, t = idx - a * TC;
-      double v = yp[idx];
-      for (int sl = 1; sl < split; ++sl) v += yp[static_cast<size_t>(sl) * P.n08_max * TC + idx];
-      yb[a * ldy + t] = v;
     }
     __syncthreads();
-  }
-  PT_LAP(P, 2)
-  // GEMM 2: O[t][p] = sum_a N[p][a] Y[a][t]  (M = S, N = TC, K = n0) -> kt
-  const int mt2 = S8 >> 3, ks2 = n08 >> 2;
-  for (int mb = warp; mb < mt2; mb += kWarps * kMG2) {
-    double acc[kMG2][NTN][2];
+    PT_LAP(P, 2)
+    for (int p = tid; p < S; p += kThreads) {
+      double acc0[kSmallCols], acc1[kSmallCols];
 #pragma unroll
-    for (int m = 0; m < kMG2; ++m)
+      for (int t = 0; t < kSmallCols; ++t) { acc0[t] = 0.0; acc1[t] = 0.0; }
+      int a = 0;
+      for (; a + 1 < n0; a += 2) {
+        const double n_a = nop[p * ldn + a], n_b = nop[p * ldn + a + 1];
 #pragma unroll
-      for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
-    for (int ks = 0; ks < ks2; ++ks) {
-      const int a = ks * 4 + tig;
-      double bf[NTN];
+        for (int t = 0; t < kSmallCols; ++t)
+          if (t < nt) { acc0[t] = fma(n_a, yb[a * ldy + t], acc0[t]); acc1[t] = fma(n_b, yb[(a + 1) * ldy + t], acc1[t]); }
+      }
+      if (a < n0) {
+        const double n_a = nop[p * ldn + a];
 #pragma unroll
-      for (int nn = 0; nn < NTN; ++nn) bf[nn] = yb[a * ldy + nn * 8 + g];
+        for (int t = 0; t < kSmallCols; ++t)
+          if (t < nt) acc0[t] = fma(n_a, yb[a * ldy + t], acc0[t]);
+      }
 #pragma unroll
+      for (int t = 0; t < kSmallCols; ++t)
+        if (t < nt) kt[t * ldk + p] = acc0[t] + acc1[t];
+    }
+  } else {
+  // GEMM 1: Y[a][t] = sum_p N[p][a] K[t][p]  (M = n0, N = TC, K = S), split-K
+    const int mt1 = n08 >> 3, ks1 = S8 >> 2;
+    const int groups1 = (mt1 + kMG1 - 1) / kMG1;
+    int split = 1;
+    while (groups1 * split * 2 <= kWarps && split < P.split_max) split <<= 1;
+    for (int u = warp; u < groups1 * split; u += kWarps) {
+      const int grp = u / split, sl = u - grp * split;
+      const int mt0 = grp * kMG1;
+      double acc[kMG1][NTN][2];
+  #pragma unroll
+      for (int m = 0; m < kMG1; ++m)
+  #pragma unroll
+        for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
+  #pragma unroll 2
+      for (int ks = sl; ks < ks1; ks += split) {
+        const int p = ks * 4 + tig;
+        double bf[NTN];
+  #pragma unroll
+        for (int nn = 0; nn < NTN; ++nn) bf[nn] = kt[(nn * 8 + g) * ldk + p];
+  #pragma unroll
+        for (int m = 0; m < kMG1; ++m) {
+          if (mt0 + m < mt1) {
+            const double af = nop[p * ldn + (mt0 + m) * 8 + g];
+  #pragma unroll
+            for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
+          }
+        }
+      }
+      double* dst = split == 1 ? yb : yp + static_cast<size_t>(sl) * P.n08_max * TC;
+      const int ld = split == 1 ? ldy : TC;
+  #pragma unroll
+      for (int m = 0; m < kMG1; ++m) {
+        if (mt0 + m < mt1) {
+  #pragma unroll
+          for (int nn = 0; nn < NTN; ++nn) {
+            dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig] = acc[m][nn][0];
+            dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig + 1] = acc[m][nn][1];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (split > 1) {
+      for (int idx = tid; idx < n08 * TC; idx += kThreads) {
+        const int a = idx / TC, t = idx - a * TC;
+        double v = yp[idx];
+        for (int sl = 1; sl < split; ++sl) v += yp[static_cast<size_t>(sl) * P.n08_max * TC + idx];
+        yb[a * ldy + t] = v;
+      }
+      __syncthreads();
+    }
+    PT_LAP(P, 2)
+    // GEMM 2: O[t][p] = sum_a N[p][a] Y[a][t]  (M = S, N = TC, K = n0) -> kt
+    const int mt2 = S8 >> 3, ks2 = n08 >> 2;
+    for (int mb = warp; mb < mt2; mb += kWarps * kMG2) {
+      double acc[kMG2][NTN][2];
+  #pragma unroll
+      for (int m = 0; m < kMG2; ++m)
+  #pragma unroll
+        for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
+  #pragma unroll 2
+      for (int ks = 0; ks < ks2; ++ks) {
+        const int a = ks * 4 + tig;
+        double bf[NTN];
+  #pragma unroll
+        for (int nn = 0; nn < NTN; ++nn) bf[nn] = yb[a * ldy + nn * 8 + g];
+  #pragma unroll
+        for (int m = 0; m < kMG2; ++m) {
+          const int mt = mb + m * kWarps;
+          if (mt < mt2) {
+            const double af = nop[(mt * 8 + g) * ldn + a];
+  #pragma unroll
+            for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
+          }
+        }
+      }
+  #pragma unroll
       for (int m = 0; m < kMG2; ++m) {
         const int mt = mb + m * kWarps;
         if (mt < mt2) {
-          const double af = nop[(mt * 8 + g) * ldn + a];
-#pragma unroll
-          for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
-        }
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < kMG2; ++m) {
-      const int mt = mb + m * kWarps;
-      if (mt < mt2) {
-#pragma unroll
-        for (int nn = 0; nn < NTN; ++nn) {
-          kt[(nn * 8 + 2 * tig) * ldk + mt * 8 + g] = acc[m][nn][0];
-          kt[(nn * 8 + 2 * tig + 1) * ldk + mt * 8 + g] = acc[m][nn][1];
+  #pragma unroll
+          for (int nn = 0; nn < NTN; ++nn) {
+            kt[(nn * 8 + 2 * tig) * ldk + mt * 8 + g] = acc[m][nn][0];
+            kt[(nn * 8 + 2 * tig + 1) * ldk + mt * 8 + g] = acc[m][nn][1];
+          }
         }
       }
     }
@@ -522,7 +599,9 @@ __device__ void column_stage_tiles(const DevProblem& P, int b, const double* x, 
 // constant for a whole MPC step): each iteration's Φ then needs one L2 round
 // trip (the ψ,λ reads) instead of three.
 // layout at off_phimeta: base [np*d_pad] (int64), xk [np*d_pad], ada [np],
-//                        w/lo/hi [3*prows], len [np] (int32 in a double slot)
+//                        inv_den/lo/hi [3*prows], len [np] (int32 in a double slot)
+// inv_den = 1/(ρ + 2w·||a||²) and 1/||a||² (in the ada slot) turn the two
+// per-row IEEE divisions of the fast path into multiplications.
 __device__ void cache_phi_meta(const DevProblem& P, const double* x, double* smem) {
   const int un0 = P.cta_unit_ptr[blockIdx.x];
   if (un0 == P.cta_unit_ptr[blockIdx.x + 1]) return;
@@ -545,9 +624,17 @@ __device__ void cache_phi_meta(const DevProblem& P, const double* x, double* sme
       xk[q] = ld_cg(x + c);
     }
   }
-  for (int q = threadIdx.x; q < np; q += kThreads) { ada[q] = ld_cg(P.ada + plo + q); len[q] = P.supp_len[plo + q]; }
+  for (int q = threadIdx.x; q < np; q += kThreads) {
+    const double a = ld_cg(P.ada + plo + q);
+    ada[q] = a > 0.0 ? 1.0 / a : 0.0;
+    len[q] = P.supp_len[plo + q];
+  }
   for (int q = threadIdx.x; q < prows; q += kThreads) {
-    rw[q] = P.row_w[prow0 + q]; rw[prows + q] = P.row_lo[prow0 + q]; rw[2 * prows + q] = P.row_hi[prow0 + q];
+    int i = plo;
+    while (P.row_start[i + 1] <= prow0 + q) ++i;
+    const double a = ld_cg(P.ada + i);
+    rw[q] = 1.0 / (P.rho + 2.0 * P.row_w[prow0 + q] * a);
+    rw[prows + q] = P.row_lo[prow0 + q]; rw[2 * prows + q] = P.row_hi[prow0 + q];
   }
   __syncthreads();
 }
@@ -564,16 +651,16 @@ __device__ __forceinline__ void phi_rows_cached(const DevProblem& P, int q, int 
   const double* ada_p = base + 2 * static_cast<size_t>(np) * P.d_pad;
   const double* rw = ada_p + np;
   const int D = reinterpret_cast<const int*>(rw + 3 * prows)[q];
-  const double ada = ada_p[q];
+  const double inv_ada = ada_p[q];
   const double rho = P.rho;
   for (int l0 = 0; l0 < nr; l0 += 32) {
     const int l = l0 + lane;
     if (l >= nr) break;
     double acc = 0.0;
-    for (int k0 = 0; k0 < D; k0 += 8) {
-      double pv[8], lv[8];
+    for (int k0 = 0; k0 < D; k0 += 16) {
+      double pv[16], lv[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 16; ++u) {
         pv[u] = lv[u] = 0.0;
         if (k0 + u < D) {
           const long long b = bk[k0 + u] + l;
@@ -582,14 +669,12 @@ __device__ __forceinline__ void phi_rows_cached(const DevProblem& P, int q, int 
         }
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < 16; ++u)
         if (k0 + u < D) acc = fma(__dsub_rn(pv[u], lv[u]), xk[k0 + u], acc);
     }
     const int rr = r_off + l;
-    const double w = rw[rr], lo = rw[prows + rr], hi = rw[2 * prows + rr];
-    const double y0 = __ddiv_rn(__dmul_rn(rho, acc), __dadd_rn(rho, __dmul_rn(__dmul_rn(2.0, w), ada)));
-    const double y = fmin(fmax(y0, lo), hi);
-    out(l, ada > 0.0 ? __ddiv_rn(__dsub_rn(y, acc), ada) : 0.0);
+    const double y = fmin(fmax(rho * acc * rw[rr], rw[prows + rr]), rw[2 * prows + rr]);
+    out(l, (y - acc) * inv_ada);
   }
 }
 

@@ -222,8 +222,10 @@ def test_n1000_step0_against_reference(variant):
 
 
 def test_patch_and_twophase_kernels_agree():
-    """The contiguous patch kernel and the generic two-phase kernel run the
-    same arithmetic per entry: identical iterates."""
+    """The contiguous patch kernel and the generic two-phase kernel agree:
+    identical iteration counts, iterates equal to rounding (the patch kernel
+    multiplies by per-step reciprocals and takes the GEMV path for small
+    chunks)."""
     system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=300, d=3, horizon=10, seed=4))
     a = pb.DlmpcSession(system, spec, mask, FAST)
     os.environ["DLMPC_FORCE_TWOPHASE"] = "1"
@@ -234,7 +236,7 @@ def test_patch_and_twophase_kernels_agree():
     ta, _ = a.simulate(x0, 3)
     tb, _ = b.simulate(x0, 3)
     assert ta.step_iterations == tb.step_iterations
-    assert np.array_equal(ta.states, tb.states)
+    assert rel_err(ta.states, tb.states) <= 1e-12
     a.close(); b.close()
 
 
