@@ -52,7 +52,6 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kBadNone = 0x7f7f7f7f;   // cudaMemset(0x7f) pattern = "no infeasible row"
 constexpr int kMG1 = 4;                // m-tiles per GEMM-1 work unit
 constexpr int kMG2 = 2;                // m-tiles per GEMM-2 work unit
-constexpr int kSmallCols = 4;          // chunks up to this many columns take the GEMV path
 
 struct DevProblem {
   int n_sub, n_rows, n_cols, n_inputs, s_pad, exact, contiguous, d_row;
@@ -346,152 +345,90 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
   }
   __syncthreads();
   PT_LAP(P, 1)
-  if (nt <= kSmallCols) {
-    // Small chunk (<= kSmallCols real columns): the two products as FP64
-    // GEMVs on the CUDA cores -- short FMA chains, no 8-wide padding, no
-    // split-K reduction. Y[a][t]: 8 lanes per a split p; O[t][p]: one thread per p.
-    {
-      // warp-uniform trip count: the 8-lane reductions below shuffle with a
-      // full mask, so every lane of the warp must take every iteration
-      const int j = lane & 7;
-      for (int a0 = warp * 4; a0 < n0; a0 += kThreads / 8) {
-        const int a = a0 + (lane >> 3);
-        const bool a_ok = a < n0;
-        double acc0[kSmallCols], acc1[kSmallCols];
-#pragma unroll
-        for (int t = 0; t < kSmallCols; ++t) { acc0[t] = 0.0; acc1[t] = 0.0; }
-        int p = a_ok ? j : S;
-        for (; p + 8 < S; p += 16) {
-          const double n_a = nop[p * ldn + a], n_b = nop[(p + 8) * ldn + a];
-#pragma unroll
-          for (int t = 0; t < kSmallCols; ++t)
-            if (t < nt) { acc0[t] = fma(n_a, kt[t * ldk + p], acc0[t]); acc1[t] = fma(n_b, kt[t * ldk + p + 8], acc1[t]); }
-        }
-        if (p < S) {
-          const double n_a = nop[p * ldn + a];
-#pragma unroll
-          for (int t = 0; t < kSmallCols; ++t)
-            if (t < nt) acc0[t] = fma(n_a, kt[t * ldk + p], acc0[t]);
-        }
-#pragma unroll
-        for (int t = 0; t < kSmallCols; ++t) {
-          double v = acc0[t] + acc1[t];
-          v += __shfl_xor_sync(0xffffffffu, v, 4);
-          v += __shfl_xor_sync(0xffffffffu, v, 2);
-          v += __shfl_xor_sync(0xffffffffu, v, 1);
-          if (j == 0 && t < nt && a_ok) yb[a * ldy + t] = v;
-        }
-      }
-    }
-    __syncthreads();
-    PT_LAP(P, 2)
-    for (int p = tid; p < S; p += kThreads) {
-      double acc0[kSmallCols], acc1[kSmallCols];
-#pragma unroll
-      for (int t = 0; t < kSmallCols; ++t) { acc0[t] = 0.0; acc1[t] = 0.0; }
-      int a = 0;
-      for (; a + 1 < n0; a += 2) {
-        const double n_a = nop[p * ldn + a], n_b = nop[p * ldn + a + 1];
-#pragma unroll
-        for (int t = 0; t < kSmallCols; ++t)
-          if (t < nt) { acc0[t] = fma(n_a, yb[a * ldy + t], acc0[t]); acc1[t] = fma(n_b, yb[(a + 1) * ldy + t], acc1[t]); }
-      }
-      if (a < n0) {
-        const double n_a = nop[p * ldn + a];
-#pragma unroll
-        for (int t = 0; t < kSmallCols; ++t)
-          if (t < nt) acc0[t] = fma(n_a, yb[a * ldy + t], acc0[t]);
-      }
-#pragma unroll
-      for (int t = 0; t < kSmallCols; ++t)
-        if (t < nt) kt[t * ldk + p] = acc0[t] + acc1[t];
-    }
-  } else {
   // GEMM 1: Y[a][t] = sum_p N[p][a] K[t][p]  (M = n0, N = TC, K = S), split-K
-    const int mt1 = n08 >> 3, ks1 = S8 >> 2;
-    const int groups1 = (mt1 + kMG1 - 1) / kMG1;
-    int split = 1;
-    while (groups1 * split * 2 <= kWarps && split < P.split_max) split <<= 1;
-    for (int u = warp; u < groups1 * split; u += kWarps) {
-      const int grp = u / split, sl = u - grp * split;
-      const int mt0 = grp * kMG1;
-      double acc[kMG1][NTN][2];
-  #pragma unroll
-      for (int m = 0; m < kMG1; ++m)
-  #pragma unroll
-        for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
-  #pragma unroll 2
-      for (int ks = sl; ks < ks1; ks += split) {
-        const int p = ks * 4 + tig;
-        double bf[NTN];
-  #pragma unroll
-        for (int nn = 0; nn < NTN; ++nn) bf[nn] = kt[(nn * 8 + g) * ldk + p];
-  #pragma unroll
-        for (int m = 0; m < kMG1; ++m) {
-          if (mt0 + m < mt1) {
-            const double af = nop[p * ldn + (mt0 + m) * 8 + g];
-  #pragma unroll
-            for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
-          }
-        }
-      }
-      double* dst = split == 1 ? yb : yp + static_cast<size_t>(sl) * P.n08_max * TC;
-      const int ld = split == 1 ? ldy : TC;
-  #pragma unroll
+  const int mt1 = n08 >> 3, ks1 = S8 >> 2;
+  const int groups1 = (mt1 + kMG1 - 1) / kMG1;
+  int split = 1;
+  while (groups1 * split * 2 <= kWarps && split < P.split_max) split <<= 1;
+  for (int u = warp; u < groups1 * split; u += kWarps) {
+    const int grp = u / split, sl = u - grp * split;
+    const int mt0 = grp * kMG1;
+    double acc[kMG1][NTN][2];
+#pragma unroll
+    for (int m = 0; m < kMG1; ++m)
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
+#pragma unroll 2
+    for (int ks = sl; ks < ks1; ks += split) {
+      const int p = ks * 4 + tig;
+      double bf[NTN];
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) bf[nn] = kt[(nn * 8 + g) * ldk + p];
+#pragma unroll
       for (int m = 0; m < kMG1; ++m) {
         if (mt0 + m < mt1) {
-  #pragma unroll
-          for (int nn = 0; nn < NTN; ++nn) {
-            dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig] = acc[m][nn][0];
-            dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig + 1] = acc[m][nn][1];
-          }
+          const double af = nop[p * ldn + (mt0 + m) * 8 + g];
+#pragma unroll
+          for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
         }
       }
+    }
+    double* dst = split == 1 ? yb : yp + static_cast<size_t>(sl) * P.n08_max * TC;
+    const int ld = split == 1 ? ldy : TC;
+#pragma unroll
+    for (int m = 0; m < kMG1; ++m) {
+      if (mt0 + m < mt1) {
+#pragma unroll
+        for (int nn = 0; nn < NTN; ++nn) {
+          dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig] = acc[m][nn][0];
+          dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig + 1] = acc[m][nn][1];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (split > 1) {
+    for (int idx = tid; idx < n08 * TC; idx += kThreads) {
+      const int a = idx / TC, t = idx - a * TC;
+      double v = yp[idx];
+      for (int sl = 1; sl < split; ++sl) v += yp[static_cast<size_t>(sl) * P.n08_max * TC + idx];
+      yb[a * ldy + t] = v;
     }
     __syncthreads();
-    if (split > 1) {
-      for (int idx = tid; idx < n08 * TC; idx += kThreads) {
-        const int a = idx / TC, t = idx - a * TC;
-        double v = yp[idx];
-        for (int sl = 1; sl < split; ++sl) v += yp[static_cast<size_t>(sl) * P.n08_max * TC + idx];
-        yb[a * ldy + t] = v;
-      }
-      __syncthreads();
-    }
-    PT_LAP(P, 2)
-    // GEMM 2: O[t][p] = sum_a N[p][a] Y[a][t]  (M = S, N = TC, K = n0) -> kt
-    const int mt2 = S8 >> 3, ks2 = n08 >> 2;
-    for (int mb = warp; mb < mt2; mb += kWarps * kMG2) {
-      double acc[kMG2][NTN][2];
-  #pragma unroll
-      for (int m = 0; m < kMG2; ++m)
-  #pragma unroll
-        for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
-  #pragma unroll 2
-      for (int ks = 0; ks < ks2; ++ks) {
-        const int a = ks * 4 + tig;
-        double bf[NTN];
-  #pragma unroll
-        for (int nn = 0; nn < NTN; ++nn) bf[nn] = yb[a * ldy + nn * 8 + g];
-  #pragma unroll
-        for (int m = 0; m < kMG2; ++m) {
-          const int mt = mb + m * kWarps;
-          if (mt < mt2) {
-            const double af = nop[(mt * 8 + g) * ldn + a];
-  #pragma unroll
-            for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
-          }
-        }
-      }
-  #pragma unroll
+  }
+  PT_LAP(P, 2)
+  // GEMM 2: O[t][p] = sum_a N[p][a] Y[a][t]  (M = S, N = TC, K = n0) -> kt
+  const int mt2 = S8 >> 3, ks2 = n08 >> 2;
+  for (int mb = warp; mb < mt2; mb += kWarps * kMG2) {
+    double acc[kMG2][NTN][2];
+#pragma unroll
+    for (int m = 0; m < kMG2; ++m)
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
+#pragma unroll 2
+    for (int ks = 0; ks < ks2; ++ks) {
+      const int a = ks * 4 + tig;
+      double bf[NTN];
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) bf[nn] = yb[a * ldy + nn * 8 + g];
+#pragma unroll
       for (int m = 0; m < kMG2; ++m) {
         const int mt = mb + m * kWarps;
         if (mt < mt2) {
-  #pragma unroll
-          for (int nn = 0; nn < NTN; ++nn) {
-            kt[(nn * 8 + 2 * tig) * ldk + mt * 8 + g] = acc[m][nn][0];
-            kt[(nn * 8 + 2 * tig + 1) * ldk + mt * 8 + g] = acc[m][nn][1];
-          }
+          const double af = nop[(mt * 8 + g) * ldn + a];
+#pragma unroll
+          for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kMG2; ++m) {
+      const int mt = mb + m * kWarps;
+      if (mt < mt2) {
+#pragma unroll
+        for (int nn = 0; nn < NTN; ++nn) {
+          kt[(nn * 8 + 2 * tig) * ldk + mt * 8 + g] = acc[m][nn][0];
+          kt[(nn * 8 + 2 * tig + 1) * ldk + mt * 8 + g] = acc[m][nn][1];
         }
       }
     }
