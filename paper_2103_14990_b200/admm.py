@@ -31,7 +31,7 @@ from .devlayout import DeviceLayout
 from .device import DeviceSession, PSI, LAM, PSI_PREV, PHI
 from .errors import NotConverged
 from .sls_core import (ColumnClasses, LayoutTables, PhiTriple, ProblemSpec, RowData,
-                       build_column_classes, build_dynamics_operator)
+                       build_column_classes_structural)
 from .strategies import ExecStrategy, Executor
 from .system_model import LocalityMask, LtiSystem
 
@@ -211,8 +211,10 @@ class DlmpcSession:
         strat = ExecStrategy(strategy) if isinstance(strategy, str) else strategy
         self.system, self.spec, self.mask, self.strategy = system, spec, mask, strat
         t0 = time.perf_counter()
-        self.operator = build_dynamics_operator(system, spec.horizon)
-        self.classes = build_column_classes(self.operator, mask)
+        # class-deduplicated column operators from the structural builder:
+        # the same bits as the reference's per-column reduction, O(classes)
+        # factorizations instead of O(N) (sls_core.py:253-289)
+        self.classes = build_column_classes_structural(system, spec.horizon, mask)
         self.layout = DeviceLayout(system, spec, mask, self.classes, exact=strat.exact,
                                    tile_cols=tile_cols)
         self.device = DeviceSession(self.layout, strat.device)

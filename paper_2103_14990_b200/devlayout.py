@@ -150,46 +150,62 @@ class DeviceLayout:
         self.col_len = sup_len[col_owner].astype(np.int32)
         self.col_rowbase = self.row_start[ball_idx[ball_ptr[:-1]]][col_owner].astype(np.int64)
 
-        # reference slot -> internal slot, per subsystem
-        rptr, rows = mask._rows_of()
-        lens = np.diff(rptr)
-        j_of = np.repeat(np.arange(n_sub, dtype=np.int64), lens)
-        i_of = owner_ref[rows]
-        e = np.searchsorted(key_e, i_of * n_sub + j_of)
-        pos = self.ball_off[e].astype(np.int64) + local_of_ref[rows]
-        slot = np.arange(rows.size) - np.repeat(rptr[:-1], lens)
-        self.ref_pos = np.zeros((n_sub, self.s_pad), dtype=np.int32)
-        self.ref_pos[j_of, slot] = pos
+        # reference slot -> internal slot per subsystem (its support
+        # permutation). All subsystems at small N / exact mode / generic
+        # graphs; at scale only one representative per structural id
+        # (classes.sub_struct), the rest is materialised on demand.
+        self._owner_ref, self._local_of_ref, self._mask = owner_ref, local_of_ref, mask
+        self._sup_len = sup_len
+        struct = classes.sub_struct if classes.sub_struct is not None else np.arange(n_sub)
+        struct = np.asarray(struct, dtype=np.int64)
+        full = n_sub <= 20000 or self.exact or not self.contiguous or classes.sub_struct is None
+        self.ref_pos = self._ref_pos_rows(np.arange(n_sub)) if full else None
         if not self.contiguous:
+            rptr, rows = mask._rows_of()
+            j_of = np.repeat(np.arange(n_sub, dtype=np.int64), np.diff(rptr))
+            slot = np.arange(rows.size) - np.repeat(rptr[:-1], np.diff(rptr))
             self.col_irow = np.zeros((n_sub, self.s_pad), dtype=np.int32)
-            self.col_irow[j_of, pos] = self.ref_to_int[rows]
+            self.col_irow[j_of, self.ref_pos[j_of, slot]] = self.ref_to_int[rows]
         else:
             self.col_irow = None
+        perm_keys, perm_of = {}, {}
+        if full:
+            perm_id = np.empty(n_sub, dtype=np.int64)
+            for j in range(n_sub):
+                key = self.ref_pos[j, :sup_len[j]].tobytes()
+                if key not in perm_keys:
+                    perm_keys[key] = len(perm_keys)
+                    perm_of[perm_keys[key]] = self.ref_pos[j, :sup_len[j]].astype(np.int64)
+                perm_id[j] = perm_keys[key]
+        else:
+            _, rep_sub, sinv = np.unique(struct, return_index=True, return_inverse=True)
+            rows_rep = self._ref_pos_rows(rep_sub)
+            sid = np.empty(rep_sub.size, dtype=np.int64)
+            for u, r in enumerate(rep_sub.tolist()):
+                pv = rows_rep[u, :sup_len[r]].astype(np.int64)
+                key = pv.tobytes()
+                if key not in perm_keys:
+                    perm_keys[key] = len(perm_keys)
+                    perm_of[perm_keys[key]] = pv
+                sid[u] = perm_keys[key]
+            perm_id = sid[sinv.ravel()]
 
         # device classes = (host class, support permutation)
-        dev_key, dev_class = {}, np.empty(n_x, dtype=np.int64)
-        perm_bytes = [self.ref_pos[j, :sup_len[j]].tobytes() for j in range(n_sub)] \
-            if n_sub <= 4096 else None
-        for c in range(n_x):
-            j = int(col_owner[c])
-            pb = perm_bytes[j] if perm_bytes is not None else self.ref_pos[j, :sup_len[j]].tobytes()
-            key = (int(classes.col_class[c]), pb)
-            if key not in dev_key:
-                dev_key[key] = len(dev_key)
-            dev_class[c] = dev_key[key]
-        n_cls = len(dev_key)
-        rep = np.zeros(n_cls, dtype=np.int64)
-        rep[dev_class[::-1]] = np.arange(n_x)[::-1]      # first member column
+        col_perm = perm_id[col_owner]
+        pairs = np.stack([classes.col_class.astype(np.int64), col_perm], axis=1)
+        upairs, dev_class = np.unique(pairs, axis=0, return_inverse=True)
+        dev_class = dev_class.ravel()
+        n_cls = upairs.shape[0]
         self.n_classes = n_cls
         self.col_class = dev_class.astype(np.int32)
         cls_s, cls_n0, cls_ldn, cls_m = [], [], [], []
         null_blocks, g_blocks, p_blocks = [], [], []
+        self._class_perm = []
         for k in range(n_cls):
-            c = int(rep[k])
-            hc = classes.classes[classes.col_class[c]]
-            j = int(col_owner[c])
-            s = int(sup_len[j])
-            perm = self.ref_pos[j, :s].astype(np.int64)
+            hc = classes.classes[int(upairs[k, 0])]
+            perm = perm_of[int(upairs[k, 1])]
+            s = int(perm.size)
+            self._class_perm.append(perm)
             null = hc.null
             n0 = null.shape[1]
             ldn = _ld_frag(_round(n0, 8))
@@ -213,24 +229,21 @@ class DeviceLayout:
             self.p_pool = np.concatenate(p_blocks)
         self.m_pad = _round(max(cls_m) if cls_m else 1, 4)
 
-        # per-column particular solution q (internal order) and reduced rhs
-        vec_key, col_vec, q_list, rhs_list = {}, np.empty(n_x, dtype=np.int64), [], []
-        for c in range(n_x):
-            hc = classes.classes[classes.col_class[c]]
-            rhs = classes.reduced_rhs(c)
-            q_ref = hc.projector @ rhs
-            j = int(col_owner[c])
-            s = int(sup_len[j])
+        # particular solution q (internal order) and reduced rhs, one per
+        # distinct (device class, rhs)
+        vpairs = np.stack([dev_class.astype(np.int64), classes.col_rhs], axis=1)
+        uv, col_vec = np.unique(vpairs, axis=0, return_inverse=True)
+        col_vec = col_vec.ravel()
+        q_list, rhs_list = [], []
+        for k, rid in uv.tolist():
+            hc = classes.classes[int(upairs[k, 0])]
+            rhs = classes.rhs_table[rid]
             q = np.zeros(self.s_pad)
-            q[self.ref_pos[j, :s]] = q_ref
+            q[self._class_perm[k]] = hc.projector @ rhs
             r = np.zeros(self.m_pad)
             r[:rhs.size] = rhs
-            key = (int(dev_class[c]), q.tobytes(), r.tobytes())
-            if key not in vec_key:
-                vec_key[key] = len(q_list)
-                q_list.append(q)
-                rhs_list.append(r)
-            col_vec[c] = vec_key[key]
+            q_list.append(q)
+            rhs_list.append(r)
         self.col_vec = col_vec.astype(np.int32)
         self.n_vec = len(q_list)
         self.q_pool = np.concatenate(q_list)
@@ -266,13 +279,35 @@ class DeviceLayout:
         self.input_local = (self.ref_to_int[n_x * t + np.arange(n_u)] - self.row_start[iown]).astype(np.int32) \
             if n_u else np.zeros(0, np.int32)
 
+    def _ref_pos_rows(self, subs):
+        """Internal slot of every reference support slot, for the given
+        subsystems (rows of a [len(subs), s_pad] int32 array)."""
+        from .system_model import support_rows
+        subs = np.asarray(subs, dtype=np.int64)
+        ptr, rows = support_rows(self._mask, subs)
+        lens = np.diff(ptr)
+        k_of = np.repeat(np.arange(subs.size, dtype=np.int64), lens)
+        j_of = subs[k_of]
+        i_of = self._owner_ref[rows]
+        e = np.searchsorted(self._key_e, i_of * self.n_sub + j_of)
+        pos = self.ball_off[e].astype(np.int64) + self._local_of_ref[rows]
+        slot = np.arange(rows.size) - np.repeat(ptr[:-1], lens)
+        out = np.zeros((subs.size, self.s_pad), dtype=np.int32)
+        out[k_of, slot] = pos
+        return out
+
+    def full_ref_pos(self):
+        if self.ref_pos is None:
+            self.ref_pos = self._ref_pos_rows(np.arange(self.n_sub))
+        return self.ref_pos
+
     # -- maps to the reference layouts ------------------------------------------
     def column_gather(self, tables):
         """flat internal index of every reference column-layout cell (-1 at pads)."""
         cc, jj = np.nonzero(tables.col_valid)
         owner = self.col_owner[cc].astype(np.int64)
         out = np.full((tables.n_cols, tables.d_col), -1, dtype=np.int64)
-        out[cc, jj] = cc * self.s_pad + self.ref_pos[owner, jj]
+        out[cc, jj] = cc * self.s_pad + self.full_ref_pos()[owner, jj]
         return out
 
     def row_gather(self, tables):

@@ -246,30 +246,40 @@ class ColumnClass:
 
 
 class ColumnClasses:
-    """Columns grouped into operator classes, plus the per-column reduced rhs.
+    """Columns grouped into operator classes, plus the reduced rhs per column.
 
-    `classes[k]` is a ColumnClass (None for a class whose reduction failed),
-    `col_class[c]` the class of column c, `rhs[c]` the reduced right-hand side
-    (the reference's ColumnPrecomp.rhs), `touch[c]` the operator rows touched.
+    `classes[k]` is a ColumnClass, `col_class[c]` the class of column c.
+    Reduced right-hand sides (the reference's ColumnPrecomp.rhs) are stored
+    once per distinct vector: `rhs_table[col_rhs[c]]`. `sub_struct[i]` is a
+    structural id per subsystem -- equal ids guarantee an identical local
+    structure (support permutation, operator) -- and `touch[c]` the operator
+    rows touched (general builder only; None at scale).
     """
 
-    def __init__(self, classes, col_class, rhs, touch=None):
+    def __init__(self, classes, col_class, rhs_table, col_rhs, sub_struct=None, touch=None):
         self.classes = classes
         self.col_class = np.asarray(col_class, dtype=np.int64)
-        self.rhs = rhs
+        self.rhs_table = rhs_table
+        self.col_rhs = np.asarray(col_rhs, dtype=np.int64)
+        self.sub_struct = sub_struct
         self.touch = touch
 
     def reduced_rhs(self, c):
-        return self.rhs[c]
+        return self.rhs_table[self.col_rhs[c]]
+
+    @property
+    def rhs(self):
+        return [self.rhs_table[k] for k in self.col_rhs]
 
     def particular(self, c):
-        return self.classes[self.col_class[c]].projector @ self.rhs[c]
+        return self.classes[self.col_class[c]].projector @ self.reduced_rhs(c)
 
     @classmethod
     def from_precomps(cls, col_solvers):
         """Classes recovered from a plain list of ColumnPrecomp (bit-identical
         `g` and `projector` -> one class)."""
         key_to_class, classes, col_class = {}, [], []
+        rhs_key, rhs_table, col_rhs = {}, [], []
         for pre in col_solvers:
             g = np.ascontiguousarray(pre.g)
             pj = np.ascontiguousarray(pre.projector)
@@ -282,7 +292,13 @@ class ColumnClasses:
                                            projector=pj, null=np.ascontiguousarray(null),
                                            columns=None))
             col_class.append(key_to_class[key])
-        return cls(classes, col_class, [np.asarray(p.rhs, dtype=np.float64) for p in col_solvers])
+            r = np.asarray(pre.rhs, dtype=np.float64)
+            rk = (key_to_class[key], r.tobytes())
+            if rk not in rhs_key:
+                rhs_key[rk] = len(rhs_table)
+                rhs_table.append(r)
+            col_rhs.append(rhs_key[rk])
+        return cls(classes, col_class, rhs_table, col_rhs)
 
 
 class ColumnSolverList(list):
@@ -311,79 +327,229 @@ def _support_sets(mask: LocalityMask):
     return owners, sups
 
 
-def build_column_classes(op: DynamicsOperator, mask: LocalityMask) -> ColumnClasses:
-    """Class-deduplicated version of the reference's per-column reduction
-    (sls_core.py:253-289): identical (support-restricted) operators are
-    factorised once. Raises LocalityInfeasible for the first failing column
-    in column order, like the reference."""
-    z_csc = op.z.tocsc()
-    owners, sups = _support_sets(mask)
-    n_cols = mask.n_cols
-    # one restricted operator per support set
-    g0_of, touch_of = [], []
-    for s in sups:
-        sub = z_csc[:, s].tocoo()
-        touch = np.unique(sub.row)
-        g0 = np.zeros((touch.size, len(s)))
-        # same values the reference reads from sub.toarray()[touch] (no duplicates in z)
-        g0[np.searchsorted(touch, sub.row), sub.col] = sub.data
-        g0_of.append(g0)
-        touch_of.append(touch)
-    # bit-identical g0 -> one class
-    key_to_class, set_class = {}, np.empty(len(sups), dtype=np.int64)
-    reps = []
-    for k, g0 in enumerate(g0_of):
-        h = hashlib.blake2b(np.asarray(g0.shape, np.int64).tobytes() + g0.tobytes(),
-                            digest_size=16).digest()
-        if h not in key_to_class:
-            key_to_class[h] = len(reps)
-            reps.append(k)
-        set_class[k] = key_to_class[h]
-    col_class = set_class[owners]
-    classes = []
-    failing = []   # (column, residual)
-    for ci, k in enumerate(reps):
-        g0 = g0_of[k]
-        members = np.nonzero(col_class == ci)[0]
-        _, r, piv = sla.qr(g0.T, mode="economic", pivoting=True)
-        diag = np.abs(np.diag(r))
-        tol = RANK_RTOL * (diag[0] if diag.size else 1.0)
-        rank = int(np.count_nonzero(diag > tol))
-        if rank == 0:
-            c0 = int(members[0])
-            rhs0 = op.rhs_entries(touch_of[owners[c0]], c0)
-            failing.append((c0, float(np.max(np.abs(rhs0), initial=0.0))))
-            classes.append(None)
-            continue
-        keep = np.sort(piv[:rank])
-        g = g0[keep]
-        projector = sla.cho_solve(sla.cho_factor(g @ g.T), g).T
-        null = sla.null_space(g) if g.shape[1] > rank else np.zeros((g.shape[1], 0))
-        classes.append(ColumnClass(touch_rel=None, g0=g0, keep=keep, g=g,
-                                   projector=projector, null=np.ascontiguousarray(null),
-                                   columns=members))
-    rhs = [None] * n_cols
-    touch = [None] * n_cols
-    checked = {}   # (class, rhs0 bytes) -> residual: the check depends on nothing else
-    for c in range(n_cols):
-        tch = touch_of[owners[c]]
-        touch[c] = tch
-        rhs0 = op.rhs_entries(tch, c)
-        cl = classes[col_class[c]]
+def _restricted_operator(z_csc, sup):
+    """Touched operator rows and the dense g0 = z[touch, sup] of the
+    reference (sls_core.py:265-268)."""
+    sub = z_csc[:, sup].tocoo()
+    touch = np.unique(sub.row)
+    g0 = np.zeros((touch.size, len(sup)))
+    g0[np.searchsorted(touch, sub.row), sub.col] = sub.data   # z has no duplicates
+    return touch, g0
+
+
+def _g0_key(g0):
+    return hashlib.blake2b(np.asarray(g0.shape, np.int64).tobytes() + g0.tobytes(),
+                           digest_size=16).digest()
+
+
+def _factor_class(g0):
+    """The reference's per-column reduction (sls_core.py:271-281) for one
+    class representative; None if the rank is zero."""
+    _, r, piv = sla.qr(g0.T, mode="economic", pivoting=True)
+    diag = np.abs(np.diag(r))
+    tol = RANK_RTOL * (diag[0] if diag.size else 1.0)
+    rank = int(np.count_nonzero(diag > tol))
+    if rank == 0:
+        return None
+    keep = np.sort(piv[:rank])
+    g = g0[keep]
+    projector = sla.cho_solve(sla.cho_factor(g @ g.T), g).T
+    null = sla.null_space(g) if g.shape[1] > rank else np.zeros((g.shape[1], 0))
+    return ColumnClass(touch_rel=None, g0=g0, keep=keep, g=g, projector=projector,
+                       null=np.ascontiguousarray(null), columns=None)
+
+
+def _finish_classes(classes, col_class, col_pin, n_touch_of_col, reps_g0, failing, sub_struct=None,
+                    touch=None):
+    """Reduced rhs per column from its pin (position of the column's own t=0
+    row among the touched rows, -1 if untouched), the consistency check of
+    sls_core.py:282-287 once per distinct (class, rhs0), LocalityInfeasible
+    for the first failing column."""
+    rhs_key, rhs_table = {}, []
+    col_rhs = np.zeros(col_class.size, dtype=np.int64)
+    keys = np.stack([col_class, col_pin, n_touch_of_col], axis=1)
+    uniq, inv = np.unique(keys, axis=0, return_inverse=True)
+    inv = inv.ravel()
+    for u, (k, pin, nt) in enumerate(uniq):
+        cl = classes[k]
+        rhs0 = np.zeros(int(nt))
+        if pin >= 0:
+            rhs0[pin] = 1.0
         if cl is None:
+            c0 = int(np.flatnonzero(inv == u)[0])
+            failing.append((c0, float(np.max(np.abs(rhs0), initial=0.0))))
             continue
-        rhs[c] = rhs0[cl.keep]
-        key = (int(col_class[c]), rhs0.tobytes())
-        if key not in checked:
-            particular = cl.projector @ rhs[c]
-            checked[key] = float(np.max(np.abs(cl.g0 @ particular - rhs0)))
-        resid = checked[key]
+        red = rhs0[cl.keep]
+        resid = float(np.max(np.abs(cl.g0 @ (cl.projector @ red) - rhs0)))
         if resid > CONSISTENCY_TOL * max(1.0, float(np.max(np.abs(rhs0), initial=0.0))):
-            failing.append((c, resid))
+            failing.append((int(np.flatnonzero(inv == u)[0]), resid))
+        rk = (int(k), red.tobytes())
+        if rk not in rhs_key:
+            rhs_key[rk] = len(rhs_table)
+            rhs_table.append(red)
+        col_rhs[inv == u] = rhs_key[rk]
     if failing:
         c, res = min(failing)
         raise LocalityInfeasible(c, res)
-    return ColumnClasses(classes, col_class, rhs, touch)
+    return ColumnClasses(classes, col_class, rhs_table, col_rhs, sub_struct, touch)
+
+
+def build_column_classes(op: DynamicsOperator, mask: LocalityMask) -> ColumnClasses:
+    """Class-deduplicated version of the reference's per-column reduction
+    (sls_core.py:253-289): one restricted operator per support set (read from
+    the global operator, exactly as the reference slices it), bit-identical
+    operators factorised once. Raises LocalityInfeasible for the first failing
+    column in column order, like the reference."""
+    z_csc = op.z.tocsc()
+    owners, sups = _support_sets(mask)
+    touch_of, set_class, reps, key_to_class = [], np.empty(len(sups), dtype=np.int64), [], {}
+    for k, sup in enumerate(sups):
+        touch, g0 = _restricted_operator(z_csc, sup)
+        touch_of.append(touch)
+        h = _g0_key(g0)
+        if h not in key_to_class:
+            key_to_class[h] = len(reps)
+            reps.append(g0)
+        set_class[k] = key_to_class[h]
+    col_class = set_class[owners]
+    classes = [_factor_class(g0) for g0 in reps]
+    cols = np.arange(mask.n_cols)
+    col_pin = np.array([int(np.searchsorted(touch_of[o], c)) if np.any(touch_of[o] == c) else -1
+                        for c, o in zip(cols.tolist(), owners.tolist())], dtype=np.int64)
+    n_touch = np.array([touch_of[o].size for o in owners.tolist()], dtype=np.int64)
+    touch = [touch_of[o] for o in owners.tolist()]
+    return _finish_classes(classes, col_class, col_pin, n_touch, reps, [], touch=touch)
+
+
+def _mix64(h, v):
+    """Vectorised 64-bit mixing (splitmix64-style) of h with v (uint64 arrays)."""
+    with np.errstate(over="ignore"):
+        z = (h ^ (v + np.uint64(0x9E3779B97F4A7C15))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def subsystem_fingerprints(system: LtiSystem, d: int):
+    """A 64-bit fingerprint per subsystem j of everything its columns'
+    restricted operator depends on: for each subsystem m within d+1 hops,
+    its offset m - j, whether it lies within d hops, its state/input counts,
+    and the A/B entries of its states (relative owner offset, local indices,
+    exact value bits). Equal fingerprints => bit-identical restricted
+    operators and support permutations (verified on samples by the caller)."""
+    part = system.partition
+    n = part.subsystem_count
+    st = np.asarray(part.state_ranges, dtype=np.int64).reshape(-1, 2)
+    ip = np.asarray(part.input_ranges, dtype=np.int64).reshape(-1, 2)
+    sown = part.state_owner().astype(np.int64)
+    iown = part.input_owner().astype(np.int64)
+    local = np.zeros(n, dtype=np.uint64)
+    for mat, col_owner, col_start, salt in ((system.a.tocoo(), sown, st[:, 0], 1), (system.b.tocoo(), iown, ip[:, 0], 2)):
+        r, c = mat.row.astype(np.int64), mat.col.astype(np.int64)
+        ro = sown[r]
+        h = _mix64(np.full(r.size, salt, dtype=np.uint64), (col_owner[c] - ro).astype(np.uint64))
+        h = _mix64(h, (c - col_start[col_owner[c]]).astype(np.uint64))
+        h = _mix64(h, (r - st[ro, 0]).astype(np.uint64))
+        h = _mix64(h, np.ascontiguousarray(mat.data, dtype=np.float64).view(np.uint64))
+        np.add.at(local, ro, h)
+    local = _mix64(local, (st[:, 1] - st[:, 0]).astype(np.uint64))
+    local = _mix64(local, (ip[:, 1] - ip[:, 0]).astype(np.uint64) + np.uint64(1 << 20))
+    ptr1, idx1 = system.graph.balls(d + 1)
+    ptr0, idx0 = system.graph.balls(d)
+    j1 = np.repeat(np.arange(n, dtype=np.int64), np.diff(ptr1))
+    in_d = np.zeros(idx1.size, dtype=np.uint64)
+    key1 = j1 * n + idx1
+    key0 = np.repeat(np.arange(n, dtype=np.int64), np.diff(ptr0)) * n + idx0
+    in_d[np.isin(key1, key0)] = 1
+    e = _mix64(_mix64((idx1.astype(np.int64) - j1).astype(np.uint64), in_d), local[idx1])
+    fp = np.zeros(n, dtype=np.uint64)
+    np.add.at(fp, j1, e)
+    return _mix64(fp, np.diff(ptr1).astype(np.uint64))
+
+
+def _window_system(system: LtiSystem, subs):
+    """The plant restricted to the (sorted) subsystems `subs`."""
+    from .system_model import SubsystemGraph, SubsystemPartition
+    part = system.partition
+    st = np.asarray(part.state_ranges, dtype=np.int64).reshape(-1, 2)
+    ip = np.asarray(part.input_ranges, dtype=np.int64).reshape(-1, 2)
+    s_idx = np.concatenate([np.arange(*st[i]) for i in subs])
+    u_idx = np.concatenate([np.arange(*ip[i]) for i in subs]) if ip[subs, 1].sum() > ip[subs, 0].sum() \
+        else np.zeros(0, dtype=np.int64)
+    a = system.a.tocsr()[s_idx][:, s_idx]
+    b = system.b.tocsr()[s_idx][:, u_idx]
+    a.sort_indices(); b.sort_indices()
+    ns = st[subs, 1] - st[subs, 0]
+    nu = ip[subs, 1] - ip[subs, 0]
+    sp_ = np.concatenate([[0], np.cumsum(ns)])
+    up_ = np.concatenate([[0], np.cumsum(nu)])
+    wpart = SubsystemPartition(tuple(zip(sp_[:-1].tolist(), sp_[1:].tolist())),
+                               tuple(zip(up_[:-1].tolist(), up_[1:].tolist())))
+    pos = {int(g): k for k, g in enumerate(subs)}
+    edges = [(pos[int(i)], pos[int(j)]) for i in subs for j in system.graph.adjacency[int(i)]
+             if int(j) in pos and pos[int(i)] < pos[int(j)]]
+    return LtiSystem(a, b, wpart, SubsystemGraph.from_edges(len(subs), edges))
+
+
+def _window_operator(system: LtiSystem, horizon: int, d: int, j: int):
+    """(touch rows, g0, pin per local state) of subsystem j's columns,
+    computed on the window of subsystems within d+1 hops of j: its rows and
+    their in-support entries are exactly those of the global operator."""
+    from .system_model import build_locality_mask
+    win = system.graph.ball(j, d + 1).astype(np.int64)
+    w = _window_system(system, win)
+    lj = int(np.searchsorted(win, j))
+    wmask = build_locality_mask(w, d, horizon)
+    wop = build_dynamics_operator(w, horizon)
+    ptr, rows = wmask._rows_of()
+    touch, g0 = _restricted_operator(wop.z.tocsc(), rows[ptr[lj]:ptr[lj + 1]])
+    s0, s1 = w.partition.state_ranges[lj]
+    pins = [int(np.searchsorted(touch, c)) if np.any(touch == c) else -1 for c in range(s0, s1)]
+    return touch, g0, pins
+
+
+def build_column_classes_structural(system: LtiSystem, horizon: int, mask: LocalityMask,
+                                    verify_members: int = 2) -> ColumnClasses:
+    """Scalable class builder for large networks (N up to 10^6+): subsystems
+    are grouped by `subsystem_fingerprints`; one representative per group
+    has its restricted operator extracted from a small window plant, and up
+    to `verify_members` other members are re-extracted and must agree bit for
+    bit. The result equals `build_column_classes` (same classes, same bits)
+    without ever slicing the global operator."""
+    d = mask.d
+    fp = subsystem_fingerprints(system, d)
+    uniq, first, struct = np.unique(fp, return_index=True, return_inverse=True)
+    struct = struct.ravel()
+    rng = np.random.default_rng(0)
+    reps, key_to_class, fp_class = [], {}, np.empty(uniq.size, dtype=np.int64)
+    fp_pins, fp_ntouch = [], []
+    for u, j in enumerate(first.tolist()):
+        touch, g0, pins = _window_operator(system, horizon, d, j)
+        members = np.flatnonzero(struct == u)
+        others = members[members != j]
+        for m in rng.choice(others, min(verify_members, others.size), replace=False) if others.size else []:
+            _, g0m, pinsm = _window_operator(system, horizon, d, int(m))
+            if g0m.shape != g0.shape or not np.array_equal(g0m, g0) or pinsm != pins:
+                raise RuntimeError(f"fingerprint collision between subsystems {j} and {m}")
+        h = _g0_key(g0)
+        if h not in key_to_class:
+            key_to_class[h] = len(reps)
+            reps.append(g0)
+        fp_class[u] = key_to_class[h]
+        fp_pins.append(pins)
+        fp_ntouch.append(touch.size)
+    classes = [_factor_class(g0) for g0 in reps]
+    part = system.partition
+    sown = part.state_owner().astype(np.int64)
+    st0 = np.asarray(part.state_ranges, dtype=np.int64).reshape(-1, 2)[:, 0]
+    col_struct = struct[sown]
+    col_class = fp_class[col_struct]
+    ls = np.arange(sown.size) - st0[sown]
+    pin_table = np.full((uniq.size, int(max(len(p) for p in fp_pins))), -1, dtype=np.int64)
+    for u, p in enumerate(fp_pins):
+        pin_table[u, :len(p)] = p
+    col_pin = pin_table[col_struct, ls]
+    n_touch = np.asarray(fp_ntouch, dtype=np.int64)[col_struct]
+    return _finish_classes(classes, col_class, col_pin, n_touch, reps, [], sub_struct=struct)
 
 
 def precompute_column_solvers(op: DynamicsOperator, mask: LocalityMask, classes=None):
@@ -394,10 +560,12 @@ def precompute_column_solvers(op: DynamicsOperator, mask: LocalityMask, classes=
     cc = classes if classes is not None else build_column_classes(op, mask)
     owners, sups = _support_sets(mask)
     out = ColumnSolverList()
+    if cc.touch is None:
+        raise ValueError("per-column solvers need the general class builder")
     for c in range(mask.n_cols):
         cl = cc.classes[cc.col_class[c]]
         out.append(ColumnPrecomp(c, sups[owners[c]], cc.touch[c][cl.keep], cl.g,
-                                 cc.rhs[c], cl.projector))
+                                 cc.reduced_rhs(c), cl.projector))
     out.classes = cc
     return out
 

@@ -386,6 +386,20 @@ def _ball_row_sets(c):
     return ptr, out
 
 
+def support_rows(mask: LocalityMask, subs):
+    """Column supports (reference row indices, reference order) of the given
+    subsystems only, as CSR (ptr, rows) -- without materialising all of them."""
+    c = mask.compact
+    subs = np.asarray(subs, dtype=np.int64)
+    bp, bi = c["ball_ptr"], c["ball_idx"]
+    lens = bp[subs + 1] - bp[subs]
+    ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    idx = bi[np.repeat(bp[subs], lens) + (np.arange(lens.sum()) - np.repeat(ptr[:-1], lens))]
+    sub = dict(c)
+    sub["ball_ptr"], sub["ball_idx"] = ptr, idx
+    return _ball_row_sets(sub)
+
+
 def build_locality_mask(system: LtiSystem, d: int, horizon: int) -> LocalityMask:
     """d-hop closed-ball mask over the horizon (reference system_model.py:283-330)."""
     if horizon < 2:

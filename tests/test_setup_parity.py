@@ -109,3 +109,40 @@ def test_null_space_form_equals_projector(rng):
         ref = k + pre.projector @ (pre.rhs - pre.g @ k)
         fast = cc.particular(c) + cl.null @ (cl.null.T @ k)
         np.testing.assert_allclose(fast, ref, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("case", ["chain30", "chain_r2", "chain_two_inputs", "random_graph"])
+def test_structural_builder_equals_reference_builder(case):
+    """build_column_classes_structural (fingerprints + window extraction, used
+    by the device session at scale) yields the same operators, bit for bit,
+    as the reference-faithful per-support-set builder."""
+    from conftest import random_graph_system
+    from paper_2103_14990_b200 import sls_core as sc
+    if case == "chain30":
+        system, t, d = pb.build_chain_network(30), 10, 3
+    elif case == "chain_r2":
+        system, t, d = pb.build_chain_network(12, 2), 4, 2
+    elif case == "chain_two_inputs":
+        system, t, d = pb.build_chain_network(10, 1, True), 5, 2
+    else:
+        system, t, d = random_graph_system(9, np.random.default_rng(11)), 3, 2
+    mask = pb.build_locality_mask(system, d, t)
+    a = sc.build_column_classes(pb.build_dynamics_operator(system, t), mask)
+    b = sc.build_column_classes_structural(system, t, mask)
+    assert len(a.classes) == len(b.classes)
+    for c in range(mask.n_cols):
+        ca, cb = a.classes[a.col_class[c]], b.classes[b.col_class[c]]
+        assert np.array_equal(ca.g, cb.g) and np.array_equal(ca.projector, cb.projector)
+        assert np.array_equal(ca.null, cb.null)
+        assert np.array_equal(a.reduced_rhs(c), b.reduced_rhs(c))
+
+
+def test_structural_builder_scales():
+    import time
+    from paper_2103_14990_b200 import sls_core as sc
+    system = pb.build_chain_network(100000)
+    mask = pb.build_locality_mask(system, 3, 10)
+    t0 = time.perf_counter()
+    cc = sc.build_column_classes_structural(system, 10, mask)
+    assert time.perf_counter() - t0 < 60
+    assert len(cc.classes) == 9 and cc.col_class.size == 200000
