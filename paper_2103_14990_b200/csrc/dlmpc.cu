@@ -165,6 +165,8 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
     }
     int tc = pr->tile_cols;
     if (h->mode == kPatch) tc = (pr->n_cols > 8LL * G) ? 16 : 8;
+    if (const char* e = getenv("DLMPC_TILE_COLS")) { const int v = atoi(e); if (v == 8 || v == 16) tc = v; }
+    const int tc0 = tc;   // tile width the chunks below are cut for
     // --- patch work units (class-aware CTA assignment) ----------------------
     std::vector<int> cta_ptr(G + 1, 0), u_lo, u_hi, p_lo, p_hi, u_chunk(1, 0), ch_cls, ch_c0, ch_n;
     long long prows_max = 0, np_max = 0;
@@ -264,6 +266,13 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       }
       const long long opr = total(opr_need, split_max, false) <= limit ? opr_need : 0;
       const bool cache = h->mode == kPatch && one_unit && total(opr, split_max, true) <= limit;
+      // cp.async staging buffers for chunk ψ,λ (patch mode): 2 if they fit, else 1, else none
+      const long long stash_one = 2LL * tc * ldk;
+      int stash_bufs = 0;
+      if (h->mode == kPatch) {
+        const long long base = total(opr, split_max, cache);
+        stash_bufs = base + 2 * stash_one + 2 <= limit ? 2 : (base + stash_one + 2 <= limit ? 1 : 0);
+      }
       long long off = (opr + 1) & ~1LL;
       P.opr_cap = (int)opr;
       P.s8_max = s8_max; P.n08_max = n08_max; P.ldk = ldk; P.ldy = ldy; P.split_max = split_max;
@@ -276,13 +285,16 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       P.patch_cap = (int)prows_max;
       P.off_phimeta = (int)off; off += cache ? meta_phi : 0;
       P.cache_phi = cache ? 1 : 0;
+      off = (off + 1) & ~1LL;   // 16-byte alignment for cp.async
+      P.off_stash = (int)off; off += stash_bufs * stash_one;
+      P.stash_bufs = stash_bufs;
       P.off_ex = (int)off;
       h->smem_bytes = (int)(off * 8);
       P.tile_cols = tc;
       break;
     }
     // chunks were cut for the initial tile width; re-cut if it shrank
-    if (h->mode == kPatch && P.tile_cols != ((pr->n_cols > 8LL * G) ? 16 : 8)) {
+    if (h->mode == kPatch && P.tile_cols != tc0) {
       std::vector<int> nc_cls, nc_c0, nc_n, nu(1, 0);
       for (size_t u = 0; u + 1 < u_chunk.size(); ++u) {
         for (int ch = u_chunk[u]; ch < u_chunk[u + 1]; ++ch)

@@ -88,6 +88,7 @@ struct DevProblem {
   int opr_cap;                 // doubles of the per-CTA operator region at smem offset 0
   int s8_max, n08_max, ldk, ldy, split_max, patch_cap, cache_phi;
   int off_k, off_y, off_yp, off_red, off_meta, off_patch, off_phimeta, off_ex;
+  int off_stash, stash_bufs;   // cp.async staging of chunk ψ,λ: [bufs][TC][2][ldk]
 };
 
 struct RunArgs {
@@ -105,6 +106,30 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" :: "r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" :: "n"(N) : "memory"); }
+
+// Stage ψ,λ of nt consecutive columns starting at c0 into `st`
+// ([t][ψ|λ][ldk]) with 16-byte cp.async copies (bypassing L1, like ld.cg);
+// commits one group. s_pad is a multiple of 4, so sources are 16-B aligned.
+__device__ __forceinline__ void stash_issue(const DevProblem& P, int c0, int nt, int S, const double* psi,
+                                            const double* lam, double* st) {
+  const int pairs = (S + 1) >> 1;
+  const int total = nt * 2 * pairs;
+  for (int q = threadIdx.x; q < total; q += blockDim.x) {
+    const int t = q / (2 * pairs), r = q - t * 2 * pairs;
+    const int arr = r >= pairs, pr = r - arr * pairs;
+    const double* src = (arr ? lam : psi) + static_cast<size_t>(c0 + t) * P.s_pad + 2 * pr;
+    cp_async16(st + (2 * t + arr) * P.ldk + 2 * pr, src);
+  }
+  cp_async_commit();
+}
 
 template <bool EXACT>
 __device__ __forceinline__ double make_phi(double v, double s, double xc) {
@@ -291,7 +316,7 @@ __device__ void phi_stage_global(const DevProblem& P, int b, const double* x) {
 template <int TC, bool S_GLOBAL, bool OPS>
 __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi, const double* lam,
                            double* psi_n, double* lam_n, const double* s_src, const int* irow_tab,
-                           double* smem, double& pri_m, double& dual_m) {
+                           double* smem, double& pri_m, double& dual_m, const double* st) {
   constexpr int NTN = TC / 8;
   constexpr int WPC = kWarps / TC;   // warps per column in the element loops
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -327,8 +352,13 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
         const int p = pb + u * PSTEP;
         ps[u] = lm[u] = sr[u] = 0.0;
         if (col_ok && p < S) {
-          ps[u] = ld_cg(psi + pos0 + p);
-          lm[u] = ld_cg(lam + pos0 + p);
+          if (st) {
+            ps[u] = st[(2 * t) * ldk + p];
+            lm[u] = st[(2 * t + 1) * ldk + p];
+          } else {
+            ps[u] = ld_cg(psi + pos0 + p);
+            lm[u] = ld_cg(lam + pos0 + p);
+          }
           sr[u] = !S_GLOBAL ? s_src[s0 + p] : ld_cg(s_src + (irow_tab ? irow_tab[s0 + p] : s0 + p));
         }
       }
@@ -345,56 +375,81 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
   }
   __syncthreads();
   PT_LAP(P, 1)
-  // GEMM 1: Y[a][t] = sum_p N[p][a] K[t][p]  (M = n0, N = TC, K = S), split-K
+  // GEMM 1: Y[a][t] = sum_p N[p][a] K[t][p]  (M = n0, N = TC, K = S)
   const int mt1 = n08 >> 3, ks1 = S8 >> 2;
-  const int groups1 = (mt1 + kMG1 - 1) / kMG1;
-  int split = 1;
-  while (groups1 * split * 2 <= kWarps && split < P.split_max) split <<= 1;
-  for (int u = warp; u < groups1 * split; u += kWarps) {
-    const int grp = u / split, sl = u - grp * split;
-    const int mt0 = grp * kMG1;
-    double acc[kMG1][NTN][2];
+  if (mt1 * NTN >= 12) {
+    // enough (m, n) tiles to keep the DMMA pipe busy: one tile per warp over
+    // the full K with two interleaved accumulator chains, no split-K pass
+    for (int u = warp; u < mt1 * NTN; u += kWarps) {
+      const int mt = u / NTN, nn = u - (u / NTN) * NTN;
+      double c0a = 0.0, c1a = 0.0, c0b = 0.0, c1b = 0.0;
+      int ks = 0;
+      for (; ks + 1 < ks1; ks += 2) {
+        const int p0 = ks * 4 + tig, p1 = p0 + 4;
+        const double a0 = nop[p0 * ldn + mt * 8 + g], b0 = kt[(nn * 8 + g) * ldk + p0];
+        const double a1 = nop[p1 * ldn + mt * 8 + g], b1 = kt[(nn * 8 + g) * ldk + p1];
+        dmma(c0a, c1a, a0, b0);
+        dmma(c0b, c1b, a1, b1);
+      }
+      if (ks < ks1) {
+        const int p0 = ks * 4 + tig;
+        dmma(c0a, c1a, nop[p0 * ldn + mt * 8 + g], kt[(nn * 8 + g) * ldk + p0]);
+      }
+      yb[(mt * 8 + g) * ldy + nn * 8 + 2 * tig] = c0a + c0b;
+      yb[(mt * 8 + g) * ldy + nn * 8 + 2 * tig + 1] = c1a + c1b;
+    }
+    __syncthreads();
+  } else {
+    const int mt1 = n08 >> 3, ks1 = S8 >> 2;
+    const int groups1 = (mt1 + kMG1 - 1) / kMG1;
+    int split = 1;
+    while (groups1 * split * 2 <= kWarps && split < P.split_max) split <<= 1;
+    for (int u = warp; u < groups1 * split; u += kWarps) {
+      const int grp = u / split, sl = u - grp * split;
+      const int mt0 = grp * kMG1;
+      double acc[kMG1][NTN][2];
 #pragma unroll
-    for (int m = 0; m < kMG1; ++m)
+      for (int m = 0; m < kMG1; ++m)
 #pragma unroll
-      for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
+        for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
 #pragma unroll 2
-    for (int ks = sl; ks < ks1; ks += split) {
-      const int p = ks * 4 + tig;
-      double bf[NTN];
+      for (int ks = sl; ks < ks1; ks += split) {
+        const int p = ks * 4 + tig;
+        double bf[NTN];
 #pragma unroll
-      for (int nn = 0; nn < NTN; ++nn) bf[nn] = kt[(nn * 8 + g) * ldk + p];
+        for (int nn = 0; nn < NTN; ++nn) bf[nn] = kt[(nn * 8 + g) * ldk + p];
+#pragma unroll
+        for (int m = 0; m < kMG1; ++m) {
+          if (mt0 + m < mt1) {
+            const double af = nop[p * ldn + (mt0 + m) * 8 + g];
+#pragma unroll
+            for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
+          }
+        }
+      }
+      double* dst = split == 1 ? yb : yp + static_cast<size_t>(sl) * P.n08_max * TC;
+      const int ld = split == 1 ? ldy : TC;
 #pragma unroll
       for (int m = 0; m < kMG1; ++m) {
         if (mt0 + m < mt1) {
-          const double af = nop[p * ldn + (mt0 + m) * 8 + g];
 #pragma unroll
-          for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
+          for (int nn = 0; nn < NTN; ++nn) {
+            dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig] = acc[m][nn][0];
+            dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig + 1] = acc[m][nn][1];
+          }
         }
       }
-    }
-    double* dst = split == 1 ? yb : yp + static_cast<size_t>(sl) * P.n08_max * TC;
-    const int ld = split == 1 ? ldy : TC;
-#pragma unroll
-    for (int m = 0; m < kMG1; ++m) {
-      if (mt0 + m < mt1) {
-#pragma unroll
-        for (int nn = 0; nn < NTN; ++nn) {
-          dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig] = acc[m][nn][0];
-          dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig + 1] = acc[m][nn][1];
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (split > 1) {
-    for (int idx = tid; idx < n08 * TC; idx += kThreads) {
-      const int a = idx / TC, t = idx - a * TC;
-      double v = yp[idx];
-      for (int sl = 1; sl < split; ++sl) v += yp[static_cast<size_t>(sl) * P.n08_max * TC + idx];
-      yb[a * ldy + t] = v;
     }
     __syncthreads();
+    if (split > 1) {
+      for (int idx = tid; idx < n08 * TC; idx += kThreads) {
+        const int a = idx / TC, t = idx - a * TC;
+        double v = yp[idx];
+        for (int sl = 1; sl < split; ++sl) v += yp[static_cast<size_t>(sl) * P.n08_max * TC + idx];
+        yb[a * ldy + t] = v;
+      }
+      __syncthreads();
+    }
   }
   PT_LAP(P, 2)
   // GEMM 2: O[t][p] = sum_a N[p][a] Y[a][t]  (M = S, N = TC, K = n0) -> kt
@@ -448,8 +503,13 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
           const int p = pb + u * PSTEP;
           ps[u] = lm[u] = sr[u] = qv[u] = 0.0;
           if (p < S) {
-            ps[u] = ld_cg(psi + pos0 + p);
-            lm[u] = ld_cg(lam + pos0 + p);
+            if (st) {
+              ps[u] = st[(2 * t) * ldk + p];
+              lm[u] = st[(2 * t + 1) * ldk + p];
+            } else {
+              ps[u] = ld_cg(psi + pos0 + p);
+              lm[u] = ld_cg(lam + pos0 + p);
+            }
             sr[u] = !S_GLOBAL ? s_src[s0 + p] : ld_cg(s_src + (irow_tab ? irow_tab[s0 + p] : s0 + p));
             qv[u] = P.q_pool[q0 + p];
           }
@@ -495,11 +555,12 @@ template <int TC, bool S_GLOBAL>
 __device__ __forceinline__ void run_chunk(const DevProblem& P, int k, int nt, const double* psi,
                                           const double* lam, double* psi_n, double* lam_n,
                                           const double* s_src, const int* irow_tab, double* smem,
-                                          int& cur, double& pri_m, double& dual_m) {
+                                          int& cur, double& pri_m, double& dual_m,
+                                          const double* st = nullptr) {
   if (stage_operator(P, k, smem, cur))
-    fast_chunk<TC, S_GLOBAL, true>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m);
+    fast_chunk<TC, S_GLOBAL, true>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st);
   else
-    fast_chunk<TC, S_GLOBAL, false>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m);
+    fast_chunk<TC, S_GLOBAL, false>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st);
 }
 
 // Column stage of the two-phase fast kernel (class-sorted tiles, generic graphs).
@@ -633,6 +694,12 @@ __device__ void patch_iteration(const DevProblem& P, int b, const double* x, int
     const int plo = P.unit_patch_lo[un], phi_ = P.unit_patch_hi[un];
     const long long prow0 = P.row_start[plo];
     const int prows = static_cast<int>(P.row_start[phi_] - prow0);
+    // first chunk's ψ,λ start streaming into shared memory under the Φ stage
+    const int ch_a = P.unit_chunk_ptr[un], ch_b = P.unit_chunk_ptr[un + 1];
+    double* stash = smem + P.off_stash;
+    const int stash_stride = 2 * TC * P.ldk;
+    if (P.stash_bufs > 0 && ch_a < ch_b)
+      stash_issue(P, P.chunk_col0[ch_a], P.chunk_n[ch_a], P.class_s[P.chunk_class[ch_a]], psi, lam, stash);
     // Φ scale of every row the unit's columns touch (own rows + d-hop halo)
     for (int i = plo + warp; i < phi_; i += kWarps) {
       const int r_off = static_cast<int>(P.row_start[i] - prow0);
@@ -650,8 +717,18 @@ __device__ void patch_iteration(const DevProblem& P, int b, const double* x, int
     }
     __syncthreads();
     PT_LAP(P, 0)
-    for (int ch = P.unit_chunk_ptr[un]; ch < P.unit_chunk_ptr[un + 1]; ++ch) {
+    // chunk pipeline: ψ,λ of chunk i+1 stream into the other staging buffer
+    // (cp.async) while chunk i runs its GEMMs
+    for (int ch = ch_a; ch < ch_b; ++ch) {
       const int k = P.chunk_class[ch], c0 = P.chunk_col0[ch], nt = P.chunk_n[ch];
+      const int sb = P.stash_bufs == 2 ? ((ch - ch_a) & 1) : 0;
+      if (P.stash_bufs == 2 && ch + 1 < ch_b) {
+        stash_issue(P, P.chunk_col0[ch + 1], P.chunk_n[ch + 1], P.class_s[P.chunk_class[ch + 1]], psi, lam,
+                    stash + (sb ^ 1) * stash_stride);
+        cp_async_wait<1>();
+      } else if (P.stash_bufs > 0) {
+        cp_async_wait<0>();
+      }
       if (threadIdx.x < TC) {
         const int t = threadIdx.x;
         long long pos = 0, s0 = 0, q0 = 0;
@@ -667,7 +744,9 @@ __device__ void patch_iteration(const DevProblem& P, int b, const double* x, int
       }
       __syncthreads();
       run_chunk<TC, false>(P, k, nt, psi, lam, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, nullptr, smem, cur,
-                           pri_m, dual_m);
+                           pri_m, dual_m, P.stash_bufs > 0 ? stash + sb * stash_stride : nullptr);
+      if (P.stash_bufs == 1 && ch + 1 < ch_b)   // single buffer: refill after the chunk is done
+        stash_issue(P, P.chunk_col0[ch + 1], P.chunk_n[ch + 1], P.class_s[P.chunk_class[ch + 1]], psi, lam, stash);
     }
   }
   PT_START
