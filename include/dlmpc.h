@@ -123,6 +123,15 @@ typedef struct dlmpc_problem {
   const int64_t* b_ptr; const int32_t* b_idx; const double* b_val;   /* n_cols rows  */
   const int32_t* input_owner;    /* [n_inputs] */
   const int32_t* input_local;    /* [n_inputs] local row index of input k at t=0 */
+  /* audit (optional, NULL disables dlmpc_audit): per class the touched-rows
+   * operator g0 [ntouch x s] in reference support order and the support
+   * permutation (reference slot -> internal slot); per column the rhs0 pin */
+  const int32_t* class_ntouch;
+  const int64_t* class_g0_off;   /* [n_classes+1] */
+  const double* g0_pool;
+  const int64_t* class_perm_off; /* [n_classes+1] */
+  const int32_t* perm_pool;
+  const int32_t* col_pin;        /* [n_cols] row of rhs0 = 1 among the touched rows, -1 if none */
 } dlmpc_problem;
 
 typedef struct dlmpc_handle dlmpc_handle;
@@ -165,6 +174,13 @@ int dlmpc_simulate_device(dlmpc_handle* h, const double* x0_dev, int t_sim, int 
                           int cold_start, int max_iters, double eps_pri, double eps_dual,
                           double* states_dev, double* inputs_dev, int* step_iters_dev,
                           int* status_dev);
+
+/* Fixed-point audit of the current iterate (reference verify_fixed_point,
+ * admm.py:417-434): out[0] dynamics residual max|g0 ψ - rhs0|, out[1]
+ * re-solve residual max|Φ(current duals) - φ|, out[2] consensus gap
+ * max|φ - ψ|. φ is the last iteration's (phi_host == NULL) or a caller's
+ * φ in internal layout. Needs the audit tables of dlmpc_problem. */
+int dlmpc_audit(dlmpc_handle* h, const double* phi_host, double* out3);
 
 /* Copy an internal-layout array to/from host memory. */
 int dlmpc_get(dlmpc_handle* h, int which, double* dst);

@@ -29,7 +29,7 @@ import numpy as np
 
 from .devlayout import DeviceLayout
 from .device import DeviceSession, PSI, LAM, PSI_PREV, PHI
-from .errors import NotConverged
+from .errors import NotConverged, RowInfeasible
 from .sls_core import (ColumnClasses, LayoutTables, PhiTriple, ProblemSpec, RowData,
                        build_column_classes_structural)
 from .strategies import ExecStrategy, Executor
@@ -61,8 +61,29 @@ def closed_loop_cost(traj: Trajectory) -> float:
 
 
 def _classes_of(col_solvers) -> ColumnClasses:
+    if isinstance(col_solvers, ColumnClasses):
+        return col_solvers
     cc = getattr(col_solvers, "classes", None)
     return cc if cc is not None else ColumnClasses.from_precomps(col_solvers)
+
+
+@dataclass
+class FixedPointReport:
+    """Residuals of an independent audit of a solve (reference admm.py:386-414)."""
+
+    dynamics_residual: float
+    resolve_residual: float
+    consensus_gap: float
+    threshold: float
+
+    @property
+    def passed(self) -> bool:
+        return (self.dynamics_residual <= self.threshold and self.resolve_residual <= self.threshold
+                and self.consensus_gap <= self.threshold)
+
+    def as_dict(self):
+        return {"dynamics_residual": self.dynamics_residual, "resolve_residual": self.resolve_residual,
+                "consensus_gap": self.consensus_gap, "threshold": self.threshold, "passed": self.passed}
 
 
 def _x_of(row_data: RowData, tables: LayoutTables) -> np.ndarray:
@@ -183,9 +204,30 @@ def admm_solve(row_data: RowData, col_solvers, triple: PhiTriple, spec: ProblemS
     n, history, ok = workspace.device_solve(strat, spec.max_iters, spec.eps_pri, spec.eps_dual)
     if executor is not None:
         executor.ledger.record_launch(n, workspace.last_device_ms)
+    triple._dlmpc_ws = (workspace, strat)
     if not ok:
         raise NotConverged(history)
     return AdmmState(triple, n, history, True)
+
+
+def verify_fixed_point(triple: PhiTriple, row_data: RowData, operator, spec: ProblemSpec) -> FixedPointReport:
+    """Audit a solve without trusting the iteration that produced it
+    (reference admm.py:417-434), on the device: the dynamics residual of the
+    projected iterate through each column's restricted operator, the change
+    of a fresh row solve at the final dual point, and the consensus gap; all
+    within 10 x eps_pri for an accepted solve. The triple's arrays (including
+    its φ) are what is audited."""
+    from .sls_core import build_column_classes
+    ws, strat = getattr(triple, "_dlmpc_ws", (None, ExecStrategy("b200")))
+    if ws is None or ws.triple is not triple:
+        ws = AdmmWorkspace(triple, build_column_classes(operator, triple.tables.mask), spec)
+    ws.set_row_data(row_data)
+    sess = ws._prepare(strat)
+    _, rg = ws._gathers(sess.layout)
+    phi = np.zeros(sess.n_cell)
+    phi[rg[rg >= 0]] = triple.phi_r[rg >= 0]      # the reference audits the row layout
+    dyn, res, gap = sess.audit(phi)
+    return FixedPointReport(dyn, res, gap, 10.0 * spec.eps_pri)
 
 
 # ---------------------------------------------------------------------------
@@ -228,6 +270,28 @@ class DlmpcSession:
         traj = Trajectory(out["states"], out["inputs"], out["step_iterations"])
         return traj, self.device.last_timing()[0]
 
+    def simulate_audited(self, x0, t_sim: int, warm_start: bool, ledger):
+        """The closed loop one MPC step per launch with the on-device
+        fixed-point audit after every solve (reference admm.py:506-513)."""
+        x = np.asarray(x0, dtype=np.float64)
+        states, inputs, iters = [x], [], []
+        worst = {"dynamics_residual": 0.0, "resolve_residual": 0.0, "consensus_gap": 0.0}
+        for step in range(t_sim):
+            try:
+                out = self.device.simulate(x, 1, self.spec.max_iters, self.spec.eps_pri, self.spec.eps_dual,
+                                           warm_start=warm_start, cold_start=(step == 0 or not warm_start))
+            except (NotConverged, RowInfeasible) as err:
+                err.step = step
+                raise
+            ledger.record_launch(out["step_iterations"][0], self.device.last_timing()[0])
+            for key, v in zip(worst, self.device.audit()):
+                worst[key] = max(worst[key], v)
+            x = out["states"][1]
+            states.append(x)
+            inputs.append(out["inputs"][0])
+            iters.append(out["step_iterations"][0])
+        return Trajectory(np.array(states), np.array(inputs), iters), worst
+
     def close(self):
         self.device.close()
 
@@ -267,9 +331,6 @@ def dlmpc_simulate(system: LtiSystem, spec: ProblemSpec, mask: LocalityMask,
         raise ValueError("x0 length must equal the global state dimension")
     if t_sim < 1:
         raise ValueError("t_sim must be >= 1")
-    if audit:
-        raise ValueError("audit=True is not available on the device path yet "
-                         "(verify_fixed_point is SURVEY §8(f) item 3)")
     strat = ExecStrategy(strategy) if isinstance(strategy, str) else strategy
     total_start = time.perf_counter()
     phases = dict.fromkeys(PHASES, 0.0)
@@ -280,11 +341,16 @@ def dlmpc_simulate(system: LtiSystem, spec: ProblemSpec, mask: LocalityMask,
     sess, _ = _cached_session(system, spec, mask, strat)
     phases["precompute_global"] = time.perf_counter() - start
     start = time.perf_counter()
+    audit_worst = None
     try:
-        traj, dev_ms = sess.simulate(x0, t_sim, warm_start)
+        if not audit:
+            traj, dev_ms = sess.simulate(x0, t_sim, warm_start)
+            executor.ledger.record_launch(sum(traj.step_iterations), dev_ms)
+        else:
+            traj, audit_worst = sess.simulate_audited(x0, t_sim, warm_start, executor.ledger)
+            dev_ms = executor.ledger.device_time_ms
     finally:
         phases["optimize"] = time.perf_counter() - start
-    executor.ledger.record_launch(sum(traj.step_iterations), dev_ms)
     report = RunReport(
         scenario={"strategy": strat.variant, "worker_count": executor.workers, "t_sim": t_sim,
                   "warm_start": warm_start, "rho": spec.rho, "eps": spec.eps_pri,
@@ -295,6 +361,6 @@ def dlmpc_simulate(system: LtiSystem, spec: ProblemSpec, mask: LocalityMask,
         closed_loop_cost=closed_loop_cost(traj),
         converged_all_steps=True,
         total_wall_ms=(time.perf_counter() - total_start) * 1e3,
-        audit_worst=None,
+        audit_worst=audit_worst,
     )
     return traj, report

@@ -32,6 +32,8 @@ struct dlmpc_handle {
   double* d_states = nullptr; double* d_inputs = nullptr; int states_cap = 0;
   float last_ms = 0.f; int last_launches = 0;
   double* d_scratch = nullptr;
+  double* d_scratch2 = nullptr;
+  double* d_audit = nullptr;
   int mode = kPatch, n_units = 0;
 };
 
@@ -385,6 +387,11 @@ int dlmpc_create(const dlmpc_problem* pr, int device, dlmpc_handle** out) {
     UP(a_ptr, pr->n_cols + 1); UP(a_idx, pr->a_ptr[pr->n_cols]); UP(a_val, pr->a_ptr[pr->n_cols]);
     UP(b_ptr, pr->n_cols + 1); UP(b_idx, pr->b_ptr[pr->n_cols]); UP(b_val, pr->b_ptr[pr->n_cols]);
     UP(input_owner, pr->n_inputs); UP(input_local, pr->n_inputs);
+    if (pr->g0_pool && pr->perm_pool && pr->col_pin) {
+      UP(class_ntouch, pr->n_classes); UP(class_g0_off, pr->n_classes + 1);
+      UP(g0_pool, pr->class_g0_off[pr->n_classes]); UP(class_perm_off, pr->n_classes + 1);
+      UP(perm_pool, pr->class_perm_off[pr->n_classes]); UP(col_pin, pr->n_cols);
+    }
     const size_t ncell = (size_t)pr->n_cols * pr->s_pad;
     for (int q = 0; q < 2; ++q) {
       if ((rc = alloc(h, ncell, &P.psi[q])) != DLMPC_OK) goto bad;
@@ -421,6 +428,8 @@ void dlmpc_destroy(dlmpc_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void* p : h->allocs) cudaFree(p);
   if (h->d_hist) cudaFree(h->d_hist);
+  if (h->d_scratch2) cudaFree(h->d_scratch2);
+  if (h->d_audit) cudaFree(h->d_audit);
   if (h->P.resid) cudaFree(h->P.resid);
   if (h->d_step_iters) cudaFree(h->d_step_iters);
   if (h->d_states) cudaFree(h->d_states);
@@ -600,6 +609,40 @@ void* dlmpc_stream(dlmpc_handle* h) { return h ? static_cast<void*>(h->stream) :
 int dlmpc_synchronize(dlmpc_handle* h) {
   if (!h) return DLMPC_BAD_ARGUMENT;
   CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  return DLMPC_OK;
+}
+
+int dlmpc_audit(dlmpc_handle* h, const double* phi_host, double* out3) {
+  if (!h || !out3) return fail(h, DLMPC_BAD_ARGUMENT, "null argument");
+  if (!h->P.g0_pool) return fail(h, DLMPC_BAD_ARGUMENT, "problem was created without audit tables");
+  cudaSetDevice(h->device);
+  int ctl[8];
+  if (int rc = read_ctl(h, ctl)) return rc;
+  const int b = ctl[4];
+  if (!h->d_audit) CUDA_OR_FAIL(h, cudaMalloc(&h->d_audit, sizeof(double) * ((size_t)h->P.n_rows + 4)));
+  double* s_fresh = h->d_audit;       // fresh Φ scale per row
+  double* out = h->d_audit + h->P.n_rows;
+  CUDA_OR_FAIL(h, cudaMemsetAsync(out, 0, sizeof(double) * 3, h->stream));
+  const double* phi_dev = nullptr;
+  if (phi_host) {   // audit a caller-provided φ (internal layout) instead of the recomputed one
+    const size_t ncell = (size_t)h->P.n_cols * h->P.s_pad;
+    if (!h->d_scratch2) CUDA_OR_FAIL(h, cudaMalloc(&h->d_scratch2, sizeof(double) * ncell));
+    CUDA_OR_FAIL(h, cudaMemcpyAsync(h->d_scratch2, phi_host, sizeof(double) * ncell, cudaMemcpyHostToDevice, h->stream));
+    phi_dev = h->d_scratch2;
+  }
+  const int warps = 16, blocks = (h->P.n_sub + warps - 1) / warps;
+  const double* x = h->P.x[0];
+  if (h->P.exact) audit_phi_kernel<true><<<blocks, 32 * warps, 0, h->stream>>>(h->P, b, x, s_fresh);
+  else audit_phi_kernel<false><<<blocks, 32 * warps, 0, h->stream>>>(h->P, b, x, s_fresh);
+  CUDA_OR_FAIL(h, cudaGetLastError());
+  if (h->P.exact) audit_entries_kernel<true><<<h->sm_count * 4, 512, 0, h->stream>>>(h->P, b, x, s_fresh, phi_dev, out);
+  else audit_entries_kernel<false><<<h->sm_count * 4, 512, 0, h->stream>>>(h->P, b, x, s_fresh, phi_dev, out);
+  CUDA_OR_FAIL(h, cudaGetLastError());
+  audit_dynamics_kernel<<<h->sm_count * 4, 256, 0, h->stream>>>(h->P, b, out);
+  CUDA_OR_FAIL(h, cudaGetLastError());
+  CUDA_OR_FAIL(h, cudaMemcpyAsync(out3, out, sizeof(double) * 3, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  h->last_launches = 3;
   return DLMPC_OK;
 }
 

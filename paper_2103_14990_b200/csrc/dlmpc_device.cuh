@@ -71,6 +71,9 @@ struct DevProblem {
   const int64_t* a_ptr; const int* a_idx; const double* a_val;
   const int64_t* b_ptr; const int* b_idx; const double* b_val;
   const int* input_owner; const int* input_local;
+  // audit tables (optional)
+  const int* class_ntouch; const int64_t* class_g0_off; const double* g0_pool;
+  const int64_t* class_perm_off; const int* perm_pool; const int* col_pin;
   // patch work units (built by the library at create time)
   const int* cta_unit_ptr;     // [grid+1]
   const int* unit_sub_lo;      // own subsystems [lo, hi)
@@ -949,6 +952,89 @@ __global__ void phi_materialize_kernel(DevProblem P, int pb, double* out) {
       v = make_phi<EXACT>(__dsub_rn(P.psi[pb][q], P.lam[pb][q]), P.s_row[ir], P.x[0][c]);
     }
     out[q] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fixed-point audit (reference verify_fixed_point, admm.py:417-434), run on
+// the current iterate after a solve. Plain (non-cooperative) launches.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void atomic_max_nonneg(double* dst, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(dst), static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+// Φ scale at the current dual point (buffer b) for every row -> s_fresh.
+template <bool EXACT>
+__global__ void audit_phi_kernel(DevProblem P, int b, const double* x, double* s_fresh) {
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= P.n_sub) return;   // warp-uniform
+  double* dst = s_fresh + P.row_start[i];
+  phi_rows_of<EXACT>(P, i, P.psi[b], P.lam[b], x, [dst](int l, double s) { dst[l] = s; });
+}
+
+// re-solve residual max|φ_fresh - φ| and consensus gap max|φ - ψ| over every
+// support entry (the reference's row_valid cells, admm.py:430-433).
+template <bool EXACT>
+__global__ void audit_entries_kernel(DevProblem P, int b, const double* x, const double* s_fresh,
+                                     const double* phi_given, double* out) {
+  __shared__ double red[64];
+  double res = 0.0, gap = 0.0;
+  const size_t n = static_cast<size_t>(P.n_cols) * P.s_pad;
+  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
+    const int c = static_cast<int>(q / P.s_pad), p = static_cast<int>(q % P.s_pad);
+    if (p >= P.col_len[c]) continue;
+    const long long ir = P.contiguous ? P.col_rowbase[c] + p
+                                      : P.col_irow[static_cast<size_t>(P.col_owner[c]) * P.s_pad + p];
+    const double xc = x[c];
+    const double phi = phi_given ? phi_given[q]
+                                 : make_phi<EXACT>(__dsub_rn(P.psi[b ^ 1][q], P.lam[b ^ 1][q]), P.s_row[ir], xc);
+    const double fresh = make_phi<EXACT>(__dsub_rn(P.psi[b][q], P.lam[b][q]), s_fresh[ir], xc);
+    res = fmax(res, fabs(__dsub_rn(fresh, phi)));
+    gap = fmax(gap, fabs(__dsub_rn(phi, P.psi[b][q])));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    res = fmax(res, __shfl_xor_sync(0xffffffffu, res, o));
+    gap = fmax(gap, __shfl_xor_sync(0xffffffffu, gap, o));
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { red[2 * warp] = res; red[2 * warp + 1] = gap; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (blockDim.x >> 5); ++w) { res = fmax(res, red[2 * w]); gap = fmax(gap, red[2 * w + 1]); }
+    atomic_max_nonneg(out + 1, res);
+    atomic_max_nonneg(out + 2, gap);
+  }
+}
+
+// dynamics residual max|z ψ - rhs| restricted to each column's touched rows
+// (the reference multiplies the sparse operator by the dense response:
+// CSR order, products rounded then summed from zero, admm.py:427).
+__global__ void audit_dynamics_kernel(DevProblem P, int b, double* out) {
+  __shared__ double red[32];
+  double worst = 0.0;
+  for (int c = blockIdx.x; c < P.n_cols; c += gridDim.x) {
+    const int k = P.col_class[c];
+    const int S = P.class_s[k], nt = P.class_ntouch[k];
+    const double* g0 = P.g0_pool + P.class_g0_off[k];
+    const int* perm = P.perm_pool + P.class_perm_off[k];
+    const double* psi = P.psi[b] + static_cast<size_t>(c) * P.s_pad;
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+      double acc = 0.0;
+      for (int j = 0; j < S; ++j) {
+        const double v = g0[static_cast<size_t>(i) * S + j];
+        if (v != 0.0) acc = __dadd_rn(acc, __dmul_rn(v, psi[perm[j]]));
+      }
+      if (i == P.col_pin[c]) acc = __dsub_rn(acc, 1.0);
+      worst = fmax(worst, fabs(acc));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = worst;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (blockDim.x >> 5); ++w) worst = fmax(worst, red[w]);
+    atomic_max_nonneg(out, worst);
   }
 }
 

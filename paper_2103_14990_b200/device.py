@@ -47,6 +47,8 @@ class _Problem(C.Structure):
         ("a_ptr", _i64p), ("a_idx", _i32p), ("a_val", _f64p),
         ("b_ptr", _i64p), ("b_idx", _i32p), ("b_val", _f64p),
         ("input_owner", _i32p), ("input_local", _i32p),
+        ("class_ntouch", _i32p), ("class_g0_off", _i64p), ("g0_pool", _f64p),
+        ("class_perm_off", _i64p), ("perm_pool", _i32p), ("col_pin", _i32p),
     ]
 
 
@@ -54,7 +56,7 @@ EXPORTS = ("dlmpc_create", "dlmpc_destroy", "dlmpc_last_error", "dlmpc_global_er
            "dlmpc_set_x", "dlmpc_solve", "dlmpc_iterate", "dlmpc_simulate",
            "dlmpc_simulate_device", "dlmpc_get", "dlmpc_put", "dlmpc_zero",
            "dlmpc_last_timing", "dlmpc_stream", "dlmpc_synchronize", "dlmpc_info",
-           "dlmpc_phase_times")
+           "dlmpc_phase_times", "dlmpc_audit")
 
 _lib = None
 
@@ -95,6 +97,7 @@ def load_library():
     lib.dlmpc_synchronize.argtypes = [vp]
     lib.dlmpc_info.argtypes = [vp, _i64p]
     lib.dlmpc_phase_times.argtypes = [vp, _P(C.c_uint64), C.c_int]
+    lib.dlmpc_audit.argtypes = [vp, _f64p, _f64p]
     _lib = lib
     return lib
 
@@ -150,6 +153,8 @@ class DeviceSession:
         p.a_ptr, p.a_idx, p.a_val = i64("a_ptr"), i32("a_idx"), f64("a_val")
         p.b_ptr, p.b_idx, p.b_val = i64("b_ptr"), i32("b_idx"), f64("b_val")
         p.input_owner, p.input_local = i32("input_owner"), i32("input_local")
+        p.class_ntouch, p.class_g0_off, p.g0_pool = i32("class_ntouch"), i64("class_g0_off"), f64("g0_pool")
+        p.class_perm_off, p.perm_pool, p.col_pin = i64("class_perm_off"), i32("perm_pool"), i32("col_pin")
         h = C.c_void_p()
         rc = lib.dlmpc_create(C.byref(p), int(device), C.byref(h))
         self._keep = []
@@ -248,6 +253,15 @@ class DeviceSession:
             raise ValueError("internal-layout array has the wrong size")
         self._check(self._lib.dlmpc_put(self._h, int(which), _ptr(v, C.c_double)), "dlmpc_put")
 
+    def audit(self, phi=None):
+        """(dynamics_residual, resolve_residual, consensus_gap) of the current
+        iterate; `phi` (internal layout) overrides the last iteration's φ."""
+        out = np.zeros(3)
+        ph = None if phi is None else np.ascontiguousarray(phi, dtype=np.float64)
+        self._check(self._lib.dlmpc_audit(self._h, _ptr(ph, C.c_double), _ptr(out, C.c_double)),
+                    "dlmpc_audit")
+        return float(out[0]), float(out[1]), float(out[2])
+
     def zero(self):
         self._check(self._lib.dlmpc_zero(self._h), "dlmpc_zero")
 
@@ -268,7 +282,7 @@ class DeviceSession:
         g = self.info()["grid"]
         out = np.zeros(8 * g, dtype=np.uint64)
         self._check(self._lib.dlmpc_phase_times(self._h, out.ctypes.data_as(_P(C.c_uint64)), int(reset)),
-                    "dlmpc_phase_times")
+                    "dlmpc_phase_times", "dlmpc_audit")
         return out.reshape(g, 8)
 
     def info(self):

@@ -245,6 +245,21 @@ class DeviceLayout:
             q_list.append(q)
             rhs_list.append(r)
         self.col_vec = col_vec.astype(np.int32)
+
+        # audit tables (on-device verify_fixed_point): per device class the
+        # reference's touched-rows operator g0 (reference support order) and
+        # the support permutation; per column the rhs0 pin
+        if classes.col_pin is not None:
+            g0s = [np.ascontiguousarray(classes.classes[int(upairs[k, 0])].g0) for k in range(n_cls)]
+            self.class_ntouch = np.array([g.shape[0] for g in g0s], dtype=np.int32)
+            self.class_g0_off = np.concatenate([[0], np.cumsum([g.size for g in g0s])]).astype(np.int64)
+            self.g0_pool = np.concatenate([g.ravel() for g in g0s])
+            self.class_perm_off = np.concatenate([[0], np.cumsum([p_.size for p_ in self._class_perm])]).astype(np.int64)
+            self.perm_pool = np.concatenate(self._class_perm).astype(np.int32)
+            self.col_pin = classes.col_pin.astype(np.int32)
+        else:
+            self.class_ntouch = self.class_g0_off = self.g0_pool = None
+            self.class_perm_off = self.perm_pool = self.col_pin = None
         self.n_vec = len(q_list)
         self.q_pool = np.concatenate(q_list)
         self.rhs_pool = np.concatenate(rhs_list)

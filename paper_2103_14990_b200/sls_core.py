@@ -256,9 +256,13 @@ class ColumnClasses:
     rows touched (general builder only; None at scale).
     """
 
-    def __init__(self, classes, col_class, rhs_table, col_rhs, sub_struct=None, touch=None):
+    def __init__(self, classes, col_class, rhs_table, col_rhs, sub_struct=None, touch=None,
+                 col_pin=None):
         self.classes = classes
         self.col_class = np.asarray(col_class, dtype=np.int64)
+        # position of the column's own t=0 row among its touched operator rows
+        # (where rhs0 = 1), -1 if untouched; None when built from precomps
+        self.col_pin = None if col_pin is None else np.asarray(col_pin, dtype=np.int64)
         self.rhs_table = rhs_table
         self.col_rhs = np.asarray(col_rhs, dtype=np.int64)
         self.sub_struct = sub_struct
@@ -391,7 +395,7 @@ def _finish_classes(classes, col_class, col_pin, n_touch_of_col, reps_g0, failin
     if failing:
         c, res = min(failing)
         raise LocalityInfeasible(c, res)
-    return ColumnClasses(classes, col_class, rhs_table, col_rhs, sub_struct, touch)
+    return ColumnClasses(classes, col_class, rhs_table, col_rhs, sub_struct, touch, col_pin)
 
 
 def build_column_classes(op: DynamicsOperator, mask: LocalityMask) -> ColumnClasses:

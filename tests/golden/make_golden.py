@@ -138,6 +138,18 @@ def main():
         lm.admm_solve(rd, b[5], lm.PhiTriple(b[3]), b[1], lm.ExecStrategy("sequential"))
     except lm.NotConverged as err:
         save("not_converged_n3", x=x, history=np.array(err.residual_history))
+    # the reference's dense KKT oracle (oracle.py:111-127) on unbounded instances
+    kk = {}
+    for n, t, d in ((2, 3, 1), (3, 4, 2), (4, 3, 1), (4, 4, 2)):
+        system = lm.build_chain_network(n)
+        spec = lm.make_benchmark_spec(system, t, eps=1e-6, bounded=False)
+        mask = lm.build_locality_mask(system, d, t)
+        x0 = lm.sample_initial_state(system.partition, np.random.default_rng(31 + n))
+        ref = lm.simulate_with_oracle(system, spec, mask, x0, 8)
+        kk[f"n{n}_t{t}_d{d}_states"] = ref.states
+        kk[f"n{n}_t{t}_d{d}_inputs"] = ref.inputs
+        kk[f"n{n}_t{t}_d{d}_x0"] = x0
+    save("kkt_oracle", **kk)
     if args.big:
         save("c3_n1000_step0", **closed_loop(lm, 1000, 3, 10, 1, 1))
 

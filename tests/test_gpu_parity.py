@@ -267,3 +267,123 @@ def test_large_network_properties():
     assert te.step_iterations[0] == t1.step_iterations[0]
     assert rel_err(te.states, t1.states[:2]) <= FAST_RTOL
     sess.close(); ex.close()
+
+
+C4_GRID = [(20, 1, 5), (16, 1, 10), (20, 2, 20), (14, 3, 30), (20, 4, 10), (20, 5, 5), (20, 6, 5)]
+
+
+@pytest.mark.parametrize("variant", [EXACT, FAST])
+@pytest.mark.parametrize("n,d,t", C4_GRID)
+def test_locality_horizon_sweep_against_oracle(n, d, t, variant):
+    """SURVEY config C4 (d = 1..6, T = 5..30; longest-vector padding): iteration
+    counts and trajectories vs the oracle on a 2-step closed loop. T=30 and
+    d=3 makes the Ψ operator (623 x 175) too large for shared memory, which
+    exercises the global-operator path and wide rows."""
+    system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=n, d=d, horizon=t, seed=3))
+    tables = pb.LayoutTables(mask)
+    cs = pb.precompute_column_solvers(pb.build_dynamics_operator(system, t), mask)
+    ref = admm_ref.simulate(system, spec, tables, cs, x0, 2)
+    traj, _ = pb.dlmpc_simulate(system, spec, mask, x0, 2, variant)
+    assert list(traj.step_iterations) == ref["step_iterations"]
+    if variant == EXACT:
+        assert np.array_equal(traj.states, ref["states"])
+        assert np.array_equal(traj.inputs, ref["inputs"])
+    else:
+        assert rel_err(traj.states, ref["states"]) <= FAST_RTOL
+
+
+@pytest.mark.parametrize("variant", [EXACT, FAST])
+def test_closed_loop_cost_matches_kkt_oracle(variant):
+    """The reference's acceptance criterion (test_acceptance.py:112-132): on
+    12 unbounded chains the ADMM closed-loop cost is within 1e-4 (relative)
+    of the dense KKT solve -- an independent algorithm (oracle/kkt.py)."""
+    from oracle import kkt
+    worst = 0.0
+    for n in (2, 3, 4):
+        for t in (3, 4):
+            for d in (1, 2):
+                system = pb.build_chain_network(n)
+                spec = pb.make_benchmark_spec(system, t, eps=1e-6, bounded=False)
+                mask = pb.build_locality_mask(system, d, t)
+                x0 = pb.sample_initial_state(system.partition, np.random.default_rng(31 + n))
+                traj, rep = pb.dlmpc_simulate(system, spec, mask, x0, 8, variant)
+                states, inputs = kkt.kkt_closed_loop(system, spec, mask, x0, 8)
+                ref_cost = float(np.sum(states ** 2) + np.sum(inputs ** 2))
+                rel = abs(rep.closed_loop_cost - ref_cost) / max(1.0, ref_cost)
+                worst = max(worst, rel)
+                assert rel <= 1e-4, (n, t, d, rel)
+
+
+class TestVerifyFixedPoint:
+    """On-device audit (reference verify_fixed_point, admm.py:417-434, and
+    its tests test_admm.py:312-363)."""
+
+    def test_exact_fixed_point_by_construction(self):
+        import scipy.sparse as sp
+        part = pb.SubsystemPartition(((0, 1),), ((0, 0),))
+        graph = pb.SubsystemGraph.from_edges(1, [])
+        system = pb.LtiSystem(sp.csr_matrix((1, 1)), sp.csr_matrix((1, 0)), part, graph)
+        mask = pb.build_locality_mask(system, 0, 2)
+        tables = pb.LayoutTables(mask)
+        operator = pb.build_dynamics_operator(system, 2)
+        spec = pb.make_benchmark_spec(system, 2, bounded=False)
+        rd = pb.precompute_row_data(np.zeros(1), spec, tables)
+        triple = pb.PhiTriple(tables)
+        pinned = np.array([1.0, 0.0])
+        triple.phi_r[:, 0] = pinned
+        triple.psi_r[:, 0] = pinned
+        triple.exchange_phi_row_to_col()
+        triple.psi_c[:] = triple.phi_c
+        rep = pb.verify_fixed_point(triple, rd, operator, spec)
+        assert (rep.dynamics_residual, rep.resolve_residual, rep.consensus_gap) == (0.0, 0.0, 0.0)
+
+    @pytest.mark.parametrize("variant", [EXACT, FAST])
+    def test_converged_solve_passes_and_perturbation_fails(self, variant):
+        b = chain_bundle(4, 4, 2)
+        x0 = pb.sample_initial_state(b["system"].partition, np.random.default_rng(1234))
+        rd = pb.precompute_row_data(x0, b["spec"], b["tables"])
+        triple = pb.PhiTriple(b["tables"])
+        pb.admm_solve(rd, b["col_solvers"], triple, b["spec"], variant)
+        rep = pb.verify_fixed_point(triple, rd, b["operator"], b["spec"])
+        assert rep.passed
+        assert max(rep.dynamics_residual, rep.resolve_residual, rep.consensus_gap) <= 1e-3
+        assert rep.dynamics_residual <= 1e-12
+        triple.phi_r[0, 0] += 0.1
+        rep = pb.verify_fixed_point(triple, rd, b["operator"], b["spec"])
+        assert rep.resolve_residual >= 0.09
+        assert not rep.passed
+
+    def test_audit_matches_host_recomputation(self):
+        """The device audit equals a host recomputation of the reference's
+        three residuals on the same (exact-mode) triple."""
+        b = chain_bundle(6, 4, 2)
+        x0 = pb.sample_initial_state(b["system"].partition, np.random.default_rng(5))
+        rd = pb.precompute_row_data(x0, b["spec"], b["tables"])
+        triple = pb.PhiTriple(b["tables"])
+        pb.admm_solve(rd, b["col_solvers"], triple, b["spec"], EXACT)
+        rep = pb.verify_fixed_point(triple, rd, b["operator"], b["spec"])
+        tb = b["tables"]
+        dyn = float(np.max(np.abs(b["operator"].residual(triple.psi_dense()))))
+        orc = admm_ref.OracleSolver(tb, b["col_solvers"], 1.0)
+        w, lo, hi = b["spec"].row_arrays()
+        orc.row_data, _ = admm_ref.row_data_for(x0, tb, w, lo, hi)
+        orc.psi_r[:], orc.lam_r[:] = triple.psi_r, triple.lam_r
+        orc._phi(0, tb.n_rows)
+        res = float(np.max(np.abs((orc.phi_r - triple.phi_r)[tb.row_valid])))
+        gap = float(np.max(np.abs((triple.phi_r - triple.psi_r)[tb.row_valid])))
+        assert rep.resolve_residual == res and rep.consensus_gap == gap
+        np.testing.assert_allclose(rep.dynamics_residual, dyn, rtol=1e-6, atol=1e-15)
+
+    @pytest.mark.parametrize("variant", [EXACT, FAST])
+    def test_closed_loop_audit(self, variant):
+        """dlmpc_simulate(audit=True): worst residuals over the loop within
+        10 x eps (the reference's acceptance audit, test_acceptance.py:98-109),
+        and the audited loop reproduces the reference trajectory."""
+        g = golden("c1_loop_seed1")
+        system, spec, mask, t_sim = loop_problem(g)
+        traj, rep = pb.dlmpc_simulate(system, spec, mask, g["x0"], t_sim, variant, audit=True)
+        assert list(traj.step_iterations) == list(g["step_iters"])
+        for key in ("dynamics_residual", "resolve_residual", "consensus_gap"):
+            assert rep.audit_worst[key] <= 1e-3, key
+        if variant == EXACT:
+            assert np.array_equal(traj.states, g["states"])

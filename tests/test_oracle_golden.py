@@ -116,3 +116,19 @@ def test_zero_state_loop():
     assert res["step_iterations"] == list(g["step_iters"])
     assert np.array_equal(res["states"], g["states"])
     assert res["step_iterations"][-1] == 1
+
+
+KKT_CASES = [(2, 3, 1), (3, 4, 2), (4, 3, 1), (4, 4, 2)]
+
+
+@pytest.mark.parametrize("n,t,d", KKT_CASES)
+def test_kkt_oracle_restatement_matches_reference(n, t, d):
+    """oracle/kkt.py reproduces the reference's dense KKT closed loop."""
+    from oracle import kkt
+    g = golden("kkt_oracle")
+    system = pb.build_chain_network(n)
+    spec = pb.make_benchmark_spec(system, t, eps=1e-6, bounded=False)
+    mask = pb.build_locality_mask(system, d, t)
+    states, inputs = kkt.kkt_closed_loop(system, spec, mask, g[f"n{n}_t{t}_d{d}_x0"], 8)
+    np.testing.assert_allclose(states, g[f"n{n}_t{t}_d{d}_states"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(inputs, g[f"n{n}_t{t}_d{d}_inputs"], rtol=1e-9, atol=1e-12)
