@@ -70,6 +70,10 @@ typedef struct dlmpc_problem {
   int32_t n_sub, n_rows, n_cols, n_inputs, s_pad, horizon;
   int32_t exact;          /* 1: reference arithmetic bit for bit; 0: fast path  */
   int32_t contiguous;     /* 1: every ball is a contiguous id range (chains)    */
+  /* owned range for graph-partitioned runs: only these subsystems / columns
+   * are solved (and enter the residuals); the rest is a read-only halo.
+   * own_sub_hi <= own_sub_lo means "everything". */
+  int32_t own_sub_lo, own_sub_hi, own_col_lo, own_col_hi;
   double rho;
   /* subsystems */
   const int64_t* row_start;      /* [n_sub+1] */
@@ -181,6 +185,29 @@ int dlmpc_simulate_device(dlmpc_handle* h, const double* x0_dev, int t_sim, int 
  * max|φ - ψ|. φ is the last iteration's (phi_host == NULL) or a caller's
  * φ in internal layout. Needs the audit tables of dlmpc_problem. */
 int dlmpc_audit(dlmpc_handle* h, const double* phi_host, double* out3);
+
+/* Column ranges of the current ψ / λ (internal layout, host or device
+ * pointers): the per-iteration halo exchange of the partitioned path. */
+int dlmpc_get_cols(dlmpc_handle* h, int which, int c0, int n, double* dst);
+int dlmpc_put_cols(dlmpc_handle* h, int which, int c0, int n, const double* src);
+
+/* Halo exchange of the partitioned path (one rank's sub-problem): register
+ * the internal cells this rank sends (concatenated over destination ranks)
+ * and receives (over source ranks) once, then every iteration pack the
+ * current (ψ, λ) of the send cells into `out` [2*n_send doubles, pairs
+ * interleaved] and unpack a received message `in` [2*n_recv] into the halo
+ * cells. Pointers may be host or device memory; both calls synchronise.
+ * Replaces the reference's shared-memory triple, which every worker reads
+ * in place (admm.py:186-253: there is no exchange on one host). */
+int dlmpc_set_halo(dlmpc_handle* h, const int64_t* send_cells, int64_t n_send,
+                   const int64_t* recv_cells, int64_t n_recv);
+int dlmpc_halo_pack(dlmpc_handle* h, double* out);
+int dlmpc_halo_unpack(dlmpc_handle* h, const double* in);
+
+/* After host-driven iterations: control extraction (admm.py:350-360) and
+ * plant step (admm.py:363-369) for the loaded x; u_out [n_inputs],
+ * x_next_out [n_cols] (valid for owned states). */
+int dlmpc_finish_step(dlmpc_handle* h, double* u_out, double* x_next_out);
 
 /* Copy an internal-layout array to/from host memory. */
 int dlmpc_get(dlmpc_handle* h, int which, double* dst);

@@ -35,6 +35,9 @@ struct dlmpc_handle {
   double* d_scratch2 = nullptr;
   double* d_audit = nullptr;
   int mode = kPatch, n_units = 0;
+  int64_t* d_send_cells = nullptr; int64_t n_send = 0;
+  int64_t* d_recv_cells = nullptr; int64_t n_recv = 0;
+  double* d_halo = nullptr;
 };
 
 namespace {
@@ -178,9 +181,10 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       auto sub_class = [&](int i) { return pr->col_class[pr->state_start[i]]; };
       // runs of consecutive same-class subsystems
       std::vector<int> run_lo, run_hi;
-      for (int i = 0; i < pr->n_sub;) {
+      const int o_lo = P.own_sub_lo, o_hi = P.own_sub_hi;
+      for (int i = o_lo; i < o_hi;) {
         int j = i + 1;
-        while (j < pr->n_sub && sub_class(j) == sub_class(i)) ++j;
+        while (j < o_hi && sub_class(j) == sub_class(i)) ++j;
         run_lo.push_back(i); run_hi.push_back(j);
         i = j;
       }
@@ -209,9 +213,10 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           }
         }
       } else {
+        const int n_own = o_hi - o_lo;
         for (int q = 0; q < G; ++q) {
-          ranges.push_back((int)((long long)pr->n_sub * q / G));
-          ranges.push_back((int)((long long)pr->n_sub * (q + 1) / G));
+          ranges.push_back(o_lo + (int)((long long)n_own * q / G));
+          ranges.push_back(o_lo + (int)((long long)n_own * (q + 1) / G));
         }
       }
       const long long cap_rows = 4096;
@@ -356,6 +361,9 @@ int dlmpc_create(const dlmpc_problem* pr, int device, dlmpc_handle** out) {
   {
     DevProblem& P = h->P;
     P.n_sub = pr->n_sub; P.n_rows = pr->n_rows; P.n_cols = pr->n_cols; P.n_inputs = pr->n_inputs;
+    P.own_sub_lo = pr->own_sub_lo; P.own_sub_hi = pr->own_sub_hi;
+    P.own_col_lo = pr->own_col_lo; P.own_col_hi = pr->own_col_hi;
+    if (P.own_sub_hi <= P.own_sub_lo) { P.own_sub_lo = 0; P.own_sub_hi = pr->n_sub; P.own_col_lo = 0; P.own_col_hi = pr->n_cols; }
     P.s_pad = pr->s_pad; P.exact = pr->exact; P.contiguous = pr->contiguous; P.rho = pr->rho;
     P.n_classes = pr->n_classes; P.m_pad = pr->m_pad; P.n_tiles = pr->n_tiles; P.tile_cols = pr->tile_cols;
     const size_t nb = (size_t)pr->ball_ptr[pr->n_sub];
@@ -430,6 +438,9 @@ void dlmpc_destroy(dlmpc_handle* h) {
   if (h->d_hist) cudaFree(h->d_hist);
   if (h->d_scratch2) cudaFree(h->d_scratch2);
   if (h->d_audit) cudaFree(h->d_audit);
+  if (h->d_send_cells) cudaFree(h->d_send_cells);
+  if (h->d_recv_cells) cudaFree(h->d_recv_cells);
+  if (h->d_halo) cudaFree(h->d_halo);
   if (h->P.resid) cudaFree(h->P.resid);
   if (h->d_step_iters) cudaFree(h->d_step_iters);
   if (h->d_states) cudaFree(h->d_states);
@@ -581,6 +592,115 @@ int dlmpc_put(dlmpc_handle* h, int which, const double* src) {
   }
   CUDA_OR_FAIL(h, cudaMemcpyAsync(dst, src, sizeof(double) * ncell, cudaMemcpyHostToDevice, h->stream));
   CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  return DLMPC_OK;
+}
+
+int dlmpc_get_cols(dlmpc_handle* h, int which, int c0, int n, double* dst) {
+  if (!h || !dst || c0 < 0 || n < 0 || c0 + n > h->P.n_cols) return fail(h, DLMPC_BAD_ARGUMENT, "bad column range");
+  cudaSetDevice(h->device);
+  int ctl[8];
+  if (int rc = read_ctl(h, ctl)) return rc;
+  const int b = ctl[4];
+  const double* src = which == DLMPC_PSI ? h->P.psi[b] : which == DLMPC_LAM ? h->P.lam[b] : nullptr;
+  if (!src) return fail(h, DLMPC_BAD_ARGUMENT, "only PSI / LAM column ranges");
+  CUDA_OR_FAIL(h, cudaMemcpyAsync(dst, src + (size_t)c0 * h->P.s_pad, sizeof(double) * (size_t)n * h->P.s_pad,
+                                  cudaMemcpyDefault, h->stream));
+  CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  return DLMPC_OK;
+}
+
+int dlmpc_put_cols(dlmpc_handle* h, int which, int c0, int n, const double* src) {
+  if (!h || !src || c0 < 0 || n < 0 || c0 + n > h->P.n_cols) return fail(h, DLMPC_BAD_ARGUMENT, "bad column range");
+  cudaSetDevice(h->device);
+  int ctl[8];
+  if (int rc = read_ctl(h, ctl)) return rc;
+  const int b = ctl[4];
+  double* dst = which == DLMPC_PSI ? h->P.psi[b] : which == DLMPC_LAM ? h->P.lam[b] : nullptr;
+  if (!dst) return fail(h, DLMPC_BAD_ARGUMENT, "only PSI / LAM column ranges");
+  CUDA_OR_FAIL(h, cudaMemcpyAsync(dst + (size_t)c0 * h->P.s_pad, src, sizeof(double) * (size_t)n * h->P.s_pad,
+                                  cudaMemcpyDefault, h->stream));
+  CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  return DLMPC_OK;
+}
+
+int dlmpc_set_halo(dlmpc_handle* h, const int64_t* send_cells, int64_t n_send,
+                   const int64_t* recv_cells, int64_t n_recv) {
+  if (!h || n_send < 0 || n_recv < 0 || (n_send && !send_cells) || (n_recv && !recv_cells))
+    return fail(h, DLMPC_BAD_ARGUMENT, "bad halo cell lists");
+  const int64_t n_cell = (int64_t)h->P.n_cols * h->P.s_pad;
+  for (int64_t k = 0; k < n_send; ++k)
+    if (send_cells[k] < 0 || send_cells[k] >= n_cell) return fail(h, DLMPC_BAD_ARGUMENT, "send cell out of range");
+  for (int64_t k = 0; k < n_recv; ++k)
+    if (recv_cells[k] < 0 || recv_cells[k] >= n_cell) return fail(h, DLMPC_BAD_ARGUMENT, "recv cell out of range");
+  cudaSetDevice(h->device);
+  CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  for (int64_t** p : {&h->d_send_cells, &h->d_recv_cells})
+    if (*p) { cudaFree(*p); *p = nullptr; }
+  if (h->d_halo) { cudaFree(h->d_halo); h->d_halo = nullptr; }
+  h->n_send = n_send; h->n_recv = n_recv;
+  if (n_send) {
+    CUDA_OR_FAIL(h, cudaMalloc(&h->d_send_cells, sizeof(int64_t) * n_send));
+    CUDA_OR_FAIL(h, cudaMemcpy(h->d_send_cells, send_cells, sizeof(int64_t) * n_send, cudaMemcpyHostToDevice));
+  }
+  if (n_recv) {
+    CUDA_OR_FAIL(h, cudaMalloc(&h->d_recv_cells, sizeof(int64_t) * n_recv));
+    CUDA_OR_FAIL(h, cudaMemcpy(h->d_recv_cells, recv_cells, sizeof(int64_t) * n_recv, cudaMemcpyHostToDevice));
+  }
+  const int64_t nb = std::max<int64_t>(1, std::max(n_send, n_recv));
+  CUDA_OR_FAIL(h, cudaMalloc(&h->d_halo, sizeof(double) * 2 * nb));
+  return DLMPC_OK;
+}
+
+int dlmpc_halo_pack(dlmpc_handle* h, double* out) {
+  if (!h || (h->n_send && !out)) return fail(h, DLMPC_BAD_ARGUMENT, "null halo buffer");
+  if (!h->n_send) return DLMPC_OK;
+  cudaSetDevice(h->device);
+  int ctl[8];
+  if (int rc = read_ctl(h, ctl)) return rc;
+  const int b = ctl[4];
+  const int blocks = (int)std::min<int64_t>(h->sm_count * 4, (h->n_send + 255) / 256);
+  halo_pack_kernel<<<blocks, 256, 0, h->stream>>>(h->P.psi[b], h->P.lam[b], h->d_send_cells, h->n_send,
+                                                  reinterpret_cast<double2*>(h->d_halo));
+  CUDA_OR_FAIL(h, cudaGetLastError());
+  CUDA_OR_FAIL(h, cudaMemcpyAsync(out, h->d_halo, sizeof(double) * 2 * h->n_send, cudaMemcpyDefault, h->stream));
+  CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  return DLMPC_OK;
+}
+
+int dlmpc_halo_unpack(dlmpc_handle* h, const double* in) {
+  if (!h || (h->n_recv && !in)) return fail(h, DLMPC_BAD_ARGUMENT, "null halo buffer");
+  if (!h->n_recv) return DLMPC_OK;
+  cudaSetDevice(h->device);
+  int ctl[8];
+  if (int rc = read_ctl(h, ctl)) return rc;
+  const int b = ctl[4];
+  CUDA_OR_FAIL(h, cudaMemcpyAsync(h->d_halo, in, sizeof(double) * 2 * h->n_recv, cudaMemcpyDefault, h->stream));
+  const int blocks = (int)std::min<int64_t>(h->sm_count * 4, (h->n_recv + 255) / 256);
+  halo_unpack_kernel<<<blocks, 256, 0, h->stream>>>(h->P.psi[b], h->P.lam[b], h->d_recv_cells, h->n_recv,
+                                                    reinterpret_cast<const double2*>(h->d_halo));
+  CUDA_OR_FAIL(h, cudaGetLastError());
+  CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  return DLMPC_OK;
+}
+
+int dlmpc_finish_step(dlmpc_handle* h, double* u_out, double* x_next_out) {
+  if (!h) return fail(h, DLMPC_BAD_ARGUMENT, "null handle");
+  cudaSetDevice(h->device);
+  int ctl[8];
+  if (int rc = read_ctl(h, ctl)) return rc;
+  const int pb = ctl[4] ^ 1;
+  const int blocks = std::max(1, std::min(h->sm_count * 4, (std::max(h->P.n_cols, h->P.n_inputs) + 255) / 256));
+  if (h->P.exact) control_kernel<true><<<blocks, 256, 0, h->stream>>>(h->P, pb);
+  else control_kernel<false><<<blocks, 256, 0, h->stream>>>(h->P, pb);
+  CUDA_OR_FAIL(h, cudaGetLastError());
+  plant_kernel<<<blocks, 256, 0, h->stream>>>(h->P);
+  CUDA_OR_FAIL(h, cudaGetLastError());
+  if (u_out && h->P.n_inputs)
+    CUDA_OR_FAIL(h, cudaMemcpyAsync(u_out, h->P.u, sizeof(double) * h->P.n_inputs, cudaMemcpyDeviceToHost, h->stream));
+  if (x_next_out)
+    CUDA_OR_FAIL(h, cudaMemcpyAsync(x_next_out, h->P.x[1], sizeof(double) * h->P.n_cols, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  h->last_launches = 2;
   return DLMPC_OK;
 }
 

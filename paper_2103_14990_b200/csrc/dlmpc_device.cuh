@@ -55,6 +55,7 @@ constexpr int kMG2 = 2;                // m-tiles per GEMM-2 work unit
 
 struct DevProblem {
   int n_sub, n_rows, n_cols, n_inputs, s_pad, exact, contiguous, d_row;
+  int own_sub_lo, own_sub_hi, own_col_lo, own_col_hi;   // owned range (graph partition)
   double rho;
   const int64_t* row_start; const int64_t* ball_ptr; const int* ball_idx; const int* ball_off;
   const int* state_start; const int* state_count; const int* sub_first_bad;
@@ -227,7 +228,8 @@ __device__ void row_data_stage(const DevProblem& P, const double* x, int* bad_sl
     }
     if (D < P.d_row) acc = __dadd_rn(acc, 0.0);   // the padded slots of a_pad
     P.ada[i] = acc;
-    if (acc == 0.0 && P.sub_first_bad[i] >= 0) atomicMin(bad_slot, P.sub_first_bad[i]);
+    if (acc == 0.0 && P.sub_first_bad[i] >= 0 && i >= P.own_sub_lo && i < P.own_sub_hi)
+      atomicMin(bad_slot, P.sub_first_bad[i]);
   }
 }
 
@@ -773,7 +775,7 @@ __device__ void column_stage_exact(const DevProblem& P, int b, const double* x, 
   double* psi_n = P.psi[b ^ 1];
   double* lam_n = P.lam[b ^ 1];
   double pri_m = 0.0, dual_m = 0.0;
-  for (int c = blockIdx.x; c < P.n_cols; c += gridDim.x) {
+  for (int c = P.own_col_lo + blockIdx.x; c < P.own_col_hi; c += gridDim.x) {
     const int owner = P.col_owner[c];
     const int k = P.col_class[c];
     const int S = P.class_s[k], m = P.class_m[k];
@@ -1035,6 +1037,34 @@ __global__ void audit_dynamics_kernel(DevProblem P, int b, double* out) {
   if (threadIdx.x == 0) {
     for (int w = 1; w < (blockDim.x >> 5); ++w) worst = fmax(worst, red[w]);
     atomic_max_nonneg(out, worst);
+  }
+}
+
+// Control extraction and plant step for the loaded x after a host-driven
+// solve (graph-partitioned multi-GPU path): plain launches, grid-stride.
+template <bool EXACT>
+__global__ void control_kernel(DevProblem P, int pb) { control_stage<EXACT>(P, pb, P.x[0]); }
+__global__ void plant_kernel(DevProblem P) { plant_stage(P, P.x[0], P.x[1]); }
+
+// Halo exchange of the partitioned path (partition.py halo_cells): gather
+// the (ψ, λ) entries a neighbour reads into one interleaved message, and
+// scatter a received message into the halo cells. Grid-stride, coalesced on
+// the message side.
+__global__ void halo_pack_kernel(const double* __restrict__ psi, const double* __restrict__ lam,
+                                 const int64_t* __restrict__ cells, int64_t n, double2* __restrict__ out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = cells[k];
+    out[k] = make_double2(psi[c], lam[c]);
+  }
+}
+
+__global__ void halo_unpack_kernel(double* __restrict__ psi, double* __restrict__ lam,
+                                   const int64_t* __restrict__ cells, int64_t n, const double2* __restrict__ in) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = cells[k];
+    const double2 v = in[k];
+    psi[c] = v.x;
+    lam[c] = v.y;
   }
 }
 

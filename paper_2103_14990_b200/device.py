@@ -29,6 +29,7 @@ class _Problem(C.Structure):
     _fields_ = [
         ("n_sub", C.c_int32), ("n_rows", C.c_int32), ("n_cols", C.c_int32), ("n_inputs", C.c_int32),
         ("s_pad", C.c_int32), ("horizon", C.c_int32), ("exact", C.c_int32), ("contiguous", C.c_int32),
+        ("own_sub_lo", C.c_int32), ("own_sub_hi", C.c_int32), ("own_col_lo", C.c_int32), ("own_col_hi", C.c_int32),
         ("rho", C.c_double),
         ("row_start", _i64p), ("ball_ptr", _i64p), ("ball_idx", _i32p), ("ball_off", _i32p),
         ("state_start", _i32p), ("state_count", _i32p), ("sub_first_bad", _i32p),
@@ -56,7 +57,8 @@ EXPORTS = ("dlmpc_create", "dlmpc_destroy", "dlmpc_last_error", "dlmpc_global_er
            "dlmpc_set_x", "dlmpc_solve", "dlmpc_iterate", "dlmpc_simulate",
            "dlmpc_simulate_device", "dlmpc_get", "dlmpc_put", "dlmpc_zero",
            "dlmpc_last_timing", "dlmpc_stream", "dlmpc_synchronize", "dlmpc_info",
-           "dlmpc_phase_times", "dlmpc_audit")
+           "dlmpc_phase_times", "dlmpc_audit", "dlmpc_get_cols", "dlmpc_put_cols",
+           "dlmpc_finish_step", "dlmpc_set_halo", "dlmpc_halo_pack", "dlmpc_halo_unpack")
 
 _lib = None
 
@@ -98,6 +100,12 @@ def load_library():
     lib.dlmpc_info.argtypes = [vp, _i64p]
     lib.dlmpc_phase_times.argtypes = [vp, _P(C.c_uint64), C.c_int]
     lib.dlmpc_audit.argtypes = [vp, _f64p, _f64p]
+    lib.dlmpc_get_cols.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp]
+    lib.dlmpc_put_cols.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp]
+    lib.dlmpc_finish_step.argtypes = [vp, _f64p, _f64p]
+    lib.dlmpc_set_halo.argtypes = [vp, _i64p, C.c_int64, _i64p, C.c_int64]
+    lib.dlmpc_halo_pack.argtypes = [vp, vp]
+    lib.dlmpc_halo_unpack.argtypes = [vp, vp]
     _lib = lib
     return lib
 
@@ -131,6 +139,8 @@ class DeviceSession:
         p.n_sub, p.n_rows, p.n_cols, p.n_inputs = L.n_sub, L.n_rows, L.n_cols, L.n_inputs
         p.s_pad, p.horizon, p.exact, p.contiguous = L.s_pad, L.horizon, int(L.exact), int(L.contiguous)
         p.rho = L.rho
+        p.own_sub_lo, p.own_sub_hi = L.own_sub
+        p.own_col_lo, p.own_col_hi = L.own_cols
         p.row_start, p.ball_ptr = i64("row_start"), i64("ball_ptr")
         p.ball_idx, p.ball_off = i32("ball_idx"), i32("ball_off")
         p.state_start, p.state_count, p.sub_first_bad = i32("state_start"), i32("state_count"), i32("sub_first_bad")
@@ -262,6 +272,42 @@ class DeviceSession:
                     "dlmpc_audit")
         return float(out[0]), float(out[1]), float(out[2])
 
+    def get_cols(self, which, c0, n, out=None):
+        """ψ or λ of columns [c0, c0+n) of the current iterate (internal layout)."""
+        out = np.empty(n * self.layout.s_pad) if out is None else out
+        self._check(self._lib.dlmpc_get_cols(self._h, int(which), int(c0), int(n), out.ctypes.data),
+                    "dlmpc_get_cols")
+        return out
+
+    def put_cols(self, which, c0, n, values):
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        self._check(self._lib.dlmpc_put_cols(self._h, int(which), int(c0), int(n), v.ctypes.data),
+                    "dlmpc_put_cols")
+
+    def set_halo(self, send_cells, recv_cells):
+        """Register the partitioned path's halo cell lists (internal layout)."""
+        self._send = np.ascontiguousarray(send_cells, dtype=np.int64)
+        self._recv = np.ascontiguousarray(recv_cells, dtype=np.int64)
+        self._check(self._lib.dlmpc_set_halo(self._h, _ptr(self._send, C.c_int64), int(self._send.size),
+                                             _ptr(self._recv, C.c_int64), int(self._recv.size)),
+                    "dlmpc_set_halo")
+
+    def halo_pack(self, out_ptr):
+        """Pack the current (ψ, λ) of the send cells into `out_ptr` (host or
+        device address, 2*n_send doubles)."""
+        self._check(self._lib.dlmpc_halo_pack(self._h, C.c_void_p(out_ptr)), "dlmpc_halo_pack")
+
+    def halo_unpack(self, in_ptr):
+        self._check(self._lib.dlmpc_halo_unpack(self._h, C.c_void_p(in_ptr)), "dlmpc_halo_unpack")
+
+    def finish_step(self):
+        """(u, x_next) for the loaded x after host-driven iterations."""
+        u = np.zeros(self.layout.n_inputs)
+        xn = np.zeros(self.layout.n_cols)
+        self._check(self._lib.dlmpc_finish_step(self._h, _ptr(u, C.c_double), _ptr(xn, C.c_double)),
+                    "dlmpc_finish_step")
+        return u, xn
+
     def zero(self):
         self._check(self._lib.dlmpc_zero(self._h), "dlmpc_zero")
 
@@ -282,7 +328,7 @@ class DeviceSession:
         g = self.info()["grid"]
         out = np.zeros(8 * g, dtype=np.uint64)
         self._check(self._lib.dlmpc_phase_times(self._h, out.ctypes.data_as(_P(C.c_uint64)), int(reset)),
-                    "dlmpc_phase_times", "dlmpc_audit")
+                    "dlmpc_phase_times")
         return out.reshape(g, 8)
 
     def info(self):

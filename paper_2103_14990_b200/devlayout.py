@@ -62,7 +62,8 @@ class DeviceLayout:
     between the internal layout and the reference's padded layouts."""
 
     def __init__(self, system: LtiSystem | None, spec: ProblemSpec, mask: LocalityMask,
-                 classes: ColumnClasses, exact: bool = False, tile_cols: int | None = None):
+                 classes: ColumnClasses, exact: bool = False, tile_cols: int | None = None,
+                 own=None):
         if mask.compact is None:
             raise ValueError("the device layout needs a mask built by build_locality_mask")
         cm = mask.compact
@@ -74,6 +75,11 @@ class DeviceLayout:
         n_sub = int(cm["state_start"].size)
         n_x, n_u = int(cm["n_x"]), int(cm["n_u"])
         self.n_sub, self.n_cols, self.n_inputs, self.horizon = n_sub, n_x, n_u, t
+        # owned subsystem range (graph partition); the rest is a read-only halo
+        own = (0, n_sub) if own is None else (int(own[0]), int(own[1]))
+        self.own_sub = own
+        st0 = cm["state_start"]
+        self.own_cols = (int(st0[own[0]]), int(st0[own[1] - 1] + cm["state_count"][own[1] - 1]))
         s_cnt, u_cnt = cm["state_count"], cm["input_count"]
         rows_per = cm["rows_per_sub"]
         self.n_rows = int(rows_per.sum())
@@ -266,8 +272,10 @@ class DeviceLayout:
 
         # tiles of same-class columns
         self.tile_cols = int(tile_cols) if tile_cols else choose_tile_cols(n_x)
-        order = np.lexsort((np.arange(n_x), dev_class))
-        self.tile_colv = order.astype(np.int32)
+        owned = np.arange(*self.own_cols)
+        order = owned[np.lexsort((owned, dev_class[owned]))]
+        self.tile_colv = np.zeros(n_x, dtype=np.int32)
+        self.tile_colv[:order.size] = order
         tcls, tfirst, tcount = [], [], []
         sorted_cls = dev_class[order]
         bounds = np.flatnonzero(np.r_[True, sorted_cls[1:] != sorted_cls[:-1], True])

@@ -84,3 +84,256 @@ def halo_bytes_per_iteration(plans, mask, s_pad):
     """Bytes each rank receives per ADMM iteration (ψ and λ, full columns)."""
     cnt = mask.compact["state_count"]
     return [int(sum(cnt[subs].sum() for subs in p.recv.values())) * s_pad * 2 * 8 for p in plans]
+
+
+# ---------------------------------------------------------------------------
+# Device-side partitioned solve
+# ---------------------------------------------------------------------------
+
+def _restrict_spec(spec, state_ids, input_ids):
+    from .sls_core import ProblemSpec
+    return ProblemSpec(spec.horizon, spec.state_weights[state_ids], spec.input_weights[input_ids],
+                       spec.terminal_weights[state_ids], spec.state_lo[state_ids], spec.state_hi[state_ids],
+                       spec.input_lo[input_ids], spec.input_hi[input_ids], rho=spec.rho,
+                       eps_pri=spec.eps_pri, eps_dual=spec.eps_dual, max_iters=spec.max_iters)
+
+
+def build_rank_layout(system, spec, mask, plan: RankPlan, exact: bool):
+    """Device layout of rank `plan.rank`'s sub-problem: the window system on
+    `plan.need` (own subsystems + 2d-hop halo, renumbered in ascending global
+    order), its locality mask and column classes, with the owned range
+    marked so the kernels solve only those columns. Host-only (no device)."""
+    from .devlayout import DeviceLayout
+    from .sls_core import _window_system, build_column_classes_structural
+    from .system_model import build_locality_mask
+    sub_ids = np.asarray(plan.need, dtype=np.int64)
+    part = system.partition
+    st = np.asarray(part.state_ranges, dtype=np.int64).reshape(-1, 2)
+    ip = np.asarray(part.input_ranges, dtype=np.int64).reshape(-1, 2)
+    state_ids = np.concatenate([np.arange(*st[i]) for i in sub_ids])
+    in_cnt = ip[sub_ids, 1] - ip[sub_ids, 0]
+    input_ids = np.concatenate([np.arange(*ip[i]) for i in sub_ids]) if in_cnt.sum() else np.zeros(0, np.int64)
+    w = _window_system(system, sub_ids)
+    wspec = _restrict_spec(spec, state_ids, input_ids)
+    wmask = build_locality_mask(w, mask.d, spec.horizon)
+    classes = build_column_classes_structural(w, spec.horizon, wmask)
+    lo, hi = plan.own
+    own_local = (int(np.searchsorted(sub_ids, lo)), int(np.searchsorted(sub_ids, hi)))
+    layout = DeviceLayout(w, wspec, wmask, classes, exact=exact, own=own_local)
+    cm = wmask.compact
+    in_start = np.concatenate([[0], np.cumsum(in_cnt)])[:-1]
+    return (layout, sub_ids, state_ids, input_ids, own_local, cm["state_start"], cm["state_count"],
+            in_start, in_cnt)
+
+
+def _offset_table(layout, sub_ids):
+    """(local row subsystem, local column subsystem) -> offset of the row
+    subsystem's rows inside that column's support (the kernel's ball_off)."""
+    li = np.repeat(np.arange(layout.n_sub), np.diff(layout.ball_ptr))
+    return {(int(a), int(b)): int(o) for a, b, o in zip(li, layout.ball_idx, layout.ball_off)}
+
+
+def halo_cells(mask, plans, src, dst, layout, sub_ids, side):
+    """Internal cell indices of the ψ,λ entries rank `src` sends to rank `dst`
+    each iteration, in the canonical message order, on `side` ("src" or
+    "dst", whose `layout`/`sub_ids` are given).
+
+    Message content: for every halo column of `dst` owned by `src` (global
+    order), the entries of the rows `dst` reads -- rows of the subsystems in
+    both the column's ball and `dst`'s patch (ascending), row by row. A
+    column's support offsets differ between the two windows when its ball is
+    truncated on `dst`'s side, so cells are mapped entry by entry; for patch
+    rows the window distances equal the global ones, so both sides list the
+    same entries."""
+    cm = mask.compact
+    gptr, gidx = cm["ball_ptr"], cm["ball_idx"].astype(np.int64)
+    patch = set(np.asarray(plans[dst].patch).tolist())
+    subs = plans[dst].recv.get(src, np.zeros(0, np.int64))
+    offs = _offset_table(layout, sub_ids)
+    pos = {int(g): k for k, g in enumerate(sub_ids)}
+    out = []
+    sp = layout.s_pad
+    for j in np.asarray(subs).tolist():
+        lj = pos[j]
+        rows_i = [i for i in gidx[gptr[j]:gptr[j + 1]].tolist() if i in patch]
+        for c in range(int(layout.state_start[lj]), int(layout.state_start[lj] + layout.state_count[lj])):
+            for i in rows_i:
+                li = pos[i]
+                base = c * sp + offs[(li, lj)]
+                out.extend(range(base, base + int(layout.row_start[li + 1] - layout.row_start[li])))
+    return np.asarray(out, dtype=np.int64)
+
+
+class RankSolver:
+    """One rank of the graph-partitioned solve: the sub-problem on its own
+    subsystems plus the 2d-hop halo (`build_rank_layout`), uploaded as a
+    device session whose kernels solve only the owned columns; the halo
+    cells are read-only input, refreshed after every iteration from the
+    neighbours' packed messages (`halo_cells` order, ψ,λ interleaved)."""
+
+    def __init__(self, system, spec, mask, plans, rank, strategy="b200", device=0):
+        from .device import DeviceSession
+        from .strategies import ExecStrategy
+        strat = ExecStrategy(strategy) if isinstance(strategy, str) else strategy
+        self.plan = plan = plans[rank]
+        self.spec = spec
+        (self.layout, self.sub_ids, self.state_ids, self.input_ids, self.own_local,
+         self._col_start, self._col_count, self._in_start, self._in_count) = \
+            build_rank_layout(system, spec, mask, plan, strat.exact)
+        self.send_to = sorted(plan.send)
+        self.recv_from = sorted(plan.recv)
+        send = [halo_cells(mask, plans, rank, q, self.layout, self.sub_ids, "src") for q in self.send_to]
+        recv = [halo_cells(mask, plans, q, rank, self.layout, self.sub_ids, "dst") for q in self.recv_from]
+        self.send_off = np.concatenate([[0], np.cumsum([2 * c.size for c in send])]).astype(np.int64)
+        self.recv_off = np.concatenate([[0], np.cumsum([2 * c.size for c in recv])]).astype(np.int64)
+        self.session = DeviceSession(self.layout, strat.device if device is None else device)
+        cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0, np.int64)
+        self.session.set_halo(cat(send), cat(recv))
+
+    @property
+    def send_doubles(self):
+        return int(self.send_off[-1])
+
+    @property
+    def recv_doubles(self):
+        return int(self.recv_off[-1])
+
+    def start_step(self, x_global, cold):
+        if cold:
+            self.session.zero()
+        self.session.set_x(np.asarray(x_global)[self.state_ids])
+
+    def iterate(self):
+        """One ADMM iteration on the owned columns -> local (pri, dual) maxima."""
+        h = self.session.iterate(1)
+        return float(h[0, 0]), float(h[0, 1])
+
+    def pack(self, out_ptr):
+        """All outgoing messages into one buffer; message to `send_to[k]` is
+        [send_off[k], send_off[k+1])."""
+        self.session.halo_pack(out_ptr)
+
+    def unpack(self, in_ptr):
+        """All incoming messages, concatenated in `recv_from` order."""
+        self.session.halo_unpack(in_ptr)
+
+    def finish_step(self):
+        """(global input ids, u, global state ids, x_next) for the owned part."""
+        u, xn = self.session.finish_step()
+        lo, hi = self.own_local
+        s0 = int(self._col_start[lo]); s1 = int(self._col_start[hi - 1] + self._col_count[hi - 1])
+        i0 = int(self._in_start[lo]); i1 = int(self._in_start[hi - 1] + self._in_count[hi - 1])
+        return self.input_ids[i0:i1], u[i0:i1], self.state_ids[s0:s1], xn[s0:s1]
+
+    def close(self):
+        self.session.close()
+
+
+def simulate_partitioned_inprocess(system, spec, mask, x0, t_sim, world, strategy="b200", device=0,
+                                   warm_start=True):
+    """The partitioned closed loop with all ranks driven in lockstep from one
+    process (one device), messages passed through host buffers. Used to
+    check on a single GPU that the partitioned algorithm reproduces the
+    single-domain solve (bit for bit in exact mode) without running ranks
+    whose kernels wait on one another. Returns (states, inputs, step_iters)."""
+    from .errors import NotConverged
+    plans = plan_partition(mask, world)
+    ranks = [RankSolver(system, spec, mask, plans, r, strategy, device) for r in range(world)]
+    try:
+        sbuf = [np.zeros(max(1, rk.send_doubles)) for rk in ranks]
+        rbuf = [np.zeros(max(1, rk.recv_doubles)) for rk in ranks]
+        x = np.asarray(x0, dtype=np.float64)
+        states, inputs, iters = [x], [], []
+        for step in range(t_sim):
+            for rk in ranks:
+                rk.start_step(x, cold=(step == 0 or not warm_start))
+            hist = []
+            for _ in range(spec.max_iters):
+                res = [rk.iterate() for rk in ranks]
+                pri, dual = max(r[0] for r in res), max(r[1] for r in res)
+                hist.append((pri, dual))
+                for r, rk in enumerate(ranks):
+                    rk.pack(sbuf[r].ctypes.data)
+                for r, rk in enumerate(ranks):
+                    for k, src in enumerate(rk.recv_from):
+                        sk = ranks[src].send_to.index(r)
+                        a, b = ranks[src].send_off[sk], ranks[src].send_off[sk + 1]
+                        rbuf[r][rk.recv_off[k]:rk.recv_off[k + 1]] = sbuf[src][a:b]
+                    rk.unpack(rbuf[r].ctypes.data)
+                if pri <= spec.eps_pri and dual <= spec.eps_dual:
+                    break
+            else:
+                raise NotConverged(hist, step=step)
+            u = np.zeros(system.n_inputs)
+            xn = np.zeros(system.n_states)
+            for rk in ranks:
+                iid, uu, sid, xx = rk.finish_step()
+                u[iid] = uu
+                xn[sid] = xx
+            x = xn
+            states.append(x)
+            inputs.append(u)
+            iters.append(len(hist))
+        return np.array(states), np.array(inputs), iters
+    finally:
+        for rk in ranks:
+            rk.close()
+
+
+def simulate_partitioned(system, spec, mask, x0, t_sim, strategy="b200", warm_start=True, group=None):
+    """The partitioned closed loop over torch.distributed ranks (one GPU per
+    rank; NCCL over NVLink): per iteration an all-reduce(max) of the two
+    residuals and one point-to-point message per neighbour rank, packed and
+    unpacked on the device; per MPC step an all-reduce of the disjoint owned
+    parts of (u, x_next). Returns (states, inputs, step_iters) on every rank."""
+    import torch
+    import torch.distributed as dist
+    from .errors import NotConverged
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    nccl = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+    plans = plan_partition(mask, world)
+    rk = RankSolver(system, spec, mask, plans, rank, strategy,
+                    torch.cuda.current_device() if torch.cuda.is_available() else 0)
+    try:
+        sbuf = torch.zeros(max(1, rk.send_doubles), dtype=torch.float64, device=dev)
+        rbuf = torch.zeros(max(1, rk.recv_doubles), dtype=torch.float64, device=dev)
+        x = np.asarray(x0, dtype=np.float64)
+        states, inputs, iters = [x], [], []
+        for step in range(t_sim):
+            rk.start_step(x, cold=(step == 0 or not warm_start))
+            hist = []
+            for _ in range(spec.max_iters):
+                loc = torch.tensor(rk.iterate(), dtype=torch.float64, device=dev)
+                dist.all_reduce(loc, op=dist.ReduceOp.MAX, group=group)
+                rk.pack(sbuf.data_ptr())
+                ops = [dist.P2POp(dist.isend, sbuf[rk.send_off[k]:rk.send_off[k + 1]], q, group)
+                       for k, q in enumerate(rk.send_to)]
+                ops += [dist.P2POp(dist.irecv, rbuf[rk.recv_off[k]:rk.recv_off[k + 1]], q, group)
+                        for k, q in enumerate(rk.recv_from)]
+                if ops:
+                    for w in dist.batch_isend_irecv(ops):
+                        w.wait()
+                if nccl:
+                    torch.cuda.current_stream().synchronize()
+                rk.unpack(rbuf.data_ptr())
+                pri, dual = (float(v) for v in loc.cpu())
+                hist.append((pri, dual))
+                if pri <= spec.eps_pri and dual <= spec.eps_dual:
+                    break
+            else:
+                raise NotConverged(hist, step=step)
+            iid, uu, sid, xx = rk.finish_step()
+            u = torch.zeros(system.n_inputs, dtype=torch.float64, device=dev)
+            xn = torch.zeros(system.n_states, dtype=torch.float64, device=dev)
+            u[torch.as_tensor(iid, device=dev)] = torch.as_tensor(uu, device=dev)
+            xn[torch.as_tensor(sid, device=dev)] = torch.as_tensor(xx, device=dev)
+            dist.all_reduce(u, group=group)         # owned parts are disjoint: the sum is a gather
+            dist.all_reduce(xn, group=group)
+            x = xn.cpu().numpy()
+            states.append(x)
+            inputs.append(u.cpu().numpy())
+            iters.append(len(hist))
+        return np.array(states), np.array(inputs), iters
+    finally:
+        rk.close()

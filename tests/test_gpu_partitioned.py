@@ -1,0 +1,103 @@
+"""Graph-partitioned device solve on one GPU.
+
+Each rank's sub-problem (own subsystems + 2d-hop halo) runs as its own
+device session whose kernels solve only the owned columns; after every
+iteration the ranks exchange packed halo messages (device pack/unpack
+kernels) and reduce the residual maxima. Driven in lockstep from one process
+(`simulate_partitioned_inprocess`) the ranks never wait on one another on
+the device, so one GPU checks the partitioned algorithm: in exact mode the
+closed loop is bit-identical to the reference's (golden fixtures) for every
+world size, which is the C5 determinism claim.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_2103_14990_b200 as pb
+from conftest import golden, random_graph_system
+from oracle import admm_ref
+from paper_2103_14990_b200.partition import simulate_partitioned, simulate_partitioned_inprocess
+
+pytestmark = pytest.mark.gpu
+
+EXACT, FAST = "b200-exact", "b200"
+
+
+def loop_problem(g):
+    n, d, t, t_sim, seed = (int(v) for v in g["config"])
+    system = pb.build_chain_network(n)
+    spec = pb.make_benchmark_spec(system, t, eps=float(g["eps"]), bounded=bool(g["bounded"]))
+    mask = pb.build_locality_mask(system, d, t)
+    return system, spec, mask, t_sim
+
+
+def rel_err(a, b):
+    return float(np.max(np.abs(np.asarray(a) - np.asarray(b)))) / max(1.0, float(np.max(np.abs(b))))
+
+
+@pytest.mark.parametrize("name,world", [("c1_loop_seed1", 2), ("c1_loop_seed1", 3), ("c2_loop_seed1", 2),
+                                        ("c2_loop_seed1", 4), ("d1_loop_n30", 5), ("d4_loop_n20", 2),
+                                        ("unbounded_loop_n8", 2)])
+@pytest.mark.parametrize("variant", [EXACT, FAST])
+def test_partitioned_closed_loop_against_reference(name, world, variant):
+    g = golden(name)
+    system, spec, mask, t_sim = loop_problem(g)
+    states, inputs, iters = simulate_partitioned_inprocess(system, spec, mask, g["x0"], t_sim, world, variant)
+    assert iters == list(g["step_iters"])
+    if variant == EXACT:
+        assert np.array_equal(states, g["states"])
+        assert np.array_equal(inputs, g["inputs"])
+    else:
+        assert rel_err(states, g["states"]) <= 1e-9
+        assert rel_err(inputs, g["inputs"]) <= 1e-9
+
+
+def test_partitioned_fast_matches_single_domain_fast():
+    """World size changes which columns share a CTA, not the per-column
+    arithmetic: the fast path agrees with its own single-domain run."""
+    g = golden("c2_loop_seed1")
+    system, spec, mask, t_sim = loop_problem(g)
+    one, _ = pb.dlmpc_simulate(system, spec, mask, g["x0"], 6, FAST)
+    states, inputs, iters = simulate_partitioned_inprocess(system, spec, mask, g["x0"], 6, 3, FAST)
+    assert iters == list(one.step_iterations)
+    assert rel_err(states, one.states) <= 1e-12
+
+
+@pytest.mark.parametrize("variant", [EXACT, FAST])
+def test_partitioned_generic_graph_against_oracle(variant):
+    rng = np.random.default_rng(11)
+    system = random_graph_system(9, rng)
+    spec = pb.make_benchmark_spec(system, 3)
+    mask = pb.build_locality_mask(system, 2, 3)
+    tables = pb.LayoutTables(mask)
+    cs = pb.precompute_column_solvers(pb.build_dynamics_operator(system, 3), mask)
+    x0 = rng.uniform(0.0, 1.0, system.n_states)
+    ref = admm_ref.simulate(system, spec, tables, cs, x0, 4)
+    states, inputs, iters = simulate_partitioned_inprocess(system, spec, mask, x0, 4, 2, variant)
+    assert iters == ref["step_iterations"]
+    if variant == EXACT:
+        assert np.array_equal(states, ref["states"])
+    else:
+        assert rel_err(states, ref["states"]) <= 1e-9
+
+
+def test_distributed_driver_single_rank_nccl():
+    """The torch.distributed driver (NCCL, world size 1 on this box)."""
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        g = golden("c1_loop_seed1")
+        system, spec, mask, t_sim = loop_problem(g)
+        states, inputs, iters = simulate_partitioned(system, spec, mask, g["x0"], t_sim, EXACT)
+        assert iters == list(g["step_iters"])
+        assert np.array_equal(states, g["states"])
+    finally:
+        dist.destroy_process_group()

@@ -167,3 +167,66 @@ def test_bench_replica_reduction():
     # iterations summed, times maxed over ranks
     for r in (0, 1):
         assert list(res[r]) == [300.0, 4.0, 100.0, 7.0]
+
+
+def _own_cols(cs, cc, own_local):
+    lo, hi = own_local
+    return np.arange(int(cs[lo]), int(cs[hi - 1] + cc[hi - 1]))
+
+
+@pytest.mark.parametrize("n,d,t,world", [(14, 2, 4, 2), (14, 2, 4, 3), (20, 1, 5, 4), (12, 3, 4, 2)])
+def test_rank_window_layouts_reproduce_single_domain(n, d, t, world):
+    """Each rank's window sub-problem (own + 2d-hop halo, `build_rank_layout`)
+    driven on its owned columns only, with halo ψ,λ copied from the owning
+    rank after every iteration, reproduces the single-domain iteration bit
+    for bit (residual maxima and every owned column)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from layout_emulator import LayoutEmulator
+    from paper_2103_14990_b200.partition import build_rank_layout, halo_cells
+    system, spec, mask, L, x0 = build(n, d, t)
+    ref = LayoutEmulator(L)
+    ref.set_x(x0)
+    plans = plan_partition(mask, world)
+    ranks = []
+    owner_of_col = np.empty(L.n_cols, dtype=np.int64)
+    ssid_sub = []
+    for p in plans:
+        RL, sub_ids, sid, iid, own_local, cs, cc, _, _ = build_rank_layout(system, spec, mask, p, True)
+        assert RL.own_sub == own_local
+        oc = _own_cols(cs, cc, own_local)
+        assert RL.own_cols == (int(oc[0]), int(oc[-1]) + 1)
+        owner_of_col[sid[oc]] = len(ranks)
+        ssid_sub.append(sub_ids)
+        em = LayoutEmulator(RL)
+        em.set_x(x0[sid])
+        ranks.append((p, RL, em, sid, oc))
+    for k in range(8):
+        want = ref.iterate()
+        pri = dual = 0.0
+        for p, RL, em, sid, oc in ranks:
+            keep_psi, keep_lam = em.psi.copy(), em.lam.copy()
+            em.iterate()
+            cell = np.zeros(RL.n_cols, dtype=bool)
+            cell[oc] = True
+            cell = np.repeat(cell, RL.s_pad)
+            em.psi = np.where(cell, em.psi, keep_psi)
+            em.lam = np.where(cell, em.lam, keep_lam)
+            pri = max(pri, float(np.max(np.abs(em.phi[cell] - em.psi[cell]))))
+            dual = max(dual, float(np.max(np.abs(em.psi[cell] - em.psi_prev[cell]))))
+        assert (pri, L.rho * dual) == want, k
+        # halo refresh: entry-wise messages from every source rank
+        for di, (p, RL, em, sid, oc) in enumerate(ranks):
+            for si in p.recv:
+                _, SL, sem, ssid, _ = ranks[si]
+                sc = halo_cells(mask, plans, si, di, SL, np.unique(ssid_sub[si]), "src")
+                dc = halo_cells(mask, plans, si, di, RL, np.unique(ssid_sub[di]), "dst")
+                assert sc.size == dc.size > 0
+                em.psi[dc] = sem.psi[sc]
+                em.lam[dc] = sem.lam[sc]
+    for p, RL, em, sid, oc in ranks:
+        for c in oc:
+            g = sid[c]
+            w = min(RL.s_pad, L.s_pad)
+            assert np.array_equal(em.psi[c * RL.s_pad:c * RL.s_pad + w], ref.psi[g * L.s_pad:g * L.s_pad + w])
+            assert np.array_equal(em.lam[c * RL.s_pad:c * RL.s_pad + w], ref.lam[g * L.s_pad:g * L.s_pad + w])
