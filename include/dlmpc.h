@@ -225,8 +225,9 @@ int dlmpc_synchronize(dlmpc_handle* h);
  * Phases: 0 Φ, 1 Ψ prologue, 2 GEMM 1, 3 GEMM 2, 4 epilogue, 5 residual
  * publish, 6 grid barrier. */
 int dlmpc_phase_times(dlmpc_handle* h, uint64_t* out, int reset);
-/* Shape info: n_rows, n_cols, s_pad, n_sub, grid CTAs, tile_cols, smem bytes. */
-int dlmpc_info(const dlmpc_handle* h, int64_t* out7);
+/* Shape info: n_rows, n_cols, s_pad, n_sub, grid CTAs, tile_cols, smem bytes,
+ * kernel mode (0 patch, 1 two-phase, 2 exact, 3 stream), work units. */
+int dlmpc_info(const dlmpc_handle* h, int64_t* out9);
 
 #ifdef __cplusplus
 }

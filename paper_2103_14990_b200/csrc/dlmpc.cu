@@ -81,6 +81,7 @@ using KernelFn = void (*)(DevProblem, RunArgs);
 KernelFn pick_kernel(int mode, int tc) {
   if (mode == kExact) return dlmpc_persistent<8, kExact>;
   if (mode == kPatch) return tc == 16 ? dlmpc_persistent<16, kPatch> : dlmpc_persistent<8, kPatch>;
+  if (mode == kStream) return tc == 16 ? dlmpc_persistent<16, kStream> : dlmpc_persistent<8, kStream>;
   return tc == 16 ? dlmpc_persistent<16, kTwoPhase> : dlmpc_persistent<8, kTwoPhase>;
 }
 
@@ -174,6 +175,9 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
     const int tc0 = tc;   // tile width the chunks below are cut for
     // --- patch work units (class-aware CTA assignment) ----------------------
     std::vector<int> cta_ptr(G + 1, 0), u_lo, u_hi, p_lo, p_hi, u_chunk(1, 0), ch_cls, ch_c0, ch_n;
+    std::vector<int> part_first, part_n;
+    std::vector<int64_t> part_off;
+    long long part_total = 0;
     long long prows_max = 0, np_max = 0;
     if (h->mode == kPatch) {
       auto bfirst = [&](int i) { return pr->ball_idx[pr->ball_ptr[i]]; };
@@ -219,40 +223,139 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           ranges.push_back(o_lo + (int)((long long)n_own * (q + 1) / G));
         }
       }
-      const long long cap_rows = 4096;
-      int b = 0;
-      for (size_t q = 0; q + 1 < ranges.size(); q += 2, ++b) {
-        const int lo = ranges[q], hi = ranges[q + 1];
-        int i = lo;
-        while (i < hi) {
-          int plo = bfirst(i), phi = blast(i) + 1, j = i + 1;
-          while (j < hi) {
-            const int nlo = std::min(plo, bfirst(j)), nhi = std::max(phi, blast(j) + 1);
-            if (pr->row_start[nhi] - pr->row_start[nlo] > cap_rows) break;
-            plo = nlo; phi = nhi; ++j;
-          }
-          u_lo.push_back(i); u_hi.push_back(j); p_lo.push_back(plo); p_hi.push_back(phi);
-          prows_max = std::max<long long>(prows_max, pr->row_start[phi] - pr->row_start[plo]);
-          np_max = std::max<long long>(np_max, phi - plo);
-          const int c_lo = pr->state_start[i], c_hi = pr->state_start[j - 1] + pr->state_count[j - 1];
-          for (int c = c_lo; c < c_hi;) {
-            const int k = pr->col_class[c];
-            int n = 1;
-            while (c + n < c_hi && n < tc && pr->col_class[c + n] == k) ++n;
-            ch_cls.push_back(k); ch_c0.push_back(c); ch_n.push_back(n);
-            c += n;
-          }
-          u_chunk.push_back((int)ch_cls.size());
-          i = j;
-        }
-        cta_ptr[b + 1] = (int)u_lo.size();
+      // subsystems per full chunk when every subsystem has the same column count
+      int gran = 1;
+      {
+        int smin = 1 << 30, smax = 0;
+        for (int i = o_lo; i < o_hi; ++i) { smin = std::min(smin, pr->state_count[i]); smax = std::max(smax, pr->state_count[i]); }
+        if (smin == smax && smax > 0 && tc % smax == 0) gran = tc / smax;
       }
-      for (++b; b <= G; ++b) cta_ptr[b] = cta_ptr[b - 1];
+      auto build_units = [&](long long cap_rows) {
+        std::fill(cta_ptr.begin(), cta_ptr.end(), 0);
+        u_lo.clear(); u_hi.clear(); p_lo.clear(); p_hi.clear(); u_chunk.assign(1, 0);
+        ch_cls.clear(); ch_c0.clear(); ch_n.clear();
+        prows_max = 0; np_max = 0;
+        int b = 0;
+        for (size_t q = 0; q + 1 < ranges.size(); q += 2, ++b) {
+          const int lo = ranges[q], hi = ranges[q + 1];
+          int i = lo;
+          while (i < hi) {
+            int plo = bfirst(i), phi = blast(i) + 1, j = i + 1;
+            while (j < hi) {
+              const int nlo = std::min(plo, bfirst(j)), nhi = std::max(phi, blast(j) + 1);
+              if (pr->row_start[nhi] - pr->row_start[nlo] > cap_rows) break;
+              plo = nlo; phi = nhi; ++j;
+            }
+            // cut units at whole chunks: a unit that stops before its range
+            // ends keeps a multiple of `gran` subsystems (no ragged chunk)
+            if (j < hi && j - i > gran) {
+              j = i + (j - i) / gran * gran;
+              plo = bfirst(i); phi = blast(i) + 1;
+              for (int q = i + 1; q < j; ++q) { plo = std::min(plo, bfirst(q)); phi = std::max(phi, blast(q) + 1); }
+            }
+            u_lo.push_back(i); u_hi.push_back(j); p_lo.push_back(plo); p_hi.push_back(phi);
+            prows_max = std::max<long long>(prows_max, pr->row_start[phi] - pr->row_start[plo]);
+            np_max = std::max<long long>(np_max, phi - plo);
+            const int c_lo = pr->state_start[i], c_hi = pr->state_start[j - 1] + pr->state_count[j - 1];
+            for (int c = c_lo; c < c_hi;) {
+              const int k = pr->col_class[c];
+              int n = 1;
+              while (c + n < c_hi && n < tc && pr->col_class[c + n] == k) ++n;
+              ch_cls.push_back(k); ch_c0.push_back(c); ch_n.push_back(n);
+              c += n;
+            }
+            u_chunk.push_back((int)ch_cls.size());
+            i = j;
+          }
+          cta_ptr[b + 1] = (int)u_lo.size();
+        }
+        for (++b; b <= G; ++b) cta_ptr[b] = cta_ptr[b - 1];
+      };
+      build_units(4096);
+      // stream mode: whole network owned, every class operator resident in
+      // shared memory; the units' Φ-dot partial slots per subsystem
+      // measured crossover (tools/stream_ab.py): a CTA needs >= 2 chunks for
+      // the streamed chunk pipeline to pay (N=3000 at d=3: 29.8 vs 30.1 us/iter;
+      // N=1e4: 94.5 vs 109.5; N=1e5: 897 vs 1170)
+      const char* nostream = getenv("DLMPC_NO_STREAM");
+      const char* forcestream = getenv("DLMPC_FORCE_STREAM");
+      const bool stream_pays = (long long)P.n_cols >= 2LL * tc * G || (forcestream && forcestream[0] == '1');
+      if (!(nostream && nostream[0] == '1') && stream_pays && o_lo == 0 && o_hi == P.n_sub) {
+        // ψ/λ staging: TMA bulk copies with smem rows at the global column
+        // stride when s_pad % 16 is 4 or 12 (FP64 fragment loads stay conflict
+        // free; one copy per chunk and array), else 16-byte cp.async
+        const char* be = getenv("DLMPC_BULK_COPY");
+        const bool bulk = !(be && be[0] == '0') && (P.s_pad % 16 == 4 || P.s_pad % 16 == 12);
+        const int ldk = bulk ? P.s_pad : ld_frag(s8_max), ldy = ld_frag(tc);
+        const int sp_max = 1;   // GEMM 1 tile-parallel for every class (no partials buffer)
+        const long long fixed = ((opr_need + 1) & ~1LL) + 3LL * tc * ldk + (long long)n08_max * ldy +
+                                (sp_max > 1 ? (long long)sp_max * n08_max * tc : 0) + 32 + 8 * tc + 8;
+        long long cap = std::min<long long>(4096, (limit - fixed) / 2);
+        if (const char* e = getenv("DLMPC_STREAM_CAP")) cap = std::min<long long>(cap, atoll(e));
+        long long ch_max = 0, extra = 0;
+        bool ok = false;
+        for (int attempt = 0; attempt < 8 && cap > 0; ++attempt) {
+          build_units(cap);
+          ch_max = 0;
+          for (size_t u = 0; u + 1 < u_chunk.size(); ++u) ch_max = std::max<long long>(ch_max, u_chunk[u + 1] - u_chunk[u]);
+          // chunk table [ch][8 ints], patch table [q][6 doubles], row map [rows] ints
+          extra = 4 * (ch_max + 1) + 6 * np_max + (cap + 2) / 2 + 12;
+          const long long need = fixed + 2 * ((cap + 1) & ~1LL) + extra;
+          if (need <= limit) { ok = prows_max <= cap; break; }
+          cap -= (need - limit + 1) / 2 + 16;
+        }
+        if (ok) {
+          int s_max = 1;
+          for (int k = 0; k < pr->n_classes; ++k) s_max = std::max(s_max, pr->class_s[k]);
+          ok = ldk >= P.s_pad && ldk >= ((s_max + 3) & ~3);
+          std::vector<int> unit_of(P.n_sub, -1);
+          for (size_t u = 0; u < u_lo.size(); ++u)
+            for (int i = u_lo[u]; i < u_hi[u]; ++i) unit_of[i] = (int)u;
+          part_first.assign(P.n_sub, 0); part_n.assign(P.n_sub, 0); part_off.assign(P.n_sub, 0);
+          long long tot = 0;
+          for (int i = 0; ok && i < P.n_sub; ++i) {
+            const int a = unit_of[bfirst(i)], z = unit_of[blast(i)];
+            ok = a >= 0 && z >= a;
+            part_first[i] = a; part_n[i] = z - a + 1; part_off[i] = tot;
+            tot += (long long)(z - a + 1) * (pr->row_start[i + 1] - pr->row_start[i]);
+          }
+          part_total = tot;
+          if (ok) {
+            h->mode = kStream;
+            P.ldk = ldk; P.ldy = ldy; P.split_max = sp_max;
+            P.s8_max = s8_max; P.n08_max = n08_max;
+            long long off = (opr_need + 1) & ~1LL;
+            P.opr_cap = (int)opr_need;
+            P.off_k = (int)off; off += 3LL * tc * ldk;
+            P.off_y = (int)off; off += (long long)n08_max * ldy;
+            P.off_yp = (int)off; off += sp_max > 1 ? (long long)sp_max * n08_max * tc : 0;
+            P.off_red = (int)off; off += 32;
+            P.off_meta = (int)off; off += 8 * tc;
+            P.off_patch = (int)off; off += (cap + 1) & ~1LL;
+            P.off_cpatch = (int)off; off += (cap + 1) & ~1LL;
+            P.patch_cap = (int)cap;
+            P.off_chtab = (int)off; off += 4 * (ch_max + 1); P.ch_cap = (int)(ch_max + 1);
+            P.off_ptab = (int)off; off += 6 * np_max; P.np_cap = (int)np_max;
+            P.off_rowq = (int)off; off += (cap + 2) / 2;
+            off = (off + 1) & ~1LL;
+            P.off_bar = (int)off; off += 4;
+            P.bulk_copy = bulk ? 1 : 0;
+            P.cache_phi = 0; P.stash_bufs = 0; P.off_stash = (int)off; P.off_phimeta = (int)off;
+            P.off_ex = (int)off;
+            h->smem_bytes = (int)(off * 8);
+            P.tile_cols = tc;
+          } else {
+            build_units(4096);
+          }
+        } else {
+          build_units(4096);
+        }
+      }
       h->n_units = (int)u_lo.size();
     }
     bool one_unit = true;
     for (int q = 0; q < G; ++q) one_unit = one_unit && (cta_ptr[q + 1] - cta_ptr[q] <= 1);
-    for (;;) {
+    for (; h->mode != kStream;) {
       const int ldk = ld_frag(s8_max), ldy = ld_frag(tc);
       int split_max = 1;
       for (int k = 0; k < pr->n_classes; ++k) {
@@ -301,7 +404,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       break;
     }
     // chunks were cut for the initial tile width; re-cut if it shrank
-    if (h->mode == kPatch && P.tile_cols != tc0) {
+    if ((h->mode == kPatch || h->mode == kStream) && P.tile_cols != tc0) {
       std::vector<int> nc_cls, nc_c0, nc_n, nu(1, 0);
       for (size_t u = 0; u + 1 < u_chunk.size(); ++u) {
         for (int ch = u_chunk[u]; ch < u_chunk[u + 1]; ++ch)
@@ -313,7 +416,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       }
       ch_cls.swap(nc_cls); ch_c0.swap(nc_c0); ch_n.swap(nc_n); u_chunk.swap(nu);
     }
-    if (h->mode == kPatch) {
+    if (h->mode == kPatch || h->mode == kStream) {
       int rc;
       if ((rc = upload(h, cta_ptr.data(), cta_ptr.size(), &P.cta_unit_ptr)) ||
           (rc = upload(h, u_lo.data(), u_lo.size(), &P.unit_sub_lo)) ||
@@ -325,6 +428,18 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           (rc = upload(h, ch_c0.data(), ch_c0.size(), &P.chunk_col0)) ||
           (rc = upload(h, ch_n.data(), ch_n.size(), &P.chunk_n)))
         return rc;
+      if (h->mode == kStream) {
+        if ((rc = upload(h, part_first.data(), part_first.size(), &P.part_first)) ||
+            (rc = upload(h, part_n.data(), part_n.size(), &P.part_n)) ||
+            (rc = upload(h, part_off.data(), part_off.size(), &P.part_off)))
+          return rc;
+        for (int q = 0; q < 2; ++q) {
+          void* ptr = nullptr;
+          CUDA_OR_FAIL(h, cudaMalloc(&ptr, sizeof(double) * std::max<long long>(1, part_total)));
+          h->allocs.push_back(ptr);
+          P.part_buf[q] = static_cast<double*>(ptr);
+        }
+      }
     }
   }
   KernelFn fn = pick_kernel(h->mode, P.tile_cols);
@@ -777,6 +892,7 @@ int dlmpc_info(const dlmpc_handle* h, int64_t* out) {
   if (!h || !out) return DLMPC_BAD_ARGUMENT;
   out[0] = h->P.n_rows; out[1] = h->P.n_cols; out[2] = h->P.s_pad; out[3] = h->P.n_sub;
   out[4] = h->grid; out[5] = h->P.tile_cols; out[6] = h->smem_bytes;
+  out[7] = h->mode; out[8] = h->n_units;
   return DLMPC_OK;
 }
 

@@ -53,6 +53,8 @@ constexpr int kBadNone = 0x7f7f7f7f;   // cudaMemset(0x7f) pattern = "no infeasi
 constexpr int kMG1 = 4;                // m-tiles per GEMM-1 work unit
 constexpr int kMG2 = 2;                // m-tiles per GEMM-2 work unit
 
+enum Mode { kPatch = 0, kTwoPhase = 1, kExact = 2, kStream = 3 };
+
 struct DevProblem {
   int n_sub, n_rows, n_cols, n_inputs, s_pad, exact, contiguous, d_row;
   int own_sub_lo, own_sub_hi, own_col_lo, own_col_hi;   // owned range (graph partition)
@@ -93,6 +95,18 @@ struct DevProblem {
   int s8_max, n08_max, ldk, ldy, split_max, patch_cap, cache_phi;
   int off_k, off_y, off_yp, off_red, off_meta, off_patch, off_phimeta, off_ex;
   int off_stash, stash_bufs;   // cp.async staging of chunk ψ,λ: [bufs][TC][2][ldk]
+  // stream mode: per-unit partials of the next iteration's Φ dots. Subsystem
+  // i's rows receive one partial from each unit a_i..a_i+n_i-1 whose patch
+  // holds i, stored at part_off[i] + (unit - a_i) * rows_i + l; ping-pong
+  // by iteration parity.
+  const int64_t* part_off; const int* part_first; const int* part_n;
+  double* part_buf[2];
+  int off_cpatch;
+  int off_chtab, ch_cap;       // per-unit chunk table: [ch_cap][8] ints (k, c0, nt, S, n08, ldn)
+  int off_ptab, np_cap;        // per-unit patch-subsystem table: [np_cap][6] doubles
+  int off_rowq;                // per patch row: its patch-subsystem index (int)
+  int off_bar;                 // 3 mbarriers (ψ buffers, λ buffer)
+  int bulk_copy;               // stream staging by TMA bulk copies (1) or cp.async (0)
 };
 
 struct RunArgs {
@@ -118,6 +132,27 @@ __device__ __forceinline__ void cp_async16(double* smem_dst, const double* gmem_
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" :: "n"(N) : "memory"); }
+
+// TMA 1-D bulk copies completing on shared-memory mbarriers (stream mode).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile("{\n .reg .pred P1;\n LAB_WAIT:\n"
+               " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+               " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n}\n" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 // Stage ψ,λ of nt consecutive columns starting at c0 into `st`
 // ([t][ψ|λ][ldk]) with 16-byte cp.async copies (bypassing L1, like ld.cg);
@@ -311,6 +346,156 @@ __device__ void phi_stage_global(const DevProblem& P, int b, const double* x) {
 }
 
 // ---------------------------------------------------------------------------
+// The two FP64 tensor-core GEMMs of the Ψ projection against a class's
+// null-space basis N ([S8][ldn] at `nop`, smem or global):
+//   GEMM 1  Y[a][t] = sum_p N[p][a] K[t][p]     (M = n0, N = TC, K = S)
+//   GEMM 2  O[t][p] = sum_a N[p][a] Y[a][t]     (M = S,  N = TC, K = n0)
+// K is read from kt [TC][ldk]; Y goes to yb [n08][ldy] (split-K partials in
+// yp). GEMM 2 hands its accumulators to `epi` (prefetch(mt) before the k
+// loop, store(mt, nn, c0, c1) after: rows mt*8+g, columns nn*8+2tig, +1).
+// ---------------------------------------------------------------------------
+struct NoHook { __device__ __forceinline__ void operator()() const {} };
+
+template <int TC, class Hook = NoHook>
+__device__ __forceinline__ void gemm1(const DevProblem& P, int SK, int n08, int ldn, const double* nop,
+                                      const double* kt, int ldk, double* yb, int ldy, double* yp,
+                                      const Hook& before_sync = Hook()) {
+  constexpr int NTN = TC / 8;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  const int mt1 = n08 >> 3, ks1 = SK >> 2;   // SK: K extent, a multiple of 4
+  if (mt1 * NTN >= 12 || P.split_max == 1) {
+    // enough (m, n) tiles to keep the DMMA pipe busy (or no room for split-K
+    // partials): one tile per warp over the full K with two interleaved
+    // accumulator chains, no split-K pass
+    for (int u = warp; u < mt1 * NTN; u += kWarps) {
+      const int mt = u / NTN, nn = u - (u / NTN) * NTN;
+      double c0a = 0.0, c1a = 0.0, c0b = 0.0, c1b = 0.0;
+      int ks = 0;
+      for (; ks + 1 < ks1; ks += 2) {
+        const int p0 = ks * 4 + tig, p1 = p0 + 4;
+        const double a0 = nop[p0 * ldn + mt * 8 + g], b0 = kt[(nn * 8 + g) * ldk + p0];
+        const double a1 = nop[p1 * ldn + mt * 8 + g], b1 = kt[(nn * 8 + g) * ldk + p1];
+        dmma(c0a, c1a, a0, b0);
+        dmma(c0b, c1b, a1, b1);
+      }
+      if (ks < ks1) {
+        const int p0 = ks * 4 + tig;
+        dmma(c0a, c1a, nop[p0 * ldn + mt * 8 + g], kt[(nn * 8 + g) * ldk + p0]);
+      }
+      yb[(mt * 8 + g) * ldy + nn * 8 + 2 * tig] = c0a + c0b;
+      yb[(mt * 8 + g) * ldy + nn * 8 + 2 * tig + 1] = c1a + c1b;
+    }
+    before_sync();
+    __syncthreads();
+    return;
+  }
+  const int groups1 = (mt1 + kMG1 - 1) / kMG1;
+  int split = 1;
+  while (groups1 * split * 2 <= kWarps && split < P.split_max) split <<= 1;
+  for (int u = warp; u < groups1 * split; u += kWarps) {
+    const int grp = u / split, sl = u - grp * split;
+    const int mt0 = grp * kMG1;
+    double acc[kMG1][NTN][2];
+#pragma unroll
+    for (int m = 0; m < kMG1; ++m)
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
+#pragma unroll 2
+    for (int ks = sl; ks < ks1; ks += split) {
+      const int p = ks * 4 + tig;
+      double bf[NTN];
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) bf[nn] = kt[(nn * 8 + g) * ldk + p];
+#pragma unroll
+      for (int m = 0; m < kMG1; ++m) {
+        if (mt0 + m < mt1) {
+          const double af = nop[p * ldn + (mt0 + m) * 8 + g];
+#pragma unroll
+          for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
+        }
+      }
+    }
+    double* dst = split == 1 ? yb : yp + static_cast<size_t>(sl) * P.n08_max * TC;
+    const int ld = split == 1 ? ldy : TC;
+#pragma unroll
+    for (int m = 0; m < kMG1; ++m) {
+      if (mt0 + m < mt1) {
+#pragma unroll
+        for (int nn = 0; nn < NTN; ++nn) {
+          dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig] = acc[m][nn][0];
+          dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig + 1] = acc[m][nn][1];
+        }
+      }
+    }
+  }
+  before_sync();
+  __syncthreads();
+  if (split > 1) {
+    for (int idx = tid; idx < n08 * TC; idx += kThreads) {
+      const int a = idx / TC, t = idx - a * TC;
+      double v = yp[idx];
+      for (int sl = 1; sl < split; ++sl) v += yp[static_cast<size_t>(sl) * P.n08_max * TC + idx];
+      yb[a * ldy + t] = v;
+    }
+    __syncthreads();
+  }
+}
+
+template <int TC, class Epi>
+__device__ __forceinline__ void gemm2(int S8, int n08, int ldn, const double* nop, const double* yb, int ldy,
+                                      Epi& epi) {
+  constexpr int NTN = TC / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  const int mt2 = S8 >> 3, ks2 = n08 >> 2;
+  for (int mb = warp; mb < mt2; mb += kWarps * kMG2) {
+#pragma unroll
+    for (int m = 0; m < kMG2; ++m) epi.prefetch(m, mb + m * kWarps);
+    double acc[kMG2][NTN][2];
+#pragma unroll
+    for (int m = 0; m < kMG2; ++m)
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
+#pragma unroll 2
+    for (int ks = 0; ks < ks2; ++ks) {
+      const int a = ks * 4 + tig;
+      double bf[NTN];
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) bf[nn] = yb[a * ldy + nn * 8 + g];
+#pragma unroll
+      for (int m = 0; m < kMG2; ++m) {
+        const int mt = mb + m * kWarps;
+        if (mt < mt2) {
+          const double af = nop[(mt * 8 + g) * ldn + a];
+#pragma unroll
+          for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kMG2; ++m) {
+      const int mt = mb + m * kWarps;
+      if (mt < mt2) {
+#pragma unroll
+        for (int nn = 0; nn < NTN; ++nn) epi.store(m, mt, nn, acc[m][nn][0], acc[m][nn][1]);
+      }
+    }
+  }
+}
+
+// GEMM-2 epilogue of the patch/two-phase kernels: O back into kt.
+struct StoreO {
+  double* kt; int ldk;
+  __device__ __forceinline__ void prefetch(int, int) const {}
+  __device__ __forceinline__ void store(int, int mt, int nn, double c0, double c1) const {
+    const int lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+    kt[(nn * 8 + 2 * tig) * ldk + mt * 8 + g] = c0;
+    kt[(nn * 8 + 2 * tig + 1) * ldk + mt * 8 + g] = c1;
+  }
+};
+
+// ---------------------------------------------------------------------------
 // Fast column chunk: TC columns of one class. The caller fills the per-column
 // metadata (smem) -- m_pos[t] = column base offset c*s_pad, m_s[t] = offset
 // of support slot 0 in the s source, m_q[t] = q offset, m_x[t] = x_c -- for
@@ -380,119 +565,11 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
   }
   __syncthreads();
   PT_LAP(P, 1)
-  // GEMM 1: Y[a][t] = sum_p N[p][a] K[t][p]  (M = n0, N = TC, K = S)
-  const int mt1 = n08 >> 3, ks1 = S8 >> 2;
-  if (mt1 * NTN >= 12) {
-    // enough (m, n) tiles to keep the DMMA pipe busy: one tile per warp over
-    // the full K with two interleaved accumulator chains, no split-K pass
-    for (int u = warp; u < mt1 * NTN; u += kWarps) {
-      const int mt = u / NTN, nn = u - (u / NTN) * NTN;
-      double c0a = 0.0, c1a = 0.0, c0b = 0.0, c1b = 0.0;
-      int ks = 0;
-      for (; ks + 1 < ks1; ks += 2) {
-        const int p0 = ks * 4 + tig, p1 = p0 + 4;
-        const double a0 = nop[p0 * ldn + mt * 8 + g], b0 = kt[(nn * 8 + g) * ldk + p0];
-        const double a1 = nop[p1 * ldn + mt * 8 + g], b1 = kt[(nn * 8 + g) * ldk + p1];
-        dmma(c0a, c1a, a0, b0);
-        dmma(c0b, c1b, a1, b1);
-      }
-      if (ks < ks1) {
-        const int p0 = ks * 4 + tig;
-        dmma(c0a, c1a, nop[p0 * ldn + mt * 8 + g], kt[(nn * 8 + g) * ldk + p0]);
-      }
-      yb[(mt * 8 + g) * ldy + nn * 8 + 2 * tig] = c0a + c0b;
-      yb[(mt * 8 + g) * ldy + nn * 8 + 2 * tig + 1] = c1a + c1b;
-    }
-    __syncthreads();
-  } else {
-    const int mt1 = n08 >> 3, ks1 = S8 >> 2;
-    const int groups1 = (mt1 + kMG1 - 1) / kMG1;
-    int split = 1;
-    while (groups1 * split * 2 <= kWarps && split < P.split_max) split <<= 1;
-    for (int u = warp; u < groups1 * split; u += kWarps) {
-      const int grp = u / split, sl = u - grp * split;
-      const int mt0 = grp * kMG1;
-      double acc[kMG1][NTN][2];
-#pragma unroll
-      for (int m = 0; m < kMG1; ++m)
-#pragma unroll
-        for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
-#pragma unroll 2
-      for (int ks = sl; ks < ks1; ks += split) {
-        const int p = ks * 4 + tig;
-        double bf[NTN];
-#pragma unroll
-        for (int nn = 0; nn < NTN; ++nn) bf[nn] = kt[(nn * 8 + g) * ldk + p];
-#pragma unroll
-        for (int m = 0; m < kMG1; ++m) {
-          if (mt0 + m < mt1) {
-            const double af = nop[p * ldn + (mt0 + m) * 8 + g];
-#pragma unroll
-            for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
-          }
-        }
-      }
-      double* dst = split == 1 ? yb : yp + static_cast<size_t>(sl) * P.n08_max * TC;
-      const int ld = split == 1 ? ldy : TC;
-#pragma unroll
-      for (int m = 0; m < kMG1; ++m) {
-        if (mt0 + m < mt1) {
-#pragma unroll
-          for (int nn = 0; nn < NTN; ++nn) {
-            dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig] = acc[m][nn][0];
-            dst[((mt0 + m) * 8 + g) * ld + nn * 8 + 2 * tig + 1] = acc[m][nn][1];
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (split > 1) {
-      for (int idx = tid; idx < n08 * TC; idx += kThreads) {
-        const int a = idx / TC, t = idx - a * TC;
-        double v = yp[idx];
-        for (int sl = 1; sl < split; ++sl) v += yp[static_cast<size_t>(sl) * P.n08_max * TC + idx];
-        yb[a * ldy + t] = v;
-      }
-      __syncthreads();
-    }
-  }
+  gemm1<TC>(P, S8, n08, ldn, nop, kt, ldk, yb, ldy, yp);
   PT_LAP(P, 2)
   // GEMM 2: O[t][p] = sum_a N[p][a] Y[a][t]  (M = S, N = TC, K = n0) -> kt
-  const int mt2 = S8 >> 3, ks2 = n08 >> 2;
-  for (int mb = warp; mb < mt2; mb += kWarps * kMG2) {
-    double acc[kMG2][NTN][2];
-#pragma unroll
-    for (int m = 0; m < kMG2; ++m)
-#pragma unroll
-      for (int nn = 0; nn < NTN; ++nn) { acc[m][nn][0] = 0.0; acc[m][nn][1] = 0.0; }
-#pragma unroll 2
-    for (int ks = 0; ks < ks2; ++ks) {
-      const int a = ks * 4 + tig;
-      double bf[NTN];
-#pragma unroll
-      for (int nn = 0; nn < NTN; ++nn) bf[nn] = yb[a * ldy + nn * 8 + g];
-#pragma unroll
-      for (int m = 0; m < kMG2; ++m) {
-        const int mt = mb + m * kWarps;
-        if (mt < mt2) {
-          const double af = nop[(mt * 8 + g) * ldn + a];
-#pragma unroll
-          for (int nn = 0; nn < NTN; ++nn) dmma(acc[m][nn][0], acc[m][nn][1], af, bf[nn]);
-        }
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < kMG2; ++m) {
-      const int mt = mb + m * kWarps;
-      if (mt < mt2) {
-#pragma unroll
-        for (int nn = 0; nn < NTN; ++nn) {
-          kt[(nn * 8 + 2 * tig) * ldk + mt * 8 + g] = acc[m][nn][0];
-          kt[(nn * 8 + 2 * tig + 1) * ldk + mt * 8 + g] = acc[m][nn][1];
-        }
-      }
-    }
-  }
+  StoreO epi{kt, ldk};
+  gemm2<TC>(S8, n08, ldn, nop, yb, ldy, epi);
   __syncthreads();
   PT_LAP(P, 3)
   // epilogue: ψ' = q + O, λ' = λ + (φ - ψ'), residuals (admm.py:186, 207, 216-217)
@@ -554,6 +631,19 @@ __device__ __forceinline__ bool stage_operator(const DevProblem& P, int k, doubl
     cur = k;
   }
   return true;
+}
+
+// stage_operator with the class sizes already known (no global loads)
+__device__ __forceinline__ void stage_operator_sized(const DevProblem& P, int k, int S8, int ldn, double* smem,
+                                                     int& cur) {
+  if (k == cur) return;
+  __syncthreads();
+  const long long n = static_cast<long long>(S8) * ldn;
+  const double2* src = reinterpret_cast<const double2*>(P.null_pool + P.class_null_off[k]);
+  double2* dst = reinterpret_cast<double2*>(smem);
+  for (long long q = threadIdx.x; q < n / 2; q += kThreads) dst[q] = __ldg(src + q);
+  __syncthreads();
+  cur = k;
 }
 
 template <int TC, bool S_GLOBAL>
@@ -759,6 +849,329 @@ __device__ void patch_iteration(const DevProblem& P, int b, const double* x, int
   PT_LAP(P, 5)
 }
 
+
+// ---------------------------------------------------------------------------
+// Stream mode (fast path, wide contiguous units; chosen by the host when
+// every d-hop ball meets at most two units). Per chunk of TC same-class
+// columns:
+//   ψ staged by cp.async one chunk ahead -> K = ψ + s·x in place (= φ + λ,
+//   one rounding) -> GEMM 1 -> GEMM 2 whose accumulators go straight into
+//   the epilogue (ψ, λ, q prefetched into registers before the GEMM-2 k
+//   loop): ψ' = q + O, λ' = λ + (φ - ψ'), residual maxima, ψ', λ' stored,
+//   and v' = ψ' - λ' left in the stage buffer -> a banded pass adds
+//   Σ_t v'(r,t)·x_t to the unit's per-row partial of the NEXT iteration's Φ
+//   dot (ascending column order). At the unit's end each partial goes to the
+//   unit's own slot of the row; the next Φ sums a row's slots in unit order
+//   (deterministic, no atomics). From the second iteration of a step on, Φ
+//   reads a few partials per row instead of the row's whole (ψ, λ)
+//   neighbourhood.
+// ---------------------------------------------------------------------------
+// Stage one array's columns [c0, c0+nt) (s_pad doubles each) into `st`
+// ([t][ldk]) with TMA bulk copies on `bar` (thread 0 issues; the caller has
+// synchronised the CTA after the buffer's last generic-proxy use).
+__device__ __forceinline__ void stash_cols_bulk(const DevProblem& P, int c0, int nt, const double* src,
+                                                double* st, unsigned long long* bar) {
+  if (threadIdx.x == 0) {
+    const unsigned bytes = static_cast<unsigned>(P.s_pad) * 8u;
+    fence_proxy_async();
+    mbar_expect_tx(bar, bytes * nt);
+    if (P.ldk == P.s_pad)   // consecutive columns are one contiguous range
+      bulk_load(st, src + static_cast<size_t>(c0) * P.s_pad, bytes * nt, bar);
+    else
+      for (int t = 0; t < nt; ++t)
+        bulk_load(st + t * P.ldk, src + static_cast<size_t>(c0 + t) * P.s_pad, bytes, bar);
+  }
+}
+
+// Same with 16-byte cp.async copies from every thread (one commit group).
+__device__ __forceinline__ void stash_cols_issue(const DevProblem& P, int c0, int nt, const double* src,
+                                                 double* st) {
+  const int pairs = P.s_pad >> 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = warp; t < nt; t += kWarps) {
+    const double* g = src + static_cast<size_t>(c0 + t) * P.s_pad;
+    double* d = st + t * P.ldk;
+    for (int pr = lane; pr < pairs; pr += 32) cp_async16(d + 2 * pr, g + 2 * pr);
+  }
+  cp_async_commit();
+}
+
+// GEMM-2 epilogue of the stream kernel, all operands in shared memory:
+// kt holds K = φ + λ, lt holds λ (then receives v' = ψ' - λ').
+//   ψ' = q + O;  λ' = λ + (φ - ψ') = K - ψ';  pri: |λ' - λ| = |φ - ψ'|;
+//   dual: |ψ' - ψ| with ψ = K - s·x.
+template <int TC>
+struct StreamEpi {
+  static constexpr int NTN = TC / 8;
+  double* psi_n; double* lam_n; const double* q_pool;
+  const long long* m_pos; const long long* m_s; const long long* m_q; const double* m_x;
+  const double* s_patch; const double* kt; double* lt; int ldk, S, nt;
+  double pri_m, dual_m;
+  double qv[kMG2][NTN][2];
+  __device__ __forceinline__ void prefetch(int m, int mt) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+    const int p = mt * 8 + g;
+#pragma unroll
+    for (int nn = 0; nn < NTN; ++nn)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int t = nn * 8 + 2 * tig + e;
+        qv[m][nn][e] = (p < S && t < nt) ? __ldg(q_pool + m_q[t] + p) : 0.0;
+      }
+  }
+  __device__ __forceinline__ void store(int m, int mt, int nn, double c0, double c1) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+    const int p = mt * 8 + g;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int t = nn * 8 + 2 * tig + e;
+      if (p < S && t < nt) {
+        const double kv = kt[t * ldk + p], lm = lt[t * ldk + p];
+        const double pn = qv[m][nn][e] + (e ? c1 : c0);
+        const double ln = __dsub_rn(kv, pn);
+        const double ps = fma(-s_patch[m_s[t] + p], m_x[t], kv);
+        const long long pos = m_pos[t] + p;
+        psi_n[pos] = pn;
+        lam_n[pos] = ln;
+        pri_m = fmax(pri_m, fabs(__dsub_rn(ln, lm)));
+        dual_m = fmax(dual_m, fabs(__dsub_rn(pn, ps)));
+        lt[t * ldk + p] = __dsub_rn(pn, ln);
+      }
+    }
+  }
+};
+
+// λ(ch) must have landed before GEMM 1's closing barrier: mbarrier phase
+// (bulk copies) or cp.async groups (allowing the younger ψ(ch+1) group).
+struct LamWait {
+  unsigned long long* bar; unsigned phase; bool bulk, has_next;
+  __device__ __forceinline__ void operator()() const {
+    if (bulk) mbar_wait(bar, phase);
+    else if (has_next) cp_async_wait<1>();
+    else cp_async_wait<0>();
+  }
+};
+
+template <int TC>
+__device__ void stream_iteration(const DevProblem& P, int b, const double* x, int it, double* smem, int& cur,
+                                 unsigned (&ph)[3]) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* s_patch = smem + P.off_patch;
+  double* c_patch = smem + P.off_cpatch;
+  double* yb = smem + P.off_y;
+  double* yp = smem + P.off_yp;
+  long long* meta0 = reinterpret_cast<long long*>(smem + P.off_meta);   // [2][4][TC]
+  int* chtab = reinterpret_cast<int*>(smem + P.off_chtab);               // [ch][8]
+  double* ptab = smem + P.off_ptab;                                      // [q][6]
+  int* rowq = reinterpret_cast<int*>(smem + P.off_rowq);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + P.off_bar);   // ψ0, ψ1, λ
+  const int ldk = P.ldk;
+  double* psi_st = smem + P.off_k;                  // [2][TC][ldk]
+  double* lam_st = psi_st + 2 * TC * ldk;           // [TC][ldk]
+  const double* psi = P.psi[b];
+  const double* lam = P.lam[b];
+  double* part_out = P.part_buf[it & 1];
+  const double* part_in = P.part_buf[(it & 1) ^ 1];
+  const double rho = P.rho;
+  double pri_m = 0.0, dual_m = 0.0;
+  PT_DECL
+  for (int un = P.cta_unit_ptr[blockIdx.x]; un < P.cta_unit_ptr[blockIdx.x + 1]; ++un) {
+    PT_START
+    const int own_lo = P.unit_sub_lo[un], own_hi = P.unit_sub_hi[un];
+    const int plo = P.unit_patch_lo[un], phi_ = P.unit_patch_hi[un];
+    const int npq = phi_ - plo;
+    const long long prow0 = P.row_start[plo];
+    const int prows = static_cast<int>(P.row_start[phi_] - prow0);
+    const int ch_a = P.unit_chunk_ptr[un], ch_b = P.unit_chunk_ptr[un + 1];
+    const int nch = ch_b - ch_a;
+    // one round trip for the unit's control data: chunk table, patch table
+    for (int q = tid; q < nch; q += kThreads) {
+      const int k = P.chunk_class[ch_a + q];
+      const int S = P.class_s[k];
+      int* e = chtab + 8 * q;
+      e[0] = k; e[1] = P.chunk_col0[ch_a + q]; e[2] = P.chunk_n[ch_a + q];
+      e[3] = S; e[4] = (P.class_n0[k] + 7) & ~7; e[5] = P.class_ldn[k];
+    }
+    for (int q = tid; q < npq; q += kThreads) {
+      const int i = plo + q;
+      const long long r0 = P.row_start[i];
+      double* e = ptab + 6 * q;
+      int* ei = reinterpret_cast<int*>(e);
+      ei[0] = static_cast<int>(r0 - prow0);                       // local row offset
+      ei[1] = static_cast<int>(P.row_start[i + 1] - r0);          // rows
+      ei[2] = P.part_n[i];
+      ei[3] = un - P.part_first[i];                               // this unit's slot
+      reinterpret_cast<long long*>(e)[2] = P.part_off[i];
+      e[3] = ld_cg(P.ada + i);
+      reinterpret_cast<long long*>(e)[4] = r0;
+      ei[10] = (i >= own_lo && i < own_hi);
+    }
+    __syncthreads();
+    for (int q = warp; q < npq; q += kWarps) {
+      const int* ei = reinterpret_cast<const int*>(ptab + 6 * q);
+      for (int l = lane; l < ei[1]; l += 32) rowq[ei[0] + l] = q;
+    }
+    for (int r = tid; r < prows; r += kThreads) c_patch[r] = 0.0;
+    int k = 0, c0 = 0, nt = 0;
+    if (nch > 0) {
+      k = chtab[0]; c0 = chtab[1]; nt = chtab[2];
+      if (P.bulk_copy) {
+        stash_cols_bulk(P, c0, nt, psi, psi_st, bars + 0);
+        stash_cols_bulk(P, c0, nt, lam, lam_st, bars + 2);
+      } else {
+        stash_cols_issue(P, c0, nt, psi, psi_st);
+        stash_cols_issue(P, c0, nt, lam, lam_st);
+      }
+      if (tid < TC) {
+        long long* mm = meta0;
+        long long pos = 0, s0 = 0, q0 = 0;
+        double xc = 0.0;
+        if (tid < nt) {
+          const int c = c0 + tid;
+          pos = static_cast<long long>(c) * P.s_pad;
+          s0 = P.col_rowbase[c] - prow0;
+          q0 = static_cast<long long>(P.col_vec[c]) * P.s_pad;
+          xc = ld_cg(x + c);
+        }
+        mm[tid] = pos; mm[TC + tid] = s0; mm[2 * TC + tid] = q0;
+        reinterpret_cast<double*>(mm)[3 * TC + tid] = xc;
+      }
+    }
+    __syncthreads();
+    // Φ scales of the patch rows
+    if (it == 0) {
+      for (int i = plo + warp; i < phi_; i += kWarps) {
+        const int r_off = static_cast<int>(P.row_start[i] - prow0);
+        double* dst = s_patch + r_off;
+        double* gdst = (i >= own_lo && i < own_hi) ? P.s_row + P.row_start[i] : nullptr;
+        auto out = [dst, gdst](int l, double s) {
+          dst[l] = s;
+          if (gdst) gdst[l] = s;
+        };
+        phi_rows_of<false>(P, i, psi, lam, x, out);
+      }
+    } else {
+      // from the per-unit dot partials of the last iteration (slot order)
+      for (int r = tid; r < prows; r += kThreads) {
+        const int q = rowq[r];
+        const double* e = ptab + 6 * q;
+        const int* ei = reinterpret_cast<const int*>(e);
+        const int l = r - ei[0], nr = ei[1], np = ei[2];
+        const long long grow = reinterpret_cast<const long long*>(e)[4] + l;
+        const double* pb = part_in + reinterpret_cast<const long long*>(e)[2] + l;
+        const double w = P.row_w[grow], lo = P.row_lo[grow], hi = P.row_hi[grow];
+        double c = ld_cg(pb);
+        for (int sl = 1; sl < np; ++sl) c += ld_cg(pb + sl * nr);
+        const double ada = e[3];
+        const double y0 = __ddiv_rn(__dmul_rn(rho, c), __dadd_rn(rho, __dmul_rn(__dmul_rn(2.0, w), ada)));
+        const double y = fmin(fmax(y0, lo), hi);
+        const double sv = ada > 0.0 ? __ddiv_rn(__dsub_rn(y, c), ada) : 0.0;
+        s_patch[r] = sv;
+        if (ei[10]) P.s_row[grow] = sv;
+      }
+    }
+    PT_LAP(P, 0)
+    for (int ch = ch_a; ch < ch_b; ++ch) {
+      const int cq = ch - ch_a;
+      const int mb = cq & 1;
+      const bool has_next = ch + 1 < ch_b;
+      double* kt = psi_st + mb * TC * ldk;
+      const long long* m_pos = meta0 + mb * 4 * TC;
+      const long long* m_s = m_pos + TC;
+      const long long* m_q = m_pos + 2 * TC;
+      const double* m_x = reinterpret_cast<const double*>(m_pos + 3 * TC);
+      const int* ce = chtab + 8 * cq;
+      const int S = ce[3], S8 = (S + 7) & ~7, n08 = ce[4], ldn = ce[5];
+      // next chunk: ψ copy in flight, its column metadata into registers
+      int c0n = 0, ntn = 0;
+      long long posn = 0, s0n = 0, q0n = 0;
+      double xn = 0.0;
+      if (has_next) {
+        c0n = ce[8 + 1]; ntn = ce[8 + 2];
+        if (P.bulk_copy) stash_cols_bulk(P, c0n, ntn, psi, psi_st + (mb ^ 1) * TC * ldk, bars + (mb ^ 1));
+        else stash_cols_issue(P, c0n, ntn, psi, psi_st + (mb ^ 1) * TC * ldk);
+        if (tid < ntn) {
+          const int c = c0n + tid;
+          posn = static_cast<long long>(c) * P.s_pad;
+          s0n = P.col_rowbase[c] - prow0;
+          q0n = static_cast<long long>(P.col_vec[c]) * P.s_pad;
+          xn = ld_cg(x + c);
+        }
+      }
+      if (P.bulk_copy) {   // ψ(ch) landed
+        mbar_wait(bars + mb, ph[mb]);
+        ph[mb] ^= 1u;
+      } else if (has_next) {
+        cp_async_wait<2>();   // λ(ch), ψ(ch+1) may still be in flight
+      } else {
+        cp_async_wait<1>();
+      }
+      stage_operator_sized(P, k, S8, ldn, smem, cur);
+      __syncthreads();
+      // K = ψ + s·x (= φ + λ), zero padded to TC x S4 (GEMM 1 k-steps of 4);
+      // one warp per column
+      const int S4 = (S + 3) & ~3;
+      for (int t = warp; t < TC; t += kWarps) {
+        double* kp = kt + t * ldk;
+        const long long s0 = m_s[t];
+        const double xc = m_x[t];
+        for (int p = lane; p < S4; p += 32)
+          kp[p] = (t < nt && p < S) ? fma(s_patch[s0 + p], xc, kp[p]) : 0.0;
+      }
+      __syncthreads();
+      PT_LAP(P, 1)
+      gemm1<TC>(P, S4, n08, ldn, smem, kt, ldk, yb, P.ldy, yp,
+                LamWait{bars + 2, ph[2], P.bulk_copy != 0, has_next});
+      if (P.bulk_copy) ph[2] ^= 1u;
+      PT_LAP(P, 2)
+      StreamEpi<TC> epi{P.psi[b ^ 1], P.lam[b ^ 1], P.q_pool, m_pos, m_s, m_q, m_x,
+                        s_patch, kt, lam_st, ldk, S, nt, pri_m, dual_m};
+      gemm2<TC>(S8, n08, ldn, smem, yb, P.ldy, epi);
+      pri_m = epi.pri_m; dual_m = epi.dual_m;
+      __syncthreads();
+      PT_LAP(P, 3)
+      // banded pass: row r of the patch gets v'(r - s0_t, t)·x_t from every
+      // chunk column t whose support holds it, in ascending column order
+      {
+        const int rlo = static_cast<int>(m_s[0]);
+        const int rhi = static_cast<int>(m_s[nt - 1]) + S;
+        for (int r = rlo + tid; r < rhi; r += kThreads) {
+          double acc = c_patch[r];
+          for (int t = 0; t < nt; ++t) {
+            const int p = r - static_cast<int>(m_s[t]);
+            if (p >= 0 && p < S) acc = fma(lam_st[t * ldk + p], m_x[t], acc);
+          }
+          c_patch[r] = acc;
+        }
+      }
+      if (has_next && tid < TC) {
+        long long* mm = meta0 + (mb ^ 1) * 4 * TC;
+        mm[tid] = posn; mm[TC + tid] = s0n; mm[2 * TC + tid] = q0n;
+        reinterpret_cast<double*>(mm)[3 * TC + tid] = xn;
+      }
+      __syncthreads();
+      if (has_next) {
+        if (P.bulk_copy) stash_cols_bulk(P, c0n, ntn, lam, lam_st, bars + 2);
+        else stash_cols_issue(P, c0n, ntn, lam, lam_st);
+        k = ce[8]; c0 = c0n; nt = ntn;
+      }
+      PT_LAP(P, 4)
+    }
+    // this unit's Φ-dot partials -> its slot of every patch row
+    for (int r = tid; r < prows; r += kThreads) {
+      const int q = rowq[r];
+      const double* e = ptab + 6 * q;
+      const int* ei = reinterpret_cast<const int*>(e);
+      part_out[reinterpret_cast<const long long*>(e)[2] + static_cast<long long>(ei[3]) * ei[1] + (r - ei[0])] =
+          c_patch[r];
+    }
+    __syncthreads();
+  }
+  PT_START
+  publish_residuals(P, it, pri_m, dual_m, smem + P.off_red);
+  PT_LAP(P, 5)
+}
+
 // Exact column stage: one column per CTA at a time, the reference's dense
 // projector with numpy's pairwise order (admm.py:183-186).
 __device__ void column_stage_exact(const DevProblem& P, int b, const double* x, int it, double* smem) {
@@ -859,7 +1272,6 @@ __device__ void zero_iterate(const DevProblem& P, int b) {
   for (size_t q = gt; q < n; q += GT) { P.psi[b][q] = 0.0; P.lam[b][q] = 0.0; }
 }
 
-enum Mode { kPatch = 0, kTwoPhase = 1, kExact = 2 };
 
 template <int TC, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, RunArgs R) {
@@ -870,6 +1282,11 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
   const bool leader = blockIdx.x == 0 && tid == 0;
   int cur = -1;   // class whose operator is staged at smem offset 0
   int b = P.ctl[4];
+  unsigned ph[3] = {0u, 0u, 0u};   // stream mode: mbarrier phases (ψ0, ψ1, λ)
+  if (MODE == kStream) {
+    if (tid < 3) mbar_init(reinterpret_cast<unsigned long long*>(smem + P.off_bar) + tid, 1);
+    __syncthreads();
+  }
   const size_t gt = blockIdx.x * blockDim.x + tid, GT = gridDim.x * blockDim.x;
   for (int step = 0; step < R.t_sim; ++step) {
     const double* x = P.x[R.closed_loop ? (step & 1) : 0];
@@ -895,6 +1312,9 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
       PT_DECL
       if (MODE == kPatch) {
         patch_iteration<TC>(P, b, x, it, smem, cur);
+        PT_START
+      } else if (MODE == kStream) {
+        stream_iteration<TC>(P, b, x, it, smem, cur, ph);
         PT_START
       } else {
         PT_START

@@ -332,7 +332,9 @@ class DeviceSession:
         return out.reshape(g, 8)
 
     def info(self):
-        out = np.zeros(7, dtype=np.int64)
+        out = np.zeros(9, dtype=np.int64)
         self._lib.dlmpc_info(self._h, _ptr(out, C.c_int64))
-        keys = ("n_rows", "n_cols", "s_pad", "n_sub", "grid", "tile_cols", "smem_bytes")
-        return dict(zip(keys, (int(v) for v in out)))
+        keys = ("n_rows", "n_cols", "s_pad", "n_sub", "grid", "tile_cols", "smem_bytes", "mode", "units")
+        d = dict(zip(keys, (int(v) for v in out)))
+        d["mode"] = ("patch", "twophase", "exact", "stream")[d["mode"]]
+        return d

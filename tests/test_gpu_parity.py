@@ -240,6 +240,34 @@ def test_patch_and_twophase_kernels_agree():
     a.close(); b.close()
 
 
+@pytest.mark.parametrize("n,t_sim", [(100, 4), (2500, 2)])
+def test_stream_and_patch_kernels_agree(n, t_sim):
+    """The stream kernel (Φ dots accumulated by the Ψ epilogues, ψ/λ staged
+    by cp.async, register epilogue) and the patch kernel agree: identical
+    iteration counts, iterates equal to rounding; and the stream kernel is
+    run to run deterministic (its cross-unit Φ partials are summed in a
+    fixed unit order)."""
+    system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=n, d=3, horizon=10, seed=5))
+    os.environ["DLMPC_FORCE_STREAM"] = "1"
+    try:
+        a = pb.DlmpcSession(system, spec, mask, FAST)
+    finally:
+        os.environ.pop("DLMPC_FORCE_STREAM")
+    os.environ["DLMPC_NO_STREAM"] = "1"
+    try:
+        b = pb.DlmpcSession(system, spec, mask, FAST)
+    finally:
+        os.environ.pop("DLMPC_NO_STREAM")
+    assert a.device.info()["mode"] == "stream" and b.device.info()["mode"] == "patch"
+    ta, _ = a.simulate(x0, t_sim)
+    ta2, _ = a.simulate(x0, t_sim)
+    tb, _ = b.simulate(x0, t_sim)
+    assert ta.step_iterations == tb.step_iterations
+    assert rel_err(ta.states, tb.states) <= 1e-12
+    assert np.array_equal(ta.states, ta2.states) and np.array_equal(ta.inputs, ta2.inputs)
+    a.close(); b.close()
+
+
 @pytest.mark.slow
 def test_large_network_properties():
     """N = 20,000 (beyond the oracle): convergence, determinism, feasibility
