@@ -163,6 +163,55 @@ def cpu_baseline(pb, system, spec, mask, seconds_budget=20.0):
             "ms_per_mpc_step": 1e3 * dt / steps}
 
 
+SWEEP_NS = (1000, 10000, 100000, 1000000)
+
+
+def sweep(pb, hbm_peak, cpu_seconds=6.0):
+    """SURVEY §8(d) C3/C5 on one GPU: the step-0 solve of the chain at
+    N = 10^3..10^6 (d=3, T=10), device-timed (CUDA events around the one
+    persistent launch, best of 3 after a warm-up), with the per-point
+    roofline fractions; plus the oracle's rate at N=1000 on the host cores
+    (bounded sample) for the >=50x target of the north star."""
+    out = []
+    for n in SWEEP_NS:
+        t0 = time.perf_counter()
+        system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=n, d=D, horizon=T, t_sim=1, seed=1))
+        sess = pb.DlmpcSession(system, spec, mask, "b200")
+        setup_s = time.perf_counter() - t0
+        traj, _ = sess.simulate(x0, 1)
+        best = min(sess.simulate(x0, 1)[1] for _ in range(3))
+        it = int(sum(traj.step_iterations))
+        flops_it, bytes_it, nnz = algorithmic_work(sess)
+        s_it = best * 1e-3 / it
+        entry = {"n_subsystems": n, "iterations": it, "ms_per_mpc_step": best, "us_per_iteration": 1e6 * s_it,
+                 "value": n / s_it, "unit": UNIT, "kernel": sess.device.info()["mode"],
+                 "setup_s": round(setup_s, 2),
+                 "fp64_tflops": flops_it / s_it / 1e12, "fp64_frac": flops_it / s_it / 1e12 / FP64_DMMA_PEAK_TFLOPS,
+                 "hbm_gbs": bytes_it / s_it / 1e9, "hbm_frac": bytes_it / s_it / 1e9 / hbm_peak,
+                 "flops_per_iteration": flops_it, "bytes_per_iteration": bytes_it}
+        if n == 1000 and cpu_seconds > 0:
+            from oracle import admm_ref
+            tables = pb.LayoutTables(mask)
+            cs = pb.precompute_column_solvers(pb.build_dynamics_operator(system, T), mask)
+            workers = max(1, min(8, os.cpu_count() or 1))
+            solver = admm_ref.OracleSolver(tables, cs, spec.rho, workers)
+            w, lo, hi = spec.row_arrays()
+            solver.row_data, _ = admm_ref.row_data_for(x0, tables, w, lo, hi)
+            k, t1 = 0, time.perf_counter()
+            while time.perf_counter() - t1 < cpu_seconds:
+                solver.iterate()
+                k += 1
+            cpu_rate = n * k / (time.perf_counter() - t1)
+            solver.close()
+            entry["cpu_baseline"] = {"value": cpu_rate, "unit": UNIT, "cores": workers, "kind": "port",
+                                     "sample": f"{k} ADMM iterations of the N=1000 step-0 solve"}
+            entry["speedup_vs_cpu"] = entry["value"] / cpu_rate
+        out.append(entry)
+        sess.close()
+        del sess
+    return out
+
+
 def run_reference_arm(args):
     """`--impl reference`: the reference's CPU path (oracle port) on the host."""
     rank, world, _ = dist_env()
@@ -321,6 +370,9 @@ def run_device_arm(args):
     }
     if not args.no_cpu and world == 1:
         line["cpu_baseline"] = cpu_baseline(pb, system, spec, mask)
+    if not args.no_sweep and world == 1:
+        sess.close()
+        line["sweep"] = sweep(pb, hbm_peak, 0.0 if args.no_cpu else 6.0)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -333,6 +385,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the N=1e3..1e6 step-0 sweep")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -177,6 +177,8 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
     std::vector<int> cta_ptr(G + 1, 0), u_lo, u_hi, p_lo, p_hi, u_chunk(1, 0), ch_cls, ch_c0, ch_n;
     std::vector<int> part_first, part_n;
     std::vector<int64_t> part_off;
+    std::vector<int> st_unit_desc, st_chunk_desc;
+    std::vector<double> st_ptab;
     long long part_total = 0;
     long long prows_max = 0, np_max = 0;
     if (h->mode == kPatch) {
@@ -299,7 +301,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           ch_max = 0;
           for (size_t u = 0; u + 1 < u_chunk.size(); ++u) ch_max = std::max<long long>(ch_max, u_chunk[u + 1] - u_chunk[u]);
           // chunk table [ch][8 ints], patch table [q][6 doubles], row map [rows] ints
-          extra = 4 * (ch_max + 1) + 6 * np_max + (cap + 2) / 2 + 12;
+          extra = (long long)(ch_max + 1) * (8 + 2 * tc) / 2 + 6 * np_max + np_max + (cap + 2) / 2 + 16;
           const long long need = fixed + 2 * ((cap + 1) & ~1LL) + extra;
           if (need <= limit) { ok = prows_max <= cap; break; }
           cap -= (need - limit + 1) / 2 + 16;
@@ -322,6 +324,45 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           part_total = tot;
           if (ok) {
             h->mode = kStream;
+            // host-built control tables (see DevProblem)
+            const int chw = 8 + 2 * tc;
+            const size_t nu = u_lo.size();
+            st_unit_desc.assign(nu * 12, 0);
+            st_chunk_desc.assign(ch_cls.size() * chw, 0);
+            st_ptab.clear();
+            int pt_off = 0;
+            for (size_t u = 0; u < nu; ++u) {
+              const long long prow0 = pr->row_start[p_lo[u]];
+              int* ud = &st_unit_desc[u * 12];
+              ud[0] = u_lo[u]; ud[1] = u_hi[u]; ud[2] = p_lo[u]; ud[3] = p_hi[u];
+              ud[4] = (int)(prow0 & 0xffffffffLL); ud[5] = (int)(prow0 >> 32);
+              ud[6] = (int)(pr->row_start[p_hi[u]] - prow0); ud[7] = u_chunk[u]; ud[8] = u_chunk[u + 1];
+              ud[9] = pt_off;
+              for (int ch = u_chunk[u]; ch < u_chunk[u + 1]; ++ch) {
+                int* cd = &st_chunk_desc[(size_t)ch * chw];
+                const int k = ch_cls[ch];
+                cd[0] = k; cd[1] = ch_c0[ch]; cd[2] = ch_n[ch]; cd[3] = pr->class_s[k];
+                cd[4] = (pr->class_n0[k] + 7) & ~7; cd[5] = pr->class_ldn[k];
+                for (int t = 0; t < ch_n[ch]; ++t) {
+                  const int c = ch_c0[ch] + t;
+                  cd[8 + t] = (int)(pr->col_rowbase[c] - prow0);
+                  cd[8 + tc + t] = pr->col_vec[c];
+                }
+              }
+              for (int i = p_lo[u]; i < p_hi[u]; ++i) {
+                double e[6] = {0, 0, 0, 0, 0, 0};
+                int* ei = reinterpret_cast<int*>(e);
+                ei[0] = (int)(pr->row_start[i] - prow0);
+                ei[1] = (int)(pr->row_start[i + 1] - pr->row_start[i]);
+                ei[2] = part_n[i];
+                ei[3] = (int)u - part_first[i];
+                reinterpret_cast<long long*>(e)[2] = part_off[i];
+                reinterpret_cast<long long*>(e)[4] = pr->row_start[i];
+                ei[10] = (i >= u_lo[u] && i < u_hi[u]) ? 1 : 0;
+                st_ptab.insert(st_ptab.end(), e, e + 6);
+                ++pt_off;
+              }
+            }
             P.ldk = ldk; P.ldy = ldy; P.split_max = sp_max;
             P.s8_max = s8_max; P.n08_max = n08_max;
             long long off = (opr_need + 1) & ~1LL;
@@ -334,8 +375,9 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
             P.off_patch = (int)off; off += (cap + 1) & ~1LL;
             P.off_cpatch = (int)off; off += (cap + 1) & ~1LL;
             P.patch_cap = (int)cap;
-            P.off_chtab = (int)off; off += 4 * (ch_max + 1); P.ch_cap = (int)(ch_max + 1);
+            P.off_chtab = (int)off; off += ((ch_max + 1) * (8 + 2 * tc) / 2 + 1) & ~1LL; P.ch_cap = (int)(ch_max + 1);
             P.off_ptab = (int)off; off += 6 * np_max; P.np_cap = (int)np_max;
+            P.off_pada = (int)off; off += np_max;
             P.off_rowq = (int)off; off += (cap + 2) / 2;
             off = (off + 1) & ~1LL;
             P.off_bar = (int)off; off += 4;
@@ -429,7 +471,10 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           (rc = upload(h, ch_n.data(), ch_n.size(), &P.chunk_n)))
         return rc;
       if (h->mode == kStream) {
-        if ((rc = upload(h, part_first.data(), part_first.size(), &P.part_first)) ||
+        if ((rc = upload(h, st_unit_desc.data(), st_unit_desc.size(), &P.unit_desc)) ||
+            (rc = upload(h, st_chunk_desc.data(), st_chunk_desc.size(), &P.chunk_desc)) ||
+            (rc = upload(h, st_ptab.data(), st_ptab.size(), &P.unit_ptab)) ||
+            (rc = upload(h, part_first.data(), part_first.size(), &P.part_first)) ||
             (rc = upload(h, part_n.data(), part_n.size(), &P.part_n)) ||
             (rc = upload(h, part_off.data(), part_off.size(), &P.part_off)))
           return rc;

@@ -105,7 +105,14 @@ struct DevProblem {
   int off_chtab, ch_cap;       // per-unit chunk table: [ch_cap][8] ints (k, c0, nt, S, n08, ldn)
   int off_ptab, np_cap;        // per-unit patch-subsystem table: [np_cap][6] doubles
   int off_rowq;                // per patch row: its patch-subsystem index (int)
+  int off_pada;                // per patch subsystem: ||a||^2 of this MPC step
   int off_bar;                 // 3 mbarriers (ψ buffers, λ buffer)
+  // stream mode, host-built control tables (one coalesced copy per unit):
+  //   unit_desc [u][12] ints: own_lo, own_hi, plo, phi, prow0 (2 ints), prows, ch_a, ch_b, pt_off, -, -
+  //   chunk_desc [ch][8 + 2*TC] ints: k, c0, nt, S, n08, ldn, -, -, then per column slot t
+  //     s0 (row of support slot 0, unit-local) and q (particular-solution vector index)
+  //   unit_ptab [pt_off + q][6] doubles: (rowoff, rows, slots, own slot) ints | part_off | - | r0 | (own, -)
+  const int* unit_desc; const int* chunk_desc; const double* unit_ptab;
   int bulk_copy;               // stream staging by TMA bulk copies (1) or cp.async (0)
 };
 
@@ -964,6 +971,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
   int* chtab = reinterpret_cast<int*>(smem + P.off_chtab);               // [ch][8]
   double* ptab = smem + P.off_ptab;                                      // [q][6]
   int* rowq = reinterpret_cast<int*>(smem + P.off_rowq);
+  double* pada = smem + P.off_pada;                                      // ||a||^2 per patch subsystem
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + P.off_bar);   // ψ0, ψ1, λ
   const int ldk = P.ldk;
   double* psi_st = smem + P.off_k;                  // [2][TC][ldk]
@@ -975,36 +983,27 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
   const double rho = P.rho;
   double pri_m = 0.0, dual_m = 0.0;
   PT_DECL
+  constexpr int CHW = 8 + 2 * TC;   // ints per chunk descriptor
   for (int un = P.cta_unit_ptr[blockIdx.x]; un < P.cta_unit_ptr[blockIdx.x + 1]; ++un) {
     PT_START
-    const int own_lo = P.unit_sub_lo[un], own_hi = P.unit_sub_hi[un];
-    const int plo = P.unit_patch_lo[un], phi_ = P.unit_patch_hi[un];
+    const int4 ud0 = __ldg(reinterpret_cast<const int4*>(P.unit_desc) + 3 * un);
+    const int4 ud1 = __ldg(reinterpret_cast<const int4*>(P.unit_desc) + 3 * un + 1);
+    const int4 ud2 = __ldg(reinterpret_cast<const int4*>(P.unit_desc) + 3 * un + 2);
+    const int own_lo = ud0.x, own_hi = ud0.y, plo = ud0.z, phi_ = ud0.w;
+    const long long prow0 = static_cast<long long>(static_cast<unsigned>(ud1.x)) |
+                            (static_cast<long long>(ud1.y) << 32);
+    const int prows = ud1.z, ch_a = ud1.w, ch_b = ud2.x, pt_off = ud2.y;
     const int npq = phi_ - plo;
-    const long long prow0 = P.row_start[plo];
-    const int prows = static_cast<int>(P.row_start[phi_] - prow0);
-    const int ch_a = P.unit_chunk_ptr[un], ch_b = P.unit_chunk_ptr[un + 1];
     const int nch = ch_b - ch_a;
-    // one round trip for the unit's control data: chunk table, patch table
-    for (int q = tid; q < nch; q += kThreads) {
-      const int k = P.chunk_class[ch_a + q];
-      const int S = P.class_s[k];
-      int* e = chtab + 8 * q;
-      e[0] = k; e[1] = P.chunk_col0[ch_a + q]; e[2] = P.chunk_n[ch_a + q];
-      e[3] = S; e[4] = (P.class_n0[k] + 7) & ~7; e[5] = P.class_ldn[k];
-    }
-    for (int q = tid; q < npq; q += kThreads) {
-      const int i = plo + q;
-      const long long r0 = P.row_start[i];
-      double* e = ptab + 6 * q;
-      int* ei = reinterpret_cast<int*>(e);
-      ei[0] = static_cast<int>(r0 - prow0);                       // local row offset
-      ei[1] = static_cast<int>(P.row_start[i + 1] - r0);          // rows
-      ei[2] = P.part_n[i];
-      ei[3] = un - P.part_first[i];                               // this unit's slot
-      reinterpret_cast<long long*>(e)[2] = P.part_off[i];
-      e[3] = ld_cg(P.ada + i);
-      reinterpret_cast<long long*>(e)[4] = r0;
-      ei[10] = (i >= own_lo && i < own_hi);
+    // the unit's control tables in one coalesced round trip
+    {
+      const int4* src = reinterpret_cast<const int4*>(P.chunk_desc + static_cast<size_t>(ch_a) * CHW);
+      int4* dst = reinterpret_cast<int4*>(chtab);
+      for (int q = tid; q < nch * CHW / 4; q += kThreads) dst[q] = __ldg(src + q);
+      const double2* ps = reinterpret_cast<const double2*>(P.unit_ptab + static_cast<size_t>(pt_off) * 6);
+      double2* pd = reinterpret_cast<double2*>(ptab);
+      for (int q = tid; q < npq * 3; q += kThreads) pd[q] = __ldg(ps + q);
+      for (int q = tid; q < npq; q += kThreads) pada[q] = ld_cg(P.ada + plo + q);
     }
     __syncthreads();
     for (int q = warp; q < npq; q += kWarps) {
@@ -1013,6 +1012,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
     }
     for (int r = tid; r < prows; r += kThreads) c_patch[r] = 0.0;
     int k = 0, c0 = 0, nt = 0;
+    double x_first = 0.0;
     if (nch > 0) {
       k = chtab[0]; c0 = chtab[1]; nt = chtab[2];
       if (P.bulk_copy) {
@@ -1022,20 +1022,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
         stash_cols_issue(P, c0, nt, psi, psi_st);
         stash_cols_issue(P, c0, nt, lam, lam_st);
       }
-      if (tid < TC) {
-        long long* mm = meta0;
-        long long pos = 0, s0 = 0, q0 = 0;
-        double xc = 0.0;
-        if (tid < nt) {
-          const int c = c0 + tid;
-          pos = static_cast<long long>(c) * P.s_pad;
-          s0 = P.col_rowbase[c] - prow0;
-          q0 = static_cast<long long>(P.col_vec[c]) * P.s_pad;
-          xc = ld_cg(x + c);
-        }
-        mm[tid] = pos; mm[TC + tid] = s0; mm[2 * TC + tid] = q0;
-        reinterpret_cast<double*>(mm)[3 * TC + tid] = xc;
-      }
+      if (tid < nt) x_first = ld_cg(x + c0 + tid);   // consumed after the Φ loop
     }
     __syncthreads();
     // Φ scales of the patch rows
@@ -1062,7 +1049,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
         const double w = P.row_w[grow], lo = P.row_lo[grow], hi = P.row_hi[grow];
         double c = ld_cg(pb);
         for (int sl = 1; sl < np; ++sl) c += ld_cg(pb + sl * nr);
-        const double ada = e[3];
+        const double ada = pada[q];
         const double y0 = __ddiv_rn(__dmul_rn(rho, c), __dadd_rn(rho, __dmul_rn(__dmul_rn(2.0, w), ada)));
         const double y = fmin(fmax(y0, lo), hi);
         const double sv = ada > 0.0 ? __ddiv_rn(__dsub_rn(y, c), ada) : 0.0;
@@ -1070,6 +1057,15 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
         if (ei[10]) P.s_row[grow] = sv;
       }
     }
+    if (nch > 0 && tid < TC) {
+      long long* mm = meta0;
+      const bool ok = tid < nt;
+      mm[tid] = ok ? static_cast<long long>(c0 + tid) * P.s_pad : 0;
+      mm[TC + tid] = ok ? chtab[8 + tid] : 0;
+      mm[2 * TC + tid] = ok ? static_cast<long long>(chtab[8 + TC + tid]) * P.s_pad : 0;
+      reinterpret_cast<double*>(mm)[3 * TC + tid] = x_first;
+    }
+    __syncthreads();
     PT_LAP(P, 0)
     for (int ch = ch_a; ch < ch_b; ++ch) {
       const int cq = ch - ch_a;
@@ -1080,24 +1076,25 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       const long long* m_s = m_pos + TC;
       const long long* m_q = m_pos + 2 * TC;
       const double* m_x = reinterpret_cast<const double*>(m_pos + 3 * TC);
-      const int* ce = chtab + 8 * cq;
+      const int* ce = chtab + CHW * cq;
       const int S = ce[3], S8 = (S + 7) & ~7, n08 = ce[4], ldn = ce[5];
       // next chunk: ψ copy in flight, its column metadata into registers
       int c0n = 0, ntn = 0;
       long long posn = 0, s0n = 0, q0n = 0;
       double xn = 0.0;
       if (has_next) {
-        c0n = ce[8 + 1]; ntn = ce[8 + 2];
+        c0n = ce[CHW + 1]; ntn = ce[CHW + 2];
         if (P.bulk_copy) stash_cols_bulk(P, c0n, ntn, psi, psi_st + (mb ^ 1) * TC * ldk, bars + (mb ^ 1));
         else stash_cols_issue(P, c0n, ntn, psi, psi_st + (mb ^ 1) * TC * ldk);
         if (tid < ntn) {
           const int c = c0n + tid;
           posn = static_cast<long long>(c) * P.s_pad;
-          s0n = P.col_rowbase[c] - prow0;
-          q0n = static_cast<long long>(P.col_vec[c]) * P.s_pad;
+          s0n = ce[CHW + 8 + tid];
+          q0n = static_cast<long long>(ce[CHW + 8 + TC + tid]) * P.s_pad;
           xn = ld_cg(x + c);
         }
       }
+      PT_LAP(P, 1)
       if (P.bulk_copy) {   // ψ(ch) landed
         mbar_wait(bars + mb, ph[mb]);
         ph[mb] ^= 1u;
@@ -1106,6 +1103,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       } else {
         cp_async_wait<1>();
       }
+      PT_LAP(P, 7)
       stage_operator_sized(P, k, S8, ldn, smem, cur);
       __syncthreads();
       // K = ψ + s·x (= φ + λ), zero padded to TC x S4 (GEMM 1 k-steps of 4);
@@ -1153,7 +1151,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       if (has_next) {
         if (P.bulk_copy) stash_cols_bulk(P, c0n, ntn, lam, lam_st, bars + 2);
         else stash_cols_issue(P, c0n, ntn, lam, lam_st);
-        k = ce[8]; c0 = c0n; nt = ntn;
+        k = ce[CHW]; c0 = c0n; nt = ntn;
       }
       PT_LAP(P, 4)
     }

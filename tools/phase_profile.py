@@ -14,9 +14,9 @@ sess.device.phase_times(reset=True)
 traj, ms = sess.simulate(x0, t_sim)
 it = sum(traj.step_iterations)
 pt = sess.device.phase_times(reset=True).astype(np.float64) / it / 1e3   # us per iteration per CTA
-names = ["phi", "prologue", "gemm1", "gemm2", "epilogue", "publish", "barrier", "-"]
+names = ["phi", "prologue", "gemm1", "gemm2", "epilogue", "publish", "barrier", "wait"]
 print(f"N={n} {sess.device.info()} iters {it} device {ms:.3f} ms = {1e3*ms/it:.2f} us/iter")
-for k, nm in enumerate(names[:7]):
+for k, nm in enumerate(names):
     col = pt[:, k]
     print(f"  {nm:9s} max {col.max():7.2f} us  mean {col.mean():7.2f} us  min {col.min():7.2f}")
 print(f"  sum(max) {pt[:, :7].max(axis=0).sum():.2f}  per-CTA total max {pt[:, :7].sum(axis=1).max():.2f}")
