@@ -85,9 +85,9 @@ KernelFn pick_kernel(int mode, int tc) {
   return tc == 16 ? dlmpc_persistent<16, kTwoPhase> : dlmpc_persistent<8, kTwoPhase>;
 }
 
-int ld_frag(int n) {   // smallest ld >= n with ld % 16 == 4: conflict-free FP64 fragments
+int ld_frag(int n) {   // smallest ld >= n with ld % 16 in {4, 12}: conflict-free FP64 fragments
   int ld = std::max(n, 1);
-  while (ld % 16 != 4) ++ld;
+  while (ld % 16 != 4 && ld % 16 != 12) ++ld;
   return ld;
 }
 
@@ -290,7 +290,11 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         const bool bulk = !(be && be[0] == '0') && (P.s_pad % 16 == 4 || P.s_pad % 16 == 12);
         const int ldk = bulk ? P.s_pad : ld_frag(s8_max), ldy = ld_frag(tc);
         const int sp_max = 1;   // GEMM 1 tile-parallel for every class (no partials buffer)
-        const long long fixed = ((opr_need + 1) & ~1LL) + 3LL * tc * ldk + (long long)n08_max * ldy +
+        // operator region: every class's basis resident in shared memory
+        // (measured: reading a rare class's basis from L2 makes its CTAs the
+        // stragglers, N=3000: 31.2 vs 29.3 us/iter)
+        const long long opr_main = opr_need;
+        const long long fixed = ((opr_main + 1) & ~1LL) + 3LL * tc * ldk + (long long)n08_max * ldy +
                                 (sp_max > 1 ? (long long)sp_max * n08_max * tc : 0) + 32 + 8 * tc + 8;
         long long cap = std::min<long long>(4096, (limit - fixed) / 2);
         if (const char* e = getenv("DLMPC_STREAM_CAP")) cap = std::min<long long>(cap, atoll(e));
@@ -343,6 +347,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
                 const int k = ch_cls[ch];
                 cd[0] = k; cd[1] = ch_c0[ch]; cd[2] = ch_n[ch]; cd[3] = pr->class_s[k];
                 cd[4] = (pr->class_n0[k] + 7) & ~7; cd[5] = pr->class_ldn[k];
+                cd[6] = (int)(pr->class_null_off[k] & 0xffffffffLL); cd[7] = (int)(pr->class_null_off[k] >> 32);
                 for (int t = 0; t < ch_n[ch]; ++t) {
                   const int c = ch_c0[ch] + t;
                   cd[8 + t] = (int)(pr->col_rowbase[c] - prow0);
@@ -365,8 +370,8 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
             }
             P.ldk = ldk; P.ldy = ldy; P.split_max = sp_max;
             P.s8_max = s8_max; P.n08_max = n08_max;
-            long long off = (opr_need + 1) & ~1LL;
-            P.opr_cap = (int)opr_need;
+            long long off = (opr_main + 1) & ~1LL;
+            P.opr_cap = (int)opr_main;
             P.off_k = (int)off; off += 3LL * tc * ldk;
             P.off_y = (int)off; off += (long long)n08_max * ldy;
             P.off_yp = (int)off; off += sp_max > 1 ? (long long)sp_max * n08_max * tc : 0;

@@ -109,7 +109,7 @@ struct DevProblem {
   int off_bar;                 // 3 mbarriers (ψ buffers, λ buffer)
   // stream mode, host-built control tables (one coalesced copy per unit):
   //   unit_desc [u][12] ints: own_lo, own_hi, plo, phi, prow0 (2 ints), prows, ch_a, ch_b, pt_off, -, -
-  //   chunk_desc [ch][8 + 2*TC] ints: k, c0, nt, S, n08, ldn, -, -, then per column slot t
+  //   chunk_desc [ch][8 + 2*TC] ints: k, c0, nt, S, n08, ldn, null_off (2 ints), then per column slot t
   //     s0 (row of support slot 0, unit-local) and q (particular-solution vector index)
   //   unit_ptab [pt_off + q][6] doubles: (rowoff, rows, slots, own slot) ints | part_off | - | r0 | (own, -)
   const int* unit_desc; const int* chunk_desc; const double* unit_ptab;
@@ -1104,6 +1104,9 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
         cp_async_wait<1>();
       }
       PT_LAP(P, 7)
+      // the class operator, resident in shared memory (the host sizes the
+      // region for every class; a pointer that may be global would turn
+      // every fragment load into a generic LD)
       stage_operator_sized(P, k, S8, ldn, smem, cur);
       __syncthreads();
       // K = ψ + s·x (= φ + λ), zero padded to TC x S4 (GEMM 1 k-steps of 4);

@@ -41,10 +41,11 @@ def _round(n, m):
 
 
 def _ld_frag(n):
-    """Smallest leading dimension >= n with ld % 16 == 4 (conflict-free
-    8x4 / 4x8 FP64 fragment loads: a half-warp hits 16 distinct banks)."""
+    """Smallest leading dimension >= n with ld % 16 in (4, 12): conflict-free
+    8x4 / 4x8 FP64 fragment loads (a half-warp's 4 rows of 4 consecutive
+    doubles land on 16 distinct 8-byte banks)."""
     ld = max(int(n), 1)
-    while ld % 16 != 4:
+    while ld % 16 not in (4, 12):
         ld += 1
     return ld
 
