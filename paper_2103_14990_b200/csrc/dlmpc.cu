@@ -286,8 +286,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         // ψ/λ staging: TMA bulk copies with smem rows at the global column
         // stride when s_pad % 16 is 4 or 12 (FP64 fragment loads stay conflict
         // free; one copy per chunk and array), else 16-byte cp.async
-        const char* be = getenv("DLMPC_BULK_COPY");
-        const bool bulk = !(be && be[0] == '0') && (P.s_pad % 16 == 4 || P.s_pad % 16 == 12);
+        const bool bulk = P.s_pad % 16 == 4 || P.s_pad % 16 == 12;   // stream mode requires it
         const int ldk = bulk ? P.s_pad : ld_frag(s8_max), ldy = ld_frag(tc);
         const int sp_max = 1;   // GEMM 1 tile-parallel for every class (no partials buffer)
         // operator region: every class's basis resident in shared memory
@@ -313,7 +312,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         if (ok) {
           int s_max = 1;
           for (int k = 0; k < pr->n_classes; ++k) s_max = std::max(s_max, pr->class_s[k]);
-          ok = ldk >= P.s_pad && ldk >= ((s_max + 3) & ~3);
+          ok = bulk && ldk >= P.s_pad && ldk >= ((s_max + 3) & ~3);
           std::vector<int> unit_of(P.n_sub, -1);
           for (size_t u = 0; u < u_lo.size(); ++u)
             for (int i = u_lo[u]; i < u_hi[u]; ++i) unit_of[i] = (int)u;

@@ -1011,20 +1011,15 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       for (int l = lane; l < ei[1]; l += 32) rowq[ei[0] + l] = q;
     }
     for (int r = tid; r < prows; r += kThreads) c_patch[r] = 0.0;
-    int k = 0, c0 = 0, nt = 0;
+    // staging: ψ(a) -> ψ buffer 0, λ(a) -> λ buffer, ψ(a+1) -> ψ buffer 1
+    // (TMA bulk copies, one per chunk and array; mbarriers ψ0, ψ1, λ)
     double x_first = 0.0;
     if (nch > 0) {
-      k = chtab[0]; c0 = chtab[1]; nt = chtab[2];
-      if (P.bulk_copy) {
-        stash_cols_bulk(P, c0, nt, psi, psi_st, bars + 0);
-        stash_cols_bulk(P, c0, nt, lam, lam_st, bars + 2);
-      } else {
-        stash_cols_issue(P, c0, nt, psi, psi_st);
-        stash_cols_issue(P, c0, nt, lam, lam_st);
-      }
-      if (tid < nt) x_first = ld_cg(x + c0 + tid);   // consumed after the Φ loop
+      stash_cols_bulk(P, chtab[1], chtab[2], psi, psi_st, bars + 0);
+      stash_cols_bulk(P, chtab[1], chtab[2], lam, lam_st, bars + 2);
+      if (nch > 1) stash_cols_bulk(P, chtab[CHW + 1], chtab[CHW + 2], psi, psi_st + TC * ldk, bars + 1);
+      if (tid < chtab[2]) x_first = ld_cg(x + chtab[1] + tid);   // consumed after the Φ loop
     }
-    __syncthreads();
     // Φ scales of the patch rows
     if (it == 0) {
       for (int i = plo + warp; i < phi_; i += kWarps) {
@@ -1059,71 +1054,59 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
     }
     if (nch > 0 && tid < TC) {
       long long* mm = meta0;
-      const bool ok = tid < nt;
-      mm[tid] = ok ? static_cast<long long>(c0 + tid) * P.s_pad : 0;
+      const bool ok = tid < chtab[2];
+      mm[tid] = ok ? static_cast<long long>(chtab[1] + tid) * P.s_pad : 0;
       mm[TC + tid] = ok ? chtab[8 + tid] : 0;
       mm[2 * TC + tid] = ok ? static_cast<long long>(chtab[8 + TC + tid]) * P.s_pad : 0;
       reinterpret_cast<double*>(mm)[3 * TC + tid] = x_first;
     }
     __syncthreads();
     PT_LAP(P, 0)
-    for (int ch = ch_a; ch < ch_b; ++ch) {
-      const int cq = ch - ch_a;
-      const int mb = cq & 1;
-      const bool has_next = ch + 1 < ch_b;
-      double* kt = psi_st + mb * TC * ldk;
-      const long long* m_pos = meta0 + mb * 4 * TC;
-      const long long* m_s = m_pos + TC;
-      const long long* m_q = m_pos + 2 * TC;
-      const double* m_x = reinterpret_cast<const double*>(m_pos + 3 * TC);
-      const int* ce = chtab + CHW * cq;
-      const int S = ce[3], S8 = (S + 7) & ~7, n08 = ce[4], ldn = ce[5];
-      // next chunk: ψ copy in flight, its column metadata into registers
-      int c0n = 0, ntn = 0;
-      long long posn = 0, s0n = 0, q0n = 0;
-      double xn = 0.0;
-      if (has_next) {
-        c0n = ce[CHW + 1]; ntn = ce[CHW + 2];
-        if (P.bulk_copy) stash_cols_bulk(P, c0n, ntn, psi, psi_st + (mb ^ 1) * TC * ldk, bars + (mb ^ 1));
-        else stash_cols_issue(P, c0n, ntn, psi, psi_st + (mb ^ 1) * TC * ldk);
-        if (tid < ntn) {
-          const int c = c0n + tid;
-          posn = static_cast<long long>(c) * P.s_pad;
-          s0n = ce[CHW + 8 + tid];
-          q0n = static_cast<long long>(ce[CHW + 8 + TC + tid]) * P.s_pad;
-          xn = ld_cg(x + c);
-        }
-      }
-      PT_LAP(P, 1)
-      if (P.bulk_copy) {   // ψ(ch) landed
-        mbar_wait(bars + mb, ph[mb]);
-        ph[mb] ^= 1u;
-      } else if (has_next) {
-        cp_async_wait<2>();   // λ(ch), ψ(ch+1) may still be in flight
-      } else {
-        cp_async_wait<1>();
-      }
-      PT_LAP(P, 7)
-      // the class operator, resident in shared memory (the host sizes the
-      // region for every class; a pointer that may be global would turn
-      // every fragment load into a generic LD)
-      stage_operator_sized(P, k, S8, ldn, smem, cur);
-      __syncthreads();
-      // K = ψ + s·x (= φ + λ), zero padded to TC x S4 (GEMM 1 k-steps of 4);
-      // one warp per column
+    // K = ψ + s·x (= φ + λ) in place, zero padded to TC x S4 (GEMM 1 k-steps
+    // of 4); one warp per column
+    auto k_pass = [&](double* kt, const long long* m_s, const double* m_x, int S, int nt_) {
       const int S4 = (S + 3) & ~3;
       for (int t = warp; t < TC; t += kWarps) {
         double* kp = kt + t * ldk;
         const long long s0 = m_s[t];
         const double xc = m_x[t];
         for (int p = lane; p < S4; p += 32)
-          kp[p] = (t < nt && p < S) ? fma(s_patch[s0 + p], xc, kp[p]) : 0.0;
+          kp[p] = (t < nt_ && p < S) ? fma(s_patch[s0 + p], xc, kp[p]) : 0.0;
       }
+    };
+    if (nch > 0) {   // first chunk: operator, ψ landed, K
+      stage_operator_sized(P, chtab[0], (chtab[3] + 7) & ~7, chtab[5], smem, cur);
+      mbar_wait(bars + 0, ph[0]);
+      ph[0] ^= 1u;
+      k_pass(psi_st, meta0 + TC, reinterpret_cast<const double*>(meta0 + 3 * TC), chtab[3], chtab[2]);
       __syncthreads();
-      PT_LAP(P, 1)
-      gemm1<TC>(P, S4, n08, ldn, smem, kt, ldk, yb, P.ldy, yp,
-                LamWait{bars + 2, ph[2], P.bulk_copy != 0, has_next});
-      if (P.bulk_copy) ph[2] ^= 1u;
+    }
+    PT_LAP(P, 1)
+    // chunk pipeline: GEMM 1 -> GEMM 2 + epilogue -> (row pass of this chunk
+    // | K pass of the next) -> stage λ(next) and ψ(next+1)
+    for (int ch = ch_a; ch < ch_b; ++ch) {
+      const int cq = ch - ch_a;
+      const int mb = cq & 1;
+      const bool has_next = ch + 1 < ch_b, has_next2 = ch + 2 < ch_b;
+      double* kt = psi_st + mb * TC * ldk;
+      const long long* m_pos = meta0 + mb * 4 * TC;
+      const long long* m_s = m_pos + TC;
+      const long long* m_q = m_pos + 2 * TC;
+      const double* m_x = reinterpret_cast<const double*>(m_pos + 3 * TC);
+      const int* ce = chtab + CHW * cq;
+      const int nt = ce[2], S = ce[3], S8 = (S + 7) & ~7, S4 = (S + 3) & ~3, n08 = ce[4], ldn = ce[5];
+      double xn = 0.0;   // x of the next chunk's columns (meta written after GEMM 1)
+      if (has_next && tid < ce[CHW + 2]) xn = ld_cg(x + ce[CHW + 1] + tid);
+      gemm1<TC>(P, S4, n08, ldn, smem, kt, ldk, yb, P.ldy, yp, LamWait{bars + 2, ph[2], true, has_next});
+      ph[2] ^= 1u;
+      if (has_next && tid < TC) {
+        long long* mm = meta0 + (mb ^ 1) * 4 * TC;
+        const bool ok = tid < ce[CHW + 2];
+        mm[tid] = ok ? static_cast<long long>(ce[CHW + 1] + tid) * P.s_pad : 0;
+        mm[TC + tid] = ok ? ce[CHW + 8 + tid] : 0;
+        mm[2 * TC + tid] = ok ? static_cast<long long>(ce[CHW + 8 + TC + tid]) * P.s_pad : 0;
+        reinterpret_cast<double*>(mm)[3 * TC + tid] = xn;
+      }
       PT_LAP(P, 2)
       StreamEpi<TC> epi{P.psi[b ^ 1], P.lam[b ^ 1], P.q_pool, m_pos, m_s, m_q, m_x,
                         s_patch, kt, lam_st, ldk, S, nt, pri_m, dual_m};
@@ -1145,17 +1128,17 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
           c_patch[r] = acc;
         }
       }
-      if (has_next && tid < TC) {
-        long long* mm = meta0 + (mb ^ 1) * 4 * TC;
-        mm[tid] = posn; mm[TC + tid] = s0n; mm[2 * TC + tid] = q0n;
-        reinterpret_cast<double*>(mm)[3 * TC + tid] = xn;
+      if (has_next) {   // next chunk: operator, ψ landed, K
+        const long long* mn = meta0 + (mb ^ 1) * 4 * TC;
+        stage_operator_sized(P, ce[CHW], (ce[CHW + 3] + 7) & ~7, ce[CHW + 5], smem, cur);
+        mbar_wait(bars + (mb ^ 1), ph[mb ^ 1]);
+        ph[mb ^ 1] ^= 1u;
+        k_pass(psi_st + (mb ^ 1) * TC * ldk, mn + TC, reinterpret_cast<const double*>(mn + 3 * TC),
+               ce[CHW + 3], ce[CHW + 2]);
       }
       __syncthreads();
-      if (has_next) {
-        if (P.bulk_copy) stash_cols_bulk(P, c0n, ntn, lam, lam_st, bars + 2);
-        else stash_cols_issue(P, c0n, ntn, lam, lam_st);
-        k = ce[CHW]; c0 = c0n; nt = ntn;
-      }
+      if (has_next) stash_cols_bulk(P, ce[CHW + 1], ce[CHW + 2], lam, lam_st, bars + 2);
+      if (has_next2) stash_cols_bulk(P, ce[2 * CHW + 1], ce[2 * CHW + 2], psi, kt, bars + mb);
       PT_LAP(P, 4)
     }
     // this unit's Φ-dot partials -> its slot of every patch row

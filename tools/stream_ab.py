@@ -7,9 +7,8 @@ import paper_2103_14990_b200 as pb
 for n in [int(a) for a in sys.argv[1:]] or [100, 1000, 10000]:
     system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=n, d=3, horizon=10, t_sim=1, seed=1))
     res = {}
-    for tag, env, bulk in (("patch", "1", "0"), ("stream-cpa", "0", "0"), ("stream", "0", "1")):
+    for tag, env in (("patch", "1"), ("stream", "0")):
         os.environ["DLMPC_NO_STREAM"] = env
-        os.environ["DLMPC_BULK_COPY"] = bulk
         sess = pb.DlmpcSession(system, spec, mask, "b200")
         best = None
         for _ in range(3):

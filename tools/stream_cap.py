@@ -7,9 +7,8 @@ n = int(sys.argv[1]); caps = sys.argv[2:] or ["4096"]
 system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=n, d=3, horizon=10, t_sim=1, seed=1))
 for rep in range(2):
     for cap in caps:
-        for bulk in ("0", "1"):
+        for bulk in ("1",):
             os.environ["DLMPC_STREAM_CAP"] = cap
-            os.environ["DLMPC_BULK_COPY"] = bulk
             sess = pb.DlmpcSession(system, spec, mask, "b200")
             best = min(sess.simulate(x0, 1)[1] for _ in range(3))
             it = 0
