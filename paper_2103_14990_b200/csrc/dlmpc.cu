@@ -293,7 +293,10 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         // (measured: reading a rare class's basis from L2 makes its CTAs the
         // stragglers, N=3000: 31.2 vs 29.3 us/iter)
         const long long opr_main = opr_need;
-        const long long fixed = ((opr_main + 1) & ~1LL) + 3LL * tc * ldk + (long long)n08_max * ldy +
+        // λ stash stride: 2*ldl % 16 in {4, 12} keeps the register epilogue conflict free
+        int ldl = P.s_pad;
+        while ((2 * ldl) % 16 != 4 && (2 * ldl) % 16 != 12) ldl += 2;
+        const long long fixed = ((opr_main + 1) & ~1LL) + 2LL * tc * ldk + (long long)tc * ldl + (long long)n08_max * ldy +
                                 (sp_max > 1 ? (long long)sp_max * n08_max * tc : 0) + 32 + 8 * tc + 8;
         long long cap = std::min<long long>(4096, (limit - fixed) / 2);
         if (const char* e = getenv("DLMPC_STREAM_CAP")) cap = std::min<long long>(cap, atoll(e));
@@ -371,7 +374,18 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
             P.s8_max = s8_max; P.n08_max = n08_max;
             long long off = (opr_main + 1) & ~1LL;
             P.opr_cap = (int)opr_main;
-            P.off_k = (int)off; off += 3LL * tc * ldk;
+            P.off_k = (int)off; off += 2LL * tc * ldk + (long long)tc * ldl;
+            P.ldl = ldl;
+            // producer/consumer warp specialisation needs one class per unit
+            // (the operator is staged once, before the chunk pipeline)
+            {
+              bool one_class = true;
+              for (size_t u = 0; one_class && u + 1 < u_chunk.size(); ++u)
+                for (int ch = u_chunk[u] + 1; ch < u_chunk[u + 1]; ++ch)
+                  if (ch_cls[ch] != ch_cls[u_chunk[u]]) { one_class = false; break; }
+              const char* e = getenv("DLMPC_WARP_SPEC");
+              P.warp_spec = (one_class && !(e && e[0] == '0')) ? 1 : 0;
+            }
             P.off_y = (int)off; off += (long long)n08_max * ldy;
             P.off_yp = (int)off; off += sp_max > 1 ? (long long)sp_max * n08_max * tc : 0;
             P.off_red = (int)off; off += 32;

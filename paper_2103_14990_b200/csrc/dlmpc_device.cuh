@@ -114,6 +114,8 @@ struct DevProblem {
   //   unit_ptab [pt_off + q][6] doubles: (rowoff, rows, slots, own slot) ints | part_off | - | r0 | (own, -)
   const int* unit_desc; const int* chunk_desc; const double* unit_ptab;
   int bulk_copy;               // stream staging by TMA bulk copies (1) or cp.async (0)
+  int ldl;                     // stream mode: row stride of the λ stash
+  int warp_spec;               // stream mode: producer/consumer warp specialisation
 };
 
 struct RunArgs {
@@ -362,11 +364,25 @@ __device__ void phi_stage_global(const DevProblem& P, int b, const double* x) {
 // loop, store(mt, nn, c0, c1) after: rows mt*8+g, columns nn*8+2tig, +1).
 // ---------------------------------------------------------------------------
 struct NoHook { __device__ __forceinline__ void operator()() const {} };
+struct CtaBar { __device__ __forceinline__ void operator()() const { __syncthreads(); } };
 
-template <int TC, class Hook = NoHook>
+// named barriers (id 0 is __syncthreads)
+__device__ __forceinline__ void nbar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" :: "r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;\n" :: "r"(id), "r"(n) : "memory");
+}
+template <int NW>
+struct GroupBar {   // barrier over the first NW warps
+  __device__ __forceinline__ void operator()() const { nbar_sync(1, NW * 32); }
+};
+
+// NW warps (warp ids 0..NW-1) run the GEMMs; `sync` is their barrier.
+template <int TC, class Hook = NoHook, int NW = kWarps, class Sync = CtaBar>
 __device__ __forceinline__ void gemm1(const DevProblem& P, int SK, int n08, int ldn, const double* nop,
                                       const double* kt, int ldk, double* yb, int ldy, double* yp,
-                                      const Hook& before_sync = Hook()) {
+                                      const Hook& before_sync = Hook(), const Sync& sync = Sync()) {
   constexpr int NTN = TC / 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
@@ -375,7 +391,7 @@ __device__ __forceinline__ void gemm1(const DevProblem& P, int SK, int n08, int 
     // enough (m, n) tiles to keep the DMMA pipe busy (or no room for split-K
     // partials): one tile per warp over the full K with two interleaved
     // accumulator chains, no split-K pass
-    for (int u = warp; u < mt1 * NTN; u += kWarps) {
+    for (int u = warp; u < mt1 * NTN; u += NW) {
       const int mt = u / NTN, nn = u - (u / NTN) * NTN;
       double c0a = 0.0, c1a = 0.0, c0b = 0.0, c1b = 0.0;
       int ks = 0;
@@ -394,13 +410,13 @@ __device__ __forceinline__ void gemm1(const DevProblem& P, int SK, int n08, int 
       yb[(mt * 8 + g) * ldy + nn * 8 + 2 * tig + 1] = c1a + c1b;
     }
     before_sync();
-    __syncthreads();
+    sync();
     return;
   }
   const int groups1 = (mt1 + kMG1 - 1) / kMG1;
   int split = 1;
-  while (groups1 * split * 2 <= kWarps && split < P.split_max) split <<= 1;
-  for (int u = warp; u < groups1 * split; u += kWarps) {
+  while (groups1 * split * 2 <= NW && split < P.split_max) split <<= 1;
+  for (int u = warp; u < groups1 * split; u += NW) {
     const int grp = u / split, sl = u - grp * split;
     const int mt0 = grp * kMG1;
     double acc[kMG1][NTN][2];
@@ -437,28 +453,28 @@ __device__ __forceinline__ void gemm1(const DevProblem& P, int SK, int n08, int 
     }
   }
   before_sync();
-  __syncthreads();
+  sync();
   if (split > 1) {
-    for (int idx = tid; idx < n08 * TC; idx += kThreads) {
+    for (int idx = tid; idx < n08 * TC; idx += NW * 32) {
       const int a = idx / TC, t = idx - a * TC;
       double v = yp[idx];
       for (int sl = 1; sl < split; ++sl) v += yp[static_cast<size_t>(sl) * P.n08_max * TC + idx];
       yb[a * ldy + t] = v;
     }
-    __syncthreads();
+    sync();
   }
 }
 
-template <int TC, class Epi>
+template <int TC, class Epi, int NW = kWarps>
 __device__ __forceinline__ void gemm2(int S8, int n08, int ldn, const double* nop, const double* yb, int ldy,
                                       Epi& epi) {
   constexpr int NTN = TC / 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, tig = lane & 3;
   const int mt2 = S8 >> 3, ks2 = n08 >> 2;
-  for (int mb = warp; mb < mt2; mb += kWarps * kMG2) {
+  for (int mb = warp; mb < mt2; mb += NW * kMG2) {
 #pragma unroll
-    for (int m = 0; m < kMG2; ++m) epi.prefetch(m, mb + m * kWarps);
+    for (int m = 0; m < kMG2; ++m) epi.prefetch(m, mb + m * NW);
     double acc[kMG2][NTN][2];
 #pragma unroll
     for (int m = 0; m < kMG2; ++m)
@@ -472,7 +488,7 @@ __device__ __forceinline__ void gemm2(int S8, int n08, int ldn, const double* no
       for (int nn = 0; nn < NTN; ++nn) bf[nn] = yb[a * ldy + nn * 8 + g];
 #pragma unroll
       for (int m = 0; m < kMG2; ++m) {
-        const int mt = mb + m * kWarps;
+        const int mt = mb + m * NW;
         if (mt < mt2) {
           const double af = nop[(mt * 8 + g) * ldn + a];
 #pragma unroll
@@ -480,9 +496,10 @@ __device__ __forceinline__ void gemm2(int S8, int n08, int ldn, const double* no
         }
       }
     }
+    epi.before_store();
 #pragma unroll
     for (int m = 0; m < kMG2; ++m) {
-      const int mt = mb + m * kWarps;
+      const int mt = mb + m * NW;
       if (mt < mt2) {
 #pragma unroll
         for (int nn = 0; nn < NTN; ++nn) epi.store(m, mt, nn, acc[m][nn][0], acc[m][nn][1]);
@@ -494,6 +511,7 @@ __device__ __forceinline__ void gemm2(int S8, int n08, int ldn, const double* no
 // GEMM-2 epilogue of the patch/two-phase kernels: O back into kt.
 struct StoreO {
   double* kt; int ldk;
+  __device__ __forceinline__ void before_store() const {}
   __device__ __forceinline__ void prefetch(int, int) const {}
   __device__ __forceinline__ void store(int, int mt, int nn, double c0, double c1) const {
     const int lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
@@ -877,8 +895,8 @@ __device__ void patch_iteration(const DevProblem& P, int b, const double* x, int
 // ([t][ldk]) with TMA bulk copies on `bar` (thread 0 issues; the caller has
 // synchronised the CTA after the buffer's last generic-proxy use).
 __device__ __forceinline__ void stash_cols_bulk(const DevProblem& P, int c0, int nt, const double* src,
-                                                double* st, unsigned long long* bar) {
-  if (threadIdx.x == 0) {
+                                                double* st, unsigned long long* bar, int issuer = 0) {
+  if (threadIdx.x == issuer) {
     const unsigned bytes = static_cast<unsigned>(P.s_pad) * 8u;
     fence_proxy_async();
     mbar_expect_tx(bar, bytes * nt);
@@ -887,6 +905,23 @@ __device__ __forceinline__ void stash_cols_bulk(const DevProblem& P, int c0, int
     else
       for (int t = 0; t < nt; ++t)
         bulk_load(st + t * P.ldk, src + static_cast<size_t>(c0 + t) * P.s_pad, bytes, bar);
+  }
+}
+
+// λ staging at its own row stride `ldl` (the register epilogue's access
+// pattern is conflict free when 2*ldl % 16 is 4 or 12): one bulk copy per
+// column, issued in parallel by the lanes of the last warp.
+__device__ __forceinline__ void stash_lam_bulk(const DevProblem& P, int c0, int nt, const double* src,
+                                               double* st, int ldl, unsigned long long* bar) {
+  if ((threadIdx.x >> 5) == kWarps - 1) {
+    const int lane = threadIdx.x & 31;
+    const unsigned bytes = static_cast<unsigned>(P.s_pad) * 8u;
+    if (lane == 0) mbar_expect_tx(bar, bytes * nt);
+    __syncwarp();
+    if (lane < nt) {
+      fence_proxy_async();
+      bulk_load(st + lane * ldl, src + static_cast<size_t>(c0 + lane) * P.s_pad, bytes, bar);
+    }
   }
 }
 
@@ -912,9 +947,13 @@ struct StreamEpi {
   static constexpr int NTN = TC / 8;
   double* psi_n; double* lam_n; const double* q_pool;
   const long long* m_pos; const long long* m_s; const long long* m_q; const double* m_x;
-  const double* s_patch; const double* kt; double* lt; int ldk, S, nt;
+  const double* s_patch; const double* kt; double* lt; int ldk, ldl, S, nt;
   double pri_m, dual_m;
+  unsigned long long* lam_bar; unsigned lam_phase;   // if set: λ lands before the first store
   double qv[kMG2][NTN][2];
+  __device__ __forceinline__ void before_store() const {
+    if (lam_bar) mbar_wait(lam_bar, lam_phase);
+  }
   __device__ __forceinline__ void prefetch(int m, int mt) {
     const int lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
     const int p = mt * 8 + g;
@@ -933,7 +972,7 @@ struct StreamEpi {
     for (int e = 0; e < 2; ++e) {
       const int t = nn * 8 + 2 * tig + e;
       if (p < S && t < nt) {
-        const double kv = kt[t * ldk + p], lm = lt[t * ldk + p];
+        const double kv = kt[t * ldk + p], lm = lt[t * ldl + p];
         const double pn = qv[m][nn][e] + (e ? c1 : c0);
         const double ln = __dsub_rn(kv, pn);
         const double ps = fma(-s_patch[m_s[t] + p], m_x[t], kv);
@@ -942,7 +981,7 @@ struct StreamEpi {
         lam_n[pos] = ln;
         pri_m = fmax(pri_m, fabs(__dsub_rn(ln, lm)));
         dual_m = fmax(dual_m, fabs(__dsub_rn(pn, ps)));
-        lt[t * ldk + p] = __dsub_rn(pn, ln);
+        lt[t * ldl + p] = __dsub_rn(pn, ln);
       }
     }
   }
@@ -975,7 +1014,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + P.off_bar);   // ψ0, ψ1, λ
   const int ldk = P.ldk;
   double* psi_st = smem + P.off_k;                  // [2][TC][ldk]
-  double* lam_st = psi_st + 2 * TC * ldk;           // [TC][ldk]
+  double* lam_st = psi_st + 2 * TC * ldk;           // [TC][ldl]
+  const int ldl = P.ldl;
   const double* psi = P.psi[b];
   const double* lam = P.lam[b];
   double* part_out = P.part_buf[it & 1];
@@ -1016,7 +1056,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
     double x_first = 0.0;
     if (nch > 0) {
       stash_cols_bulk(P, chtab[1], chtab[2], psi, psi_st, bars + 0);
-      stash_cols_bulk(P, chtab[1], chtab[2], lam, lam_st, bars + 2);
+      stash_lam_bulk(P, chtab[1], chtab[2], lam, lam_st, ldl, bars + 2);
       if (nch > 1) stash_cols_bulk(P, chtab[CHW + 1], chtab[CHW + 2], psi, psi_st + TC * ldk, bars + 1);
       if (tid < chtab[2]) x_first = ld_cg(x + chtab[1] + tid);   // consumed after the Φ loop
     }
@@ -1064,9 +1104,10 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
     PT_LAP(P, 0)
     // K = ψ + s·x (= φ + λ) in place, zero padded to TC x S4 (GEMM 1 k-steps
     // of 4); one warp per column
-    auto k_pass = [&](double* kt, const long long* m_s, const double* m_x, int S, int nt_) {
+    auto k_pass = [&](double* kt, const long long* m_s, const double* m_x, int S, int nt_,
+                      int w0 = 0, int nw = kWarps) {
       const int S4 = (S + 3) & ~3;
-      for (int t = warp; t < TC; t += kWarps) {
+      for (int t = warp - w0; t < TC; t += nw) {
         double* kp = kt + t * ldk;
         const long long s0 = m_s[t];
         const double xc = m_x[t];
@@ -1082,6 +1123,69 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       __syncthreads();
     }
     PT_LAP(P, 1)
+    auto row_pass = [&](const long long* m_s, const double* m_x, int S, int nt_, int t0, int nthr) {
+      const int rlo = static_cast<int>(m_s[0]);
+      const int rhi = static_cast<int>(m_s[nt_ - 1]) + S;
+      for (int r = rlo + t0; r < rhi; r += nthr) {
+        double acc = c_patch[r];
+        for (int t = 0; t < nt_; ++t) {
+          const int p = r - static_cast<int>(m_s[t]);
+          if (p >= 0 && p < S) acc = fma(lam_st[t * ldl + p], m_x[t], acc);
+        }
+        c_patch[r] = acc;
+      }
+    };
+    if (P.warp_spec) {
+      // Hybrid pipeline: while warps 0..kCons-1 run GEMM 1 and GEMM 2 +
+      // epilogue of chunk ch (13 warps split GEMM 2's 26 m-tiles evenly), the
+      // other warps -- idle in the GEMMs -- build K(ch+1). The row pass of ch
+      // stays a whole-CTA phase (latency-bound, it needs every thread).
+      constexpr int kCons = 13, kProd = kWarps - kCons;
+      const bool prod = warp >= kCons;
+      const int ptid = tid - kCons * 32;
+      for (int ch = ch_a; ch < ch_b; ++ch) {
+        const int cq = ch - ch_a;
+        const int mb = cq & 1;
+        const bool has_next = ch + 1 < ch_b, has_next2 = ch + 2 < ch_b;
+        const int* ce = chtab + CHW * cq;
+        const int nt = ce[2], S = ce[3], S8 = (S + 7) & ~7, S4 = (S + 3) & ~3, n08 = ce[4], ldn = ce[5];
+        const long long* m_pos = meta0 + mb * 4 * TC;
+        const long long* m_s = m_pos + TC;
+        const long long* m_q = m_pos + 2 * TC;
+        const double* m_x = reinterpret_cast<const double*>(m_pos + 3 * TC);
+        double* kt = psi_st + mb * TC * ldk;
+        if (prod) {
+          if (has_next) {
+            if (ptid < TC) {
+              long long* mm = meta0 + (mb ^ 1) * 4 * TC;
+              const bool ok = ptid < ce[CHW + 2];
+              mm[ptid] = ok ? static_cast<long long>(ce[CHW + 1] + ptid) * P.s_pad : 0;
+              mm[TC + ptid] = ok ? ce[CHW + 8 + ptid] : 0;
+              mm[2 * TC + ptid] = ok ? static_cast<long long>(ce[CHW + 8 + TC + ptid]) * P.s_pad : 0;
+              reinterpret_cast<double*>(mm)[3 * TC + ptid] = ok ? ld_cg(x + ce[CHW + 1] + ptid) : 0.0;
+            }
+            nbar_sync(6, kProd * 32);
+            mbar_wait(bars + (mb ^ 1), ph[mb ^ 1]);
+            const long long* mn = meta0 + (mb ^ 1) * 4 * TC;
+            k_pass(psi_st + (mb ^ 1) * TC * ldk, mn + TC, reinterpret_cast<const double*>(mn + 3 * TC),
+                   ce[CHW + 3], ce[CHW + 2], kCons, kProd);
+          }
+        } else {
+          gemm1<TC, NoHook, kCons, GroupBar<kCons>>(P, S4, n08, ldn, smem, kt, ldk, yb, P.ldy, yp);
+          StreamEpi<TC> epi{P.psi[b ^ 1], P.lam[b ^ 1], P.q_pool, m_pos, m_s, m_q, m_x,
+                            s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, bars + 2, ph[2]};
+          gemm2<TC, StreamEpi<TC>, kCons>(S8, n08, ldn, smem, yb, P.ldy, epi);
+          pri_m = epi.pri_m; dual_m = epi.dual_m;
+        }
+        ph[2] ^= 1u;
+        if (has_next) ph[mb ^ 1] ^= 1u;
+        __syncthreads();
+        row_pass(m_s, m_x, S, nt, tid, kThreads);
+        __syncthreads();
+        if (has_next) stash_lam_bulk(P, ce[CHW + 1], ce[CHW + 2], lam, lam_st, ldl, bars + 2);
+        if (has_next2) stash_cols_bulk(P, ce[2 * CHW + 1], ce[2 * CHW + 2], psi, kt, bars + mb);
+      }
+    } else
     // chunk pipeline: GEMM 1 -> GEMM 2 + epilogue -> (row pass of this chunk
     // | K pass of the next) -> stage λ(next) and ψ(next+1)
     for (int ch = ch_a; ch < ch_b; ++ch) {
@@ -1109,7 +1213,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       }
       PT_LAP(P, 2)
       StreamEpi<TC> epi{P.psi[b ^ 1], P.lam[b ^ 1], P.q_pool, m_pos, m_s, m_q, m_x,
-                        s_patch, kt, lam_st, ldk, S, nt, pri_m, dual_m};
+                        s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, nullptr, 0u};
       gemm2<TC>(S8, n08, ldn, smem, yb, P.ldy, epi);
       pri_m = epi.pri_m; dual_m = epi.dual_m;
       __syncthreads();
@@ -1123,7 +1227,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
           double acc = c_patch[r];
           for (int t = 0; t < nt; ++t) {
             const int p = r - static_cast<int>(m_s[t]);
-            if (p >= 0 && p < S) acc = fma(lam_st[t * ldk + p], m_x[t], acc);
+            if (p >= 0 && p < S) acc = fma(lam_st[t * ldl + p], m_x[t], acc);
           }
           c_patch[r] = acc;
         }
@@ -1137,7 +1241,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
                ce[CHW + 3], ce[CHW + 2]);
       }
       __syncthreads();
-      if (has_next) stash_cols_bulk(P, ce[CHW + 1], ce[CHW + 2], lam, lam_st, bars + 2);
+      if (has_next) stash_lam_bulk(P, ce[CHW + 1], ce[CHW + 2], lam, lam_st, ldl, bars + 2);
       if (has_next2) stash_cols_bulk(P, ce[2 * CHW + 1], ce[2 * CHW + 2], psi, kt, bars + mb);
       PT_LAP(P, 4)
     }
