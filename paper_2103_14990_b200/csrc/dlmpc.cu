@@ -307,7 +307,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           ch_max = 0;
           for (size_t u = 0; u + 1 < u_chunk.size(); ++u) ch_max = std::max<long long>(ch_max, u_chunk[u + 1] - u_chunk[u]);
           // chunk table [ch][8 ints], patch table [q][6 doubles], row map [rows] ints
-          extra = (long long)(ch_max + 1) * (8 + 2 * tc) / 2 + 6 * np_max + np_max + (cap + 2) / 2 + 16;
+          extra = (long long)(ch_max + 1) * (8 + 2 * tc) / 2 + 6 * np_max + np_max + (cap + 2) / 2 + 32;
           const long long need = fixed + 2 * ((cap + 1) & ~1LL) + extra;
           if (need <= limit) { ok = prows_max <= cap; break; }
           cap -= (need - limit + 1) / 2 + 16;
@@ -333,17 +333,19 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
             // host-built control tables (see DevProblem)
             const int chw = 8 + 2 * tc;
             const size_t nu = u_lo.size();
-            st_unit_desc.assign(nu * 12, 0);
+            st_unit_desc.assign(nu * 16, 0);
             st_chunk_desc.assign(ch_cls.size() * chw, 0);
             st_ptab.clear();
             int pt_off = 0;
             for (size_t u = 0; u < nu; ++u) {
               const long long prow0 = pr->row_start[p_lo[u]];
-              int* ud = &st_unit_desc[u * 12];
+              int* ud = &st_unit_desc[u * 16];
               ud[0] = u_lo[u]; ud[1] = u_hi[u]; ud[2] = p_lo[u]; ud[3] = p_hi[u];
               ud[4] = (int)(prow0 & 0xffffffffLL); ud[5] = (int)(prow0 >> 32);
               ud[6] = (int)(pr->row_start[p_hi[u]] - prow0); ud[7] = u_chunk[u]; ud[8] = u_chunk[u + 1];
               ud[9] = pt_off;
+              if (u_chunk[u + 1] > u_chunk[u]) { ud[10] = ch_n[u_chunk[u]]; ud[11] = ch_c0[u_chunk[u]]; }
+              if (u_chunk[u + 1] > u_chunk[u] + 1) ud[12] = ch_n[u_chunk[u] + 1];
               for (int ch = u_chunk[u]; ch < u_chunk[u + 1]; ++ch) {
                 int* cd = &st_chunk_desc[(size_t)ch * chw];
                 const int k = ch_cls[ch];
@@ -398,6 +400,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
             P.off_pada = (int)off; off += np_max;
             P.off_rowq = (int)off; off += (cap + 2) / 2;
             off = (off + 1) & ~1LL;
+            P.off_udesc = (int)off; off += 16;
             P.off_bar = (int)off; off += 4;
             P.bulk_copy = bulk ? 1 : 0;
             P.cache_phi = 0; P.stash_bufs = 0; P.off_stash = (int)off; P.off_phimeta = (int)off;

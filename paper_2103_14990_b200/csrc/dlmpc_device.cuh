@@ -106,9 +106,11 @@ struct DevProblem {
   int off_ptab, np_cap;        // per-unit patch-subsystem table: [np_cap][6] doubles
   int off_rowq;                // per patch row: its patch-subsystem index (int)
   int off_pada;                // per patch subsystem: ||a||^2 of this MPC step
+  int off_udesc;               // two unit descriptors (16 ints each)
   int off_bar;                 // 3 mbarriers (ψ buffers, λ buffer)
   // stream mode, host-built control tables (one coalesced copy per unit):
-  //   unit_desc [u][12] ints: own_lo, own_hi, plo, phi, prow0 (2 ints), prows, ch_a, ch_b, pt_off, -, -
+  //   unit_desc [u][16] ints: own_lo, own_hi, plo, phi, prow0 (2 ints), prows, ch_a, ch_b, pt_off,
+  //     nt and c0 of the first chunk, nt of the second (0 if none), -, -, -
   //   chunk_desc [ch][8 + 2*TC] ints: k, c0, nt, S, n08, ldn, null_off (2 ints), then per column slot t
   //     s0 (row of support slot 0, unit-local) and q (particular-solution vector index)
   //   unit_ptab [pt_off + q][6] doubles: (rowoff, rows, slots, own slot) ints | part_off | - | r0 | (own, -)
@@ -1024,11 +1026,31 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
   double pri_m = 0.0, dual_m = 0.0;
   PT_DECL
   constexpr int CHW = 8 + 2 * TC;   // ints per chunk descriptor
-  for (int un = P.cta_unit_ptr[blockIdx.x]; un < P.cta_unit_ptr[blockIdx.x + 1]; ++un) {
+  // unit descriptors, double-buffered in shared memory: the next unit's is
+  // fetched (cp.async) while the current unit runs
+  int* udesc = reinterpret_cast<int*>(smem + P.off_udesc);   // [2][16]
+  const int un_a = P.cta_unit_ptr[blockIdx.x], un_b = P.cta_unit_ptr[blockIdx.x + 1];
+  if (un_a < un_b && tid < 4)
+    reinterpret_cast<int4*>(udesc)[tid] = __ldg(reinterpret_cast<const int4*>(P.unit_desc) + 4 * un_a + tid);
+  __syncthreads();
+  for (int un = un_a; un < un_b; ++un) {
     PT_START
-    const int4 ud0 = __ldg(reinterpret_cast<const int4*>(P.unit_desc) + 3 * un);
-    const int4 ud1 = __ldg(reinterpret_cast<const int4*>(P.unit_desc) + 3 * un + 1);
-    const int4 ud2 = __ldg(reinterpret_cast<const int4*>(P.unit_desc) + 3 * un + 2);
+    const int ub = (un - un_a) & 1;
+    const int4 ud0 = reinterpret_cast<const int4*>(udesc + 16 * ub)[0];
+    const int4 ud1 = reinterpret_cast<const int4*>(udesc + 16 * ub)[1];
+    const int4 ud2 = reinterpret_cast<const int4*>(udesc + 16 * ub)[2];
+    const int4 ud3 = reinterpret_cast<const int4*>(udesc + 16 * ub)[3];
+    if (un + 1 < un_b && tid < 4) {
+      cp_async16(reinterpret_cast<double*>(udesc + 16 * (ub ^ 1) + 4 * tid),
+                 reinterpret_cast<const double*>(P.unit_desc + 16 * static_cast<size_t>(un + 1) + 4 * tid));
+    }
+    cp_async_commit();
+    // the first chunks' ψ/λ copies start before the tables arrive
+    if (ud2.z > 0) {
+      stash_cols_bulk(P, ud2.w, ud2.z, psi, psi_st, bars + 0);
+      stash_lam_bulk(P, ud2.w, ud2.z, lam, lam_st, ldl, bars + 2);
+      if (ud3.x > 0) stash_cols_bulk(P, ud2.w + ud2.z, ud3.x, psi, psi_st + TC * ldk, bars + 1);
+    }
     const int own_lo = ud0.x, own_hi = ud0.y, plo = ud0.z, phi_ = ud0.w;
     const long long prow0 = static_cast<long long>(static_cast<unsigned>(ud1.x)) |
                             (static_cast<long long>(ud1.y) << 32);
@@ -1046,6 +1068,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       for (int q = tid; q < npq; q += kThreads) pada[q] = ld_cg(P.ada + plo + q);
     }
     __syncthreads();
+    PT_LAP(P, 2)
     for (int q = warp; q < npq; q += kWarps) {
       const int* ei = reinterpret_cast<const int*>(ptab + 6 * q);
       for (int l = lane; l < ei[1]; l += 32) rowq[ei[0] + l] = q;
@@ -1054,12 +1077,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
     // staging: ψ(a) -> ψ buffer 0, λ(a) -> λ buffer, ψ(a+1) -> ψ buffer 1
     // (TMA bulk copies, one per chunk and array; mbarriers ψ0, ψ1, λ)
     double x_first = 0.0;
-    if (nch > 0) {
-      stash_cols_bulk(P, chtab[1], chtab[2], psi, psi_st, bars + 0);
-      stash_lam_bulk(P, chtab[1], chtab[2], lam, lam_st, ldl, bars + 2);
-      if (nch > 1) stash_cols_bulk(P, chtab[CHW + 1], chtab[CHW + 2], psi, psi_st + TC * ldk, bars + 1);
-      if (tid < chtab[2]) x_first = ld_cg(x + chtab[1] + tid);   // consumed after the Φ loop
-    }
+    if (nch > 0 && tid < chtab[2]) x_first = ld_cg(x + chtab[1] + tid);   // consumed after the Φ loop
+    PT_LAP(P, 3)
     // Φ scales of the patch rows
     if (it == 0) {
       for (int i = plo + warp; i < phi_; i += kWarps) {
@@ -1073,23 +1092,42 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
         phi_rows_of<false>(P, i, psi, lam, x, out);
       }
     } else {
-      // from the per-unit dot partials of the last iteration (slot order)
-      for (int r = tid; r < prows; r += kThreads) {
-        const int q = rowq[r];
-        const double* e = ptab + 6 * q;
-        const int* ei = reinterpret_cast<const int*>(e);
-        const int l = r - ei[0], nr = ei[1], np = ei[2];
-        const long long grow = reinterpret_cast<const long long*>(e)[4] + l;
-        const double* pb = part_in + reinterpret_cast<const long long*>(e)[2] + l;
-        const double w = P.row_w[grow], lo = P.row_lo[grow], hi = P.row_hi[grow];
-        double c = ld_cg(pb);
-        for (int sl = 1; sl < np; ++sl) c += ld_cg(pb + sl * nr);
-        const double ada = pada[q];
-        const double y0 = __ddiv_rn(__dmul_rn(rho, c), __dadd_rn(rho, __dmul_rn(__dmul_rn(2.0, w), ada)));
-        const double y = fmin(fmax(y0, lo), hi);
-        const double sv = ada > 0.0 ? __ddiv_rn(__dsub_rn(y, c), ada) : 0.0;
-        s_patch[r] = sv;
-        if (ei[10]) P.s_row[grow] = sv;
+      // from the per-unit dot partials of the last iteration (slot order);
+      // every thread issues the loads of up to kRB rows before using any
+      constexpr int kRB = 3;
+      for (int r0 = tid; r0 < prows; r0 += kRB * kThreads) {
+        double w[kRB], lo[kRB], hi[kRB], c[kRB], ada[kRB];
+        long long grow[kRB];
+        bool own[kRB], ok[kRB];
+#pragma unroll
+        for (int u = 0; u < kRB; ++u) {
+          const int r = r0 + u * kThreads;
+          ok[u] = r < prows;
+          w[u] = lo[u] = hi[u] = c[u] = ada[u] = 0.0;
+          grow[u] = 0; own[u] = false;
+          if (ok[u]) {
+            const int q = rowq[r];
+            const double* e = ptab + 6 * q;
+            const int* ei = reinterpret_cast<const int*>(e);
+            const int l = r - ei[0], nr = ei[1], np = ei[2];
+            grow[u] = reinterpret_cast<const long long*>(e)[4] + l;
+            own[u] = ei[10] != 0;
+            ada[u] = pada[q];
+            const double* pb = part_in + reinterpret_cast<const long long*>(e)[2] + l;
+            w[u] = __ldg(P.row_w + grow[u]); lo[u] = __ldg(P.row_lo + grow[u]); hi[u] = __ldg(P.row_hi + grow[u]);
+            c[u] = __ldcg(pb);
+            for (int sl = 1; sl < np; ++sl) c[u] += __ldcg(pb + sl * nr);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kRB; ++u) {
+          if (!ok[u]) continue;
+          const double y0 = __ddiv_rn(__dmul_rn(rho, c[u]), __dadd_rn(rho, __dmul_rn(__dmul_rn(2.0, w[u]), ada[u])));
+          const double y = fmin(fmax(y0, lo[u]), hi[u]);
+          const double sv = ada[u] > 0.0 ? __ddiv_rn(__dsub_rn(y, c[u]), ada[u]) : 0.0;
+          s_patch[r0 + u * kThreads] = sv;
+          if (own[u]) P.s_row[grow[u]] = sv;
+        }
       }
     }
     if (nch > 0 && tid < TC) {
@@ -1122,7 +1160,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       k_pass(psi_st, meta0 + TC, reinterpret_cast<const double*>(meta0 + 3 * TC), chtab[3], chtab[2]);
       __syncthreads();
     }
-    PT_LAP(P, 1)
+    PT_LAP(P, 4)
     auto row_pass = [&](const long long* m_s, const double* m_x, int S, int nt_, int t0, int nthr) {
       const int rlo = static_cast<int>(m_s[0]);
       const int rhi = static_cast<int>(m_s[nt_ - 1]) + S;
@@ -1245,6 +1283,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       if (has_next2) stash_cols_bulk(P, ce[2 * CHW + 1], ce[2 * CHW + 2], psi, kt, bars + mb);
       PT_LAP(P, 4)
     }
+    PT_LAP(P, 1)
+    cp_async_wait<0>();   // next unit's descriptor
     // this unit's Φ-dot partials -> its slot of every patch row
     for (int r = tid; r < prows; r += kThreads) {
       const int q = rowq[r];
@@ -1254,6 +1294,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
           c_patch[r];
     }
     __syncthreads();
+    PT_LAP(P, 7)
   }
   PT_START
   publish_residuals(P, it, pri_m, dual_m, smem + P.off_red);
