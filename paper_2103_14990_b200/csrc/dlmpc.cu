@@ -351,7 +351,11 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
                 const int k = ch_cls[ch];
                 cd[0] = k; cd[1] = ch_c0[ch]; cd[2] = ch_n[ch]; cd[3] = pr->class_s[k];
                 cd[4] = (pr->class_n0[k] + 7) & ~7; cd[5] = pr->class_ldn[k];
-                cd[6] = (int)(pr->class_null_off[k] & 0xffffffffLL); cd[7] = (int)(pr->class_null_off[k] >> 32);
+                // paired: columns (2q, 2q+1) of the chunk share their support rows
+                bool paired = true;
+                for (int t = 0; t + 1 < ch_n[ch]; t += 2)
+                  paired = paired && pr->col_rowbase[ch_c0[ch] + t] == pr->col_rowbase[ch_c0[ch] + t + 1];
+                cd[6] = paired ? 1 : 0;
                 for (int t = 0; t < ch_n[ch]; ++t) {
                   const int c = ch_c0[ch] + t;
                   cd[8 + t] = (int)(pr->col_rowbase[c] - prow0);

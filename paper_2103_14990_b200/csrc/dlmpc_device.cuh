@@ -111,7 +111,7 @@ struct DevProblem {
   // stream mode, host-built control tables (one coalesced copy per unit):
   //   unit_desc [u][16] ints: own_lo, own_hi, plo, phi, prow0 (2 ints), prows, ch_a, ch_b, pt_off,
   //     nt and c0 of the first chunk, nt of the second (0 if none), -, -, -
-  //   chunk_desc [ch][8 + 2*TC] ints: k, c0, nt, S, n08, ldn, null_off (2 ints), then per column slot t
+  //   chunk_desc [ch][8 + 2*TC] ints: k, c0, nt, S, n08, ldn, paired, -, then per column slot t
   //     s0 (row of support slot 0, unit-local) and q (particular-solution vector index)
   //   unit_ptab [pt_off + q][6] doubles: (rowoff, rows, slots, own slot) ints | part_off | - | r0 | (own, -)
   const int* unit_desc; const int* chunk_desc; const double* unit_ptab;
@@ -952,6 +952,7 @@ struct StreamEpi {
   const double* s_patch; const double* kt; double* lt; int ldk, ldl, S, nt;
   double pri_m, dual_m;
   unsigned long long* lam_bar; unsigned lam_phase;   // if set: λ lands before the first store
+  bool paired;   // column pairs (2q, 2q+1) share support rows (host flag per chunk)
   double qv[kMG2][NTN][2];
   __device__ __forceinline__ void before_store() const {
     if (lam_bar) mbar_wait(lam_bar, lam_phase);
@@ -970,6 +971,7 @@ struct StreamEpi {
   __device__ __forceinline__ void store(int m, int mt, int nn, double c0, double c1) {
     const int lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
     const int p = mt * 8 + g;
+    double contrib = 0.0;   // paired chunks: this pair's share of the row's next Φ dot
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int t = nn * 8 + 2 * tig + e;
@@ -983,9 +985,14 @@ struct StreamEpi {
         lam_n[pos] = ln;
         pri_m = fmax(pri_m, fabs(__dsub_rn(ln, lm)));
         dual_m = fmax(dual_m, fabs(__dsub_rn(pn, ps)));
-        lt[t * ldl + p] = __dsub_rn(pn, ln);
+        const double v = __dsub_rn(pn, ln);
+        if (paired) contrib = e ? fma(v, m_x[t], contrib) : __dmul_rn(v, m_x[t]);
+        else lt[t * ldl + p] = v;
       }
     }
+    // the pair's two columns share support rows: one value in the even slot
+    // (both of its λ reads above were this thread's own)
+    if (paired && p < S && nn * 8 + 2 * tig < nt) lt[(nn * 8 + 2 * tig) * ldl + p] = contrib;
   }
 };
 
@@ -1161,14 +1168,21 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       __syncthreads();
     }
     PT_LAP(P, 4)
-    auto row_pass = [&](const long long* m_s, const double* m_x, int S, int nt_, int t0, int nthr) {
+    auto row_pass = [&](const long long* m_s, const double* m_x, int S, int nt_, int t0, int nthr, bool paired) {
       const int rlo = static_cast<int>(m_s[0]);
       const int rhi = static_cast<int>(m_s[nt_ - 1]) + S;
       for (int r = rlo + t0; r < rhi; r += nthr) {
         double acc = c_patch[r];
-        for (int t = 0; t < nt_; ++t) {
-          const int p = r - static_cast<int>(m_s[t]);
-          if (p >= 0 && p < S) acc = fma(lam_st[t * ldl + p], m_x[t], acc);
+        if (paired) {
+          for (int t = 0; t < nt_; t += 2) {
+            const int p = r - static_cast<int>(m_s[t]);
+            if (p >= 0 && p < S) acc += lam_st[t * ldl + p];
+          }
+        } else {
+          for (int t = 0; t < nt_; ++t) {
+            const int p = r - static_cast<int>(m_s[t]);
+            if (p >= 0 && p < S) acc = fma(lam_st[t * ldl + p], m_x[t], acc);
+          }
         }
         c_patch[r] = acc;
       }
@@ -1211,14 +1225,14 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
         } else {
           gemm1<TC, NoHook, kCons, GroupBar<kCons>>(P, S4, n08, ldn, smem, kt, ldk, yb, P.ldy, yp);
           StreamEpi<TC> epi{P.psi[b ^ 1], P.lam[b ^ 1], P.q_pool, m_pos, m_s, m_q, m_x,
-                            s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, bars + 2, ph[2]};
+                            s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, bars + 2, ph[2], ce[6] != 0};
           gemm2<TC, StreamEpi<TC>, kCons>(S8, n08, ldn, smem, yb, P.ldy, epi);
           pri_m = epi.pri_m; dual_m = epi.dual_m;
         }
         ph[2] ^= 1u;
         if (has_next) ph[mb ^ 1] ^= 1u;
         __syncthreads();
-        row_pass(m_s, m_x, S, nt, tid, kThreads);
+        row_pass(m_s, m_x, S, nt, tid, kThreads, ce[6] != 0);
         __syncthreads();
         if (has_next) stash_lam_bulk(P, ce[CHW + 1], ce[CHW + 2], lam, lam_st, ldl, bars + 2);
         if (has_next2) stash_cols_bulk(P, ce[2 * CHW + 1], ce[2 * CHW + 2], psi, kt, bars + mb);
@@ -1251,25 +1265,14 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       }
       PT_LAP(P, 2)
       StreamEpi<TC> epi{P.psi[b ^ 1], P.lam[b ^ 1], P.q_pool, m_pos, m_s, m_q, m_x,
-                        s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, nullptr, 0u};
+                        s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, nullptr, 0u, ce[6] != 0};
       gemm2<TC>(S8, n08, ldn, smem, yb, P.ldy, epi);
       pri_m = epi.pri_m; dual_m = epi.dual_m;
       __syncthreads();
       PT_LAP(P, 3)
       // banded pass: row r of the patch gets v'(r - s0_t, t)·x_t from every
       // chunk column t whose support holds it, in ascending column order
-      {
-        const int rlo = static_cast<int>(m_s[0]);
-        const int rhi = static_cast<int>(m_s[nt - 1]) + S;
-        for (int r = rlo + tid; r < rhi; r += kThreads) {
-          double acc = c_patch[r];
-          for (int t = 0; t < nt; ++t) {
-            const int p = r - static_cast<int>(m_s[t]);
-            if (p >= 0 && p < S) acc = fma(lam_st[t * ldl + p], m_x[t], acc);
-          }
-          c_patch[r] = acc;
-        }
-      }
+      row_pass(m_s, m_x, S, nt, tid, kThreads, ce[6] != 0);
       if (has_next) {   // next chunk: operator, ψ landed, K
         const long long* mn = meta0 + (mb ^ 1) * 4 * TC;
         stage_operator_sized(P, ce[CHW], (ce[CHW + 3] + 7) & ~7, ce[CHW + 5], smem, cur);
