@@ -799,9 +799,23 @@ __device__ __forceinline__ void phi_rows_cached(const DevProblem& P, int q, int 
 }
 
 // One ADMM iteration of the patch kernel for this CTA's units.
+// The stop test of iteration it-1 (global residual maxima, published before
+// the grid barrier) is overlapped with iteration it's first Φ stage: the two
+// words are fetched first, the unit's Φ goes to shared memory only, then the
+// test; on convergence the CTA returns `true` with the state of iteration
+// it-1 untouched (ψ, λ and the global s_row of its own rows). Every CTA reads
+// the same words, so the decision is grid-uniform.
+__device__ __forceinline__ bool patch_stop_test(const DevProblem& P, const RunArgs& R, int it,
+                                                unsigned long long rp, unsigned long long rd) {
+  const double pri = __longlong_as_double(static_cast<long long>(rp));
+  const double dual = P.rho * __longlong_as_double(static_cast<long long>(rd));
+  if (blockIdx.x == 0 && threadIdx.x == 0) { R.hist[2 * (it - 1)] = pri; R.hist[2 * (it - 1) + 1] = dual; }
+  return R.stop_on_conv && pri <= R.eps_pri && dual <= R.eps_dual;
+}
+
 template <int TC>
-__device__ void patch_iteration(const DevProblem& P, int b, const double* x, int it, double* smem,
-                                int& cur) {
+__device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int it, double* smem,
+                                int& cur, const RunArgs& R) {
   double* s_patch = smem + P.off_patch;
   long long* m_pos = reinterpret_cast<long long*>(smem + P.off_meta);
   double* m_x = smem + P.off_meta + 3 * TC;
@@ -809,8 +823,13 @@ __device__ void patch_iteration(const DevProblem& P, int b, const double* x, int
   const double* psi = P.psi[b];
   const double* lam = P.lam[b];
   double pri_m = 0.0, dual_m = 0.0;
+  bool tested = it == 0;
+  unsigned long long rp = 0, rd = 0;
+  if (!tested) { rp = __ldcg(P.resid + 2 * (it - 1)); rd = __ldcg(P.resid + 2 * (it - 1) + 1); }
   PT_DECL
-  for (int un = P.cta_unit_ptr[blockIdx.x]; un < P.cta_unit_ptr[blockIdx.x + 1]; ++un) {
+  const int un_a = P.cta_unit_ptr[blockIdx.x];
+  if (un_a == P.cta_unit_ptr[blockIdx.x + 1] && !tested && patch_stop_test(P, R, it, rp, rd)) return true;
+  for (int un = un_a; un < P.cta_unit_ptr[blockIdx.x + 1]; ++un) {
     PT_START
     const int own_lo = P.unit_sub_lo[un], own_hi = P.unit_sub_hi[un];
     const int plo = P.unit_patch_lo[un], phi_ = P.unit_patch_hi[un];
@@ -822,11 +841,12 @@ __device__ void patch_iteration(const DevProblem& P, int b, const double* x, int
     const int stash_stride = 2 * TC * P.ldk;
     if (P.stash_bufs > 0 && ch_a < ch_b)
       stash_issue(P, P.chunk_col0[ch_a], P.chunk_n[ch_a], P.class_s[P.chunk_class[ch_a]], psi, lam, stash);
-    // Φ scale of every row the unit's columns touch (own rows + d-hop halo)
+    // Φ scale of every row the unit's columns touch (own rows + d-hop halo);
+    // before the stop test the own rows' s goes to shared memory only
     for (int i = plo + warp; i < phi_; i += kWarps) {
       const int r_off = static_cast<int>(P.row_start[i] - prow0);
       double* dst = s_patch + r_off;
-      double* gdst = (i >= own_lo && i < own_hi) ? P.s_row + P.row_start[i] : nullptr;
+      double* gdst = (tested && i >= own_lo && i < own_hi) ? P.s_row + P.row_start[i] : nullptr;
       auto out = [dst, gdst](int l, double s) {
         dst[l] = s;
         if (gdst) gdst[l] = s;
@@ -838,6 +858,16 @@ __device__ void patch_iteration(const DevProblem& P, int b, const double* x, int
         phi_rows_of<false>(P, i, psi, lam, x, out);
     }
     __syncthreads();
+    if (!tested) {
+      tested = true;
+      if (patch_stop_test(P, R, it, rp, rd)) {
+        cp_async_wait<0>();
+        return true;
+      }
+      const long long o0 = P.row_start[own_lo];
+      const int on = static_cast<int>(P.row_start[own_hi] - o0), off0 = static_cast<int>(o0 - prow0);
+      for (int r = threadIdx.x; r < on; r += kThreads) P.s_row[o0 + r] = s_patch[off0 + r];
+    }
     PT_LAP(P, 0)
     // chunk pipeline: ψ,λ of chunk i+1 stream into the other staging buffer
     // (cp.async) while chunk i runs its GEMMs
@@ -874,6 +904,7 @@ __device__ void patch_iteration(const DevProblem& P, int b, const double* x, int
   PT_START
   publish_residuals(P, it, pri_m, dual_m, smem + P.off_red);
   PT_LAP(P, 5)
+  return false;
 }
 
 
@@ -1440,12 +1471,28 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
     if (MODE == kPatch && P.cache_phi) cache_phi_meta(P, x, smem);
     int it = 0;
     bool conv = false;
-    while (it < R.max_iters) {
-      PT_DECL
-      if (MODE == kPatch) {
-        patch_iteration<TC>(P, b, x, it, smem, cur);
+    if (MODE == kPatch) {
+      // stop test of iteration it-1 overlapped with iteration it's first Φ
+      while (true) {
+        PT_DECL
+        if (it == R.max_iters) {
+          if (it > 0) {
+            const unsigned long long rp = __ldcg(P.resid + 2 * (it - 1)), rd = __ldcg(P.resid + 2 * (it - 1) + 1);
+            conv = patch_stop_test(P, R, it, rp, rd);
+          }
+          break;
+        }
+        if (patch_iteration<TC>(P, b, x, it, smem, cur, R)) { conv = true; break; }
         PT_START
-      } else if (MODE == kStream) {
+        grid.sync();
+        PT_LAP(P, 6)
+        b ^= 1;
+        ++it;
+      }
+    }
+    while (MODE != kPatch && it < R.max_iters) {
+      PT_DECL
+      if (MODE == kStream) {
         stream_iteration<TC>(P, b, x, it, smem, cur, ph);
         PT_START
       } else {
