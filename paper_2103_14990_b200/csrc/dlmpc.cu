@@ -456,6 +456,10 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       P.off_k = (int)off; off += (long long)tc * ldk;
       P.off_y = (int)off; off += (long long)n08_max * ldy;
       P.off_yp = (int)off; off += split_max > 1 ? (long long)split_max * n08_max * tc : 0;
+      {   // GEMV partials of small chunks share the split-K partials region
+        const char* e = getenv("DLMPC_SMALL_GEMV");
+        P.small_gemv = (split_max > 1 && (long long)split_max * tc >= 10 && !(e && e[0] == '0')) ? 1 : 0;
+      }
       P.off_red = (int)off; off += 32;
       P.off_meta = (int)off; off += 4 * tc;
       P.off_patch = (int)off; off += (prows_max + 1) & ~1LL;

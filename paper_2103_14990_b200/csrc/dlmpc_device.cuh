@@ -118,6 +118,7 @@ struct DevProblem {
   int bulk_copy;               // stream staging by TMA bulk copies (1) or cp.async (0)
   int ldl;                     // stream mode: row stride of the λ stash
   int warp_spec;               // stream mode: producer/consumer warp specialisation
+  int small_gemv;              // patch mode: DFMA GEMV for GEMM 1 of chunks with <= 2 columns
 };
 
 struct RunArgs {
@@ -510,6 +511,42 @@ __device__ __forceinline__ void gemm2(int S8, int n08, int ldn, const double* no
   }
 }
 
+// GEMM 1 for chunks of at most two live columns (C2-sized networks): a DFMA
+// GEMV, Y[a][t] = sum_p N[p][a] K[t][p], split over support slices whose
+// partials are reduced in shared memory (`part`, >= 10*n08 doubles). Lanes
+// walk consecutive a (conflict free for any ldn); K is a broadcast. Columns
+// t >= nt of Y are zeroed for GEMM 2. Measured 1.2 vs 1.6 us (split-K DMMA).
+template <int TC>
+__device__ __forceinline__ void gemv1_small(int S, int n08, int ldn, const double* nop, const double* kt, int ldk,
+                                            double* part, double* yb, int ldy, int nt) {
+  constexpr int PS = 5;
+  const int tid = threadIdx.x;
+  const int a = tid % n08, rest = tid / n08;   // n08 x (t, ps)
+  const int t = rest & 1, ps = rest >> 1;
+  const int pl = (S + PS - 1) / PS;
+  if (ps < PS && t < nt) {
+    const int p0 = ps * pl, p1 = min(S, p0 + pl);
+    const double* kr = kt + t * ldk;
+    double c0 = 0.0, c1 = 0.0;
+    int p = p0;
+    for (; p + 1 < p1; p += 2) {
+      c0 = fma(nop[p * ldn + a], kr[p], c0);
+      c1 = fma(nop[(p + 1) * ldn + a], kr[p + 1], c1);
+    }
+    if (p < p1) c0 = fma(nop[p * ldn + a], kr[p], c0);
+    part[(ps * 2 + t) * n08 + a] = c0 + c1;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < n08 * TC; idx += kThreads) {
+    const int aa = idx / TC, tt = idx - aa * TC;
+    double v = 0.0;
+    if (tt < nt)
+      for (int q = 0; q < PS; ++q) v += part[(q * 2 + tt) * n08 + aa];
+    yb[aa * ldy + tt] = v;
+  }
+  __syncthreads();
+}
+
 // GEMM-2 epilogue of the patch/two-phase kernels: O back into kt.
 struct StoreO {
   double* kt; int ldk;
@@ -592,7 +629,10 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
   }
   __syncthreads();
   PT_LAP(P, 1)
-  gemm1<TC>(P, S8, n08, ldn, nop, kt, ldk, yb, ldy, yp);
+  if (TC == 8 && nt <= 2 && P.small_gemv && n08 * 10 <= kThreads)
+    gemv1_small<TC>(S, n08, ldn, nop, kt, ldk, yp, yb, ldy, nt);
+  else
+    gemm1<TC>(P, S8, n08, ldn, nop, kt, ldk, yb, ldy, yp);
   PT_LAP(P, 2)
   // GEMM 2: O[t][p] = sum_a N[p][a] Y[a][t]  (M = S, N = TC, K = n0) -> kt
   StoreO epi{kt, ldk};
