@@ -431,7 +431,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         while (groups1 * sp * 2 <= kWarps && sp < 4) sp <<= 1;
         split_max = std::max(split_max, sp);
       }
-      const long long meta_phi = np_max * pr->d_pad * 2 + np_max + 3 * prows_max + (np_max + 1) / 2 + 2;
+      const long long meta_phi = np_max * pr->d_pad * 2 + np_max + 3 * prows_max + (np_max + 1) / 2 + np_max + 8 + 2;
       auto total = [&](long long opr, int sp, bool cache) {
         return opr + (long long)tc * ldk + (long long)n08_max * ldy + (sp > 1 ? (long long)sp * n08_max * tc : 0)
                + 32 + 4 * tc + prows_max + (cache ? meta_phi : 0) + 4;
@@ -465,6 +465,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       P.off_patch = (int)off; off += (prows_max + 1) & ~1LL;
       P.patch_cap = (int)prows_max;
       P.off_phimeta = (int)off; off += cache ? meta_phi : 0;
+      P.off_ublk = (int)(off - (np_max + 8 + 2));   // tail of the Φ metadata block (cache only)
       P.cache_phi = cache ? 1 : 0;
       off = (off + 1) & ~1LL;   // 16-byte alignment for cp.async
       P.off_stash = (int)off; off += stash_bufs * stash_one;

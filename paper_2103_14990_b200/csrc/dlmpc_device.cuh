@@ -107,6 +107,7 @@ struct DevProblem {
   int off_rowq;                // per patch row: its patch-subsystem index (int)
   int off_pada;                // per patch subsystem: ||a||^2 of this MPC step
   int off_udesc;               // two unit descriptors (16 ints each)
+  int off_ublk;                // patch mode, cached single unit: unit block + per-subsystem row info
   int off_bar;                 // 3 mbarriers (ψ buffers, λ buffer)
   // stream mode, host-built control tables (one coalesced copy per unit):
   //   unit_desc [u][16] ints: own_lo, own_hi, plo, phi, prow0 (2 ints), prows, ch_a, ch_b, pt_off,
@@ -759,9 +760,16 @@ __device__ void column_stage_tiles(const DevProblem& P, int b, const double* x, 
 // constant for a whole MPC step): each iteration's Φ then needs one L2 round
 // trip (the ψ,λ reads) instead of three.
 // layout at off_phimeta: base [np*d_pad] (int64), xk [np*d_pad], ada [np],
-//                        inv_den/lo/hi [3*prows], len [np] (int32 in a double slot)
+//                        inv_den/lo/hi [3*prows], len [np] (int32 in a double slot),
+//                        then at off_ublk: ublk [16 ints], rinfo [np] (int2: local row offset, rows)
 // inv_den = 1/(ρ + 2w·||a||²) and 1/||a||² (in the ada slot) turn the two
-// per-row IEEE divisions of the fast path into multiplications.
+// per-row IEEE divisions of the fast path into multiplications. The unit
+// block holds the unit's ranges and its first chunk; a unit of one chunk
+// also gets that chunk's column metadata (off_meta) once per step, so an
+// iteration's control path touches no global memory.
+// ublk: has_unit, own_lo, own_hi, plo, phi, prows, prow0 (2 ints), ch_a, ch_b,
+//       k, c0, nt, S of the first chunk, own-row offset in the patch, own rows
+template <int TC>
 __device__ void cache_phi_meta(const DevProblem& P, const double* x, double* smem) {
   const int un0 = P.cta_unit_ptr[blockIdx.x];
   if (un0 == P.cta_unit_ptr[blockIdx.x + 1]) return;
@@ -795,6 +803,37 @@ __device__ void cache_phi_meta(const DevProblem& P, const double* x, double* sme
     const double a = ld_cg(P.ada + i);
     rw[q] = 1.0 / (P.rho + 2.0 * P.row_w[prow0 + q] * a);
     rw[prows + q] = P.row_lo[prow0 + q]; rw[2 * prows + q] = P.row_hi[prow0 + q];
+  }
+  int* ublk = reinterpret_cast<int*>(smem + P.off_ublk);
+  int2* rinfo = reinterpret_cast<int2*>(smem + P.off_ublk + 8);
+  for (int q = threadIdx.x; q < np; q += kThreads)
+    rinfo[q] = make_int2(static_cast<int>(P.row_start[plo + q] - prow0),
+                         static_cast<int>(P.row_start[plo + q + 1] - P.row_start[plo + q]));
+  const int own_lo = P.unit_sub_lo[un0], own_hi = P.unit_sub_hi[un0];
+  const int ch_a = P.unit_chunk_ptr[un0], ch_b = P.unit_chunk_ptr[un0 + 1];
+  if (threadIdx.x == 0) {
+    ublk[0] = 1; ublk[1] = own_lo; ublk[2] = own_hi; ublk[3] = plo; ublk[4] = phi_; ublk[5] = prows;
+    ublk[6] = static_cast<int>(prow0 & 0xffffffffLL); ublk[7] = static_cast<int>(prow0 >> 32);
+    ublk[8] = ch_a; ublk[9] = ch_b;
+    const int k = P.chunk_class[ch_a];
+    ublk[10] = k; ublk[11] = P.chunk_col0[ch_a]; ublk[12] = P.chunk_n[ch_a]; ublk[13] = P.class_s[k];
+    ublk[14] = static_cast<int>(P.row_start[own_lo] - prow0);
+    ublk[15] = static_cast<int>(P.row_start[own_hi] - P.row_start[own_lo]);
+  }
+  if (ch_b - ch_a == 1 && threadIdx.x < TC) {   // the single chunk's column metadata
+    long long* m_pos = reinterpret_cast<long long*>(smem + P.off_meta);
+    double* m_x = smem + P.off_meta + 3 * TC;
+    const int t = threadIdx.x, c0 = P.chunk_col0[ch_a], nt = P.chunk_n[ch_a];
+    long long pos = 0, s0 = 0, q0 = 0;
+    double xc = 0.0;
+    if (t < nt) {
+      const int c = c0 + t;
+      pos = static_cast<long long>(c) * P.s_pad;
+      s0 = P.col_rowbase[c] - prow0;
+      q0 = static_cast<long long>(P.col_vec[c]) * P.s_pad;
+      xc = ld_cg(x + c);
+    }
+    m_pos[t] = pos; m_pos[TC + t] = s0; m_pos[2 * TC + t] = q0; m_x[t] = xc;
   }
   __syncthreads();
 }
@@ -871,29 +910,47 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
   if (un_a == P.cta_unit_ptr[blockIdx.x + 1] && !tested && patch_stop_test(P, R, it, rp, rd)) return true;
   for (int un = un_a; un < P.cta_unit_ptr[blockIdx.x + 1]; ++un) {
     PT_START
-    const int own_lo = P.unit_sub_lo[un], own_hi = P.unit_sub_hi[un];
-    const int plo = P.unit_patch_lo[un], phi_ = P.unit_patch_hi[un];
-    const long long prow0 = P.row_start[plo];
-    const int prows = static_cast<int>(P.row_start[phi_] - prow0);
+    int own_lo, own_hi, plo, phi_, prows, ch_a, ch_b, k0 = 0, c00 = 0, nt0 = 0, S0 = 0, o_off, o_n;
+    long long prow0;
+    const int* ublk = nullptr;
+    const int2* rinfo = nullptr;
+    if (P.cache_phi) {   // one unit per CTA: the control data cached at step start
+      ublk = reinterpret_cast<const int*>(smem + P.off_ublk);
+      rinfo = reinterpret_cast<const int2*>(smem + P.off_ublk + 8);
+      own_lo = ublk[1]; own_hi = ublk[2]; plo = ublk[3]; phi_ = ublk[4]; prows = ublk[5];
+      prow0 = static_cast<long long>(static_cast<unsigned>(ublk[6])) | (static_cast<long long>(ublk[7]) << 32);
+      ch_a = ublk[8]; ch_b = ublk[9]; k0 = ublk[10]; c00 = ublk[11]; nt0 = ublk[12]; S0 = ublk[13];
+      o_off = ublk[14]; o_n = ublk[15];
+    } else {
+      own_lo = P.unit_sub_lo[un]; own_hi = P.unit_sub_hi[un];
+      plo = P.unit_patch_lo[un]; phi_ = P.unit_patch_hi[un];
+      prow0 = P.row_start[plo];
+      prows = static_cast<int>(P.row_start[phi_] - prow0);
+      ch_a = P.unit_chunk_ptr[un]; ch_b = P.unit_chunk_ptr[un + 1];
+      if (ch_a < ch_b) {
+        k0 = P.chunk_class[ch_a]; c00 = P.chunk_col0[ch_a]; nt0 = P.chunk_n[ch_a]; S0 = P.class_s[k0];
+      }
+      o_off = static_cast<int>(P.row_start[own_lo] - prow0);
+      o_n = static_cast<int>(P.row_start[own_hi] - P.row_start[own_lo]);
+    }
     // first chunk's ψ,λ start streaming into shared memory under the Φ stage
-    const int ch_a = P.unit_chunk_ptr[un], ch_b = P.unit_chunk_ptr[un + 1];
     double* stash = smem + P.off_stash;
     const int stash_stride = 2 * TC * P.ldk;
-    if (P.stash_bufs > 0 && ch_a < ch_b)
-      stash_issue(P, P.chunk_col0[ch_a], P.chunk_n[ch_a], P.class_s[P.chunk_class[ch_a]], psi, lam, stash);
+    if (P.stash_bufs > 0 && ch_a < ch_b) stash_issue(P, c00, nt0, S0, psi, lam, stash);
     // Φ scale of every row the unit's columns touch (own rows + d-hop halo);
     // before the stop test the own rows' s goes to shared memory only
     for (int i = plo + warp; i < phi_; i += kWarps) {
-      const int r_off = static_cast<int>(P.row_start[i] - prow0);
+      int r_off, nrow;
+      if (rinfo) { const int2 ri = rinfo[i - plo]; r_off = ri.x; nrow = ri.y; }
+      else { r_off = static_cast<int>(P.row_start[i] - prow0); nrow = static_cast<int>(P.row_start[i + 1] - P.row_start[i]); }
       double* dst = s_patch + r_off;
-      double* gdst = (tested && i >= own_lo && i < own_hi) ? P.s_row + P.row_start[i] : nullptr;
+      double* gdst = (tested && i >= own_lo && i < own_hi) ? P.s_row + prow0 + r_off : nullptr;
       auto out = [dst, gdst](int l, double s) {
         dst[l] = s;
         if (gdst) gdst[l] = s;
       };
       if (P.cache_phi)
-        phi_rows_cached(P, i - plo, phi_ - plo, prows, r_off, static_cast<int>(P.row_start[i + 1] - P.row_start[i]),
-                        psi, lam, smem, out);
+        phi_rows_cached(P, i - plo, phi_ - plo, prows, r_off, nrow, psi, lam, smem, out);
       else
         phi_rows_of<false>(P, i, psi, lam, x, out);
     }
@@ -904,15 +961,16 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
         cp_async_wait<0>();
         return true;
       }
-      const long long o0 = P.row_start[own_lo];
-      const int on = static_cast<int>(P.row_start[own_hi] - o0), off0 = static_cast<int>(o0 - prow0);
-      for (int r = threadIdx.x; r < on; r += kThreads) P.s_row[o0 + r] = s_patch[off0 + r];
+      for (int r = threadIdx.x; r < o_n; r += kThreads) P.s_row[prow0 + o_off + r] = s_patch[o_off + r];
     }
     PT_LAP(P, 0)
     // chunk pipeline: ψ,λ of chunk i+1 stream into the other staging buffer
     // (cp.async) while chunk i runs its GEMMs
+    const bool meta_cached = P.cache_phi && ch_b - ch_a == 1;
     for (int ch = ch_a; ch < ch_b; ++ch) {
-      const int k = P.chunk_class[ch], c0 = P.chunk_col0[ch], nt = P.chunk_n[ch];
+      const int k = ch == ch_a ? k0 : P.chunk_class[ch];
+      const int c0 = ch == ch_a ? c00 : P.chunk_col0[ch];
+      const int nt = ch == ch_a ? nt0 : P.chunk_n[ch];
       const int sb = P.stash_bufs == 2 ? ((ch - ch_a) & 1) : 0;
       if (P.stash_bufs == 2 && ch + 1 < ch_b) {
         stash_issue(P, P.chunk_col0[ch + 1], P.chunk_n[ch + 1], P.class_s[P.chunk_class[ch + 1]], psi, lam,
@@ -921,7 +979,7 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
       } else if (P.stash_bufs > 0) {
         cp_async_wait<0>();
       }
-      if (threadIdx.x < TC) {
+      if (!meta_cached && threadIdx.x < TC) {
         const int t = threadIdx.x;
         long long pos = 0, s0 = 0, q0 = 0;
         double xc = 0.0;
@@ -1508,7 +1566,7 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
       }
       if (leader) P.ctl[2 + ((step + 1) & 1)] = kBadNone;
     }
-    if (MODE == kPatch && P.cache_phi) cache_phi_meta(P, x, smem);
+    if (MODE == kPatch && P.cache_phi) cache_phi_meta<TC>(P, x, smem);
     int it = 0;
     bool conv = false;
     if (MODE == kPatch) {
