@@ -955,6 +955,7 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
         phi_rows_of<false>(P, i, psi, lam, x, out);
     }
     __syncthreads();
+    PT_LAP(P, 0)
     if (!tested) {
       tested = true;
       if (patch_stop_test(P, R, it, rp, rd)) {
@@ -963,7 +964,7 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
       }
       for (int r = threadIdx.x; r < o_n; r += kThreads) P.s_row[prow0 + o_off + r] = s_patch[o_off + r];
     }
-    PT_LAP(P, 0)
+    PT_LAP(P, 7)
     // chunk pipeline: ψ,λ of chunk i+1 stream into the other staging buffer
     // (cp.async) while chunk i runs its GEMMs
     const bool meta_cached = P.cache_phi && ch_b - ch_a == 1;

@@ -13,5 +13,5 @@ L = sess.layout
 print("iters", it, "us/iter", 1e3 * ms / it)
 order = np.argsort(-pt[:, 0])
 for c in order[:12]:
-    print(f"cta {c:3d} phi {pt[c,0]:.2f} pro {pt[c,1]:.2f} g1 {pt[c,2]:.2f} g2 {pt[c,3]:.2f} epi {pt[c,4]:.2f} pub {pt[c,5]:.2f} bar {pt[c,6]:.2f}")
+    print(f"cta {c:3d} phi {pt[c,0]:.2f} stoptest {pt[c,7]:.2f} pro {pt[c,1]:.2f} g1 {pt[c,2]:.2f} g2 {pt[c,3]:.2f} epi {pt[c,4]:.2f} pub {pt[c,5]:.2f} bar {pt[c,6]:.2f}")
 print("median phi", np.median(pt[:100, 0]))
