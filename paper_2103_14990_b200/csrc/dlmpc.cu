@@ -514,6 +514,12 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           h->allocs.push_back(ptr);
           P.part_buf[q] = static_cast<double*>(ptr);
         }
+        {
+          void* ptr = nullptr;
+          CUDA_OR_FAIL(h, cudaMalloc(&ptr, sizeof(double) * std::max<long long>(1, P.n_rows)));
+          h->allocs.push_back(ptr);
+          P.row_invden = static_cast<double*>(ptr);
+        }
       }
     }
   }

@@ -102,6 +102,7 @@ struct DevProblem {
   const int64_t* part_off; const int* part_first; const int* part_n;
   double* part_buf[2];
   int off_cpatch;
+  double* row_invden;          // stream mode: 1/(ρ + 2w·||a||²) per row of the current MPC step
   int off_chtab, ch_cap;       // per-unit chunk table: [ch_cap][8] ints (k, c0, nt, S, n08, ldn)
   int off_ptab, np_cap;        // per-unit patch-subsystem table: [np_cap][6] doubles
   int off_rowq;                // per patch row: its patch-subsystem index (int)
@@ -287,7 +288,8 @@ __device__ void row_data_stage(const DevProblem& P, const double* x, int* bad_sl
 // Calls `out(row_local, s)` for every row.
 template <bool EXACT, class Out>
 __device__ __forceinline__ void phi_rows_of(const DevProblem& P, int i, const double* psi,
-                                            const double* lam, const double* x, const Out& out) {
+                                            const double* lam, const double* x, const Out& out,
+                                            double* inv_den_out = nullptr) {
   const int lane = threadIdx.x & 31;
   const int D = P.supp_len[i];
   const int* sc = P.supp_col + static_cast<size_t>(i) * P.d_pad;
@@ -342,7 +344,9 @@ __device__ __forceinline__ void phi_rows_of(const DevProblem& P, int i, const do
     if (!row_ok) continue;
     if (EXACT && D < P.d_row) acc = __dadd_rn(acc, 0.0);
     // y0 = ρc/(ρ + 2w·ada); clip; s = (y - c)/ada   (admm.py:162-166)
-    const double y0 = __ddiv_rn(__dmul_rn(rho, acc), __dadd_rn(rho, __dmul_rn(__dmul_rn(2.0, w), ada)));
+    const double den = __dadd_rn(rho, __dmul_rn(__dmul_rn(2.0, w), ada));
+    if (inv_den_out) inv_den_out[l] = 1.0 / den;   // stream mode: later iterations multiply
+    const double y0 = __ddiv_rn(__dmul_rn(rho, acc), den);
     const double y = fmin(fmax(y0, lo), hi);
     out(l, ada > 0.0 ? __ddiv_rn(__dsub_rn(y, acc), ada) : 0.0);
   }
@@ -1102,6 +1106,7 @@ struct StreamEpi {
     const int lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
     const int p = mt * 8 + g;
     double contrib = 0.0;   // paired chunks: this pair's share of the row's next Φ dot
+    double s_pair = 0.0;    // paired chunks: both columns share the support row's Φ scale
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int t = nn * 8 + 2 * tig + e;
@@ -1109,7 +1114,9 @@ struct StreamEpi {
         const double kv = kt[t * ldk + p], lm = lt[t * ldl + p];
         const double pn = qv[m][nn][e] + (e ? c1 : c0);
         const double ln = __dsub_rn(kv, pn);
-        const double ps = fma(-s_patch[m_s[t] + p], m_x[t], kv);
+        const double sv = (paired && e) ? s_pair : s_patch[m_s[t] + p];
+        s_pair = sv;
+        const double ps = fma(-sv, m_x[t], kv);
         const long long pos = m_pos[t] + p;
         psi_n[pos] = pn;
         lam_n[pos] = ln;
@@ -1202,7 +1209,10 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       const double2* ps = reinterpret_cast<const double2*>(P.unit_ptab + static_cast<size_t>(pt_off) * 6);
       double2* pd = reinterpret_cast<double2*>(ptab);
       for (int q = tid; q < npq * 3; q += kThreads) pd[q] = __ldg(ps + q);
-      for (int q = tid; q < npq; q += kThreads) pada[q] = ld_cg(P.ada + plo + q);
+      for (int q = tid; q < npq; q += kThreads) {
+        const double a = ld_cg(P.ada + plo + q);
+        pada[q] = a > 0.0 ? 1.0 / a : 0.0;   // only read in iterations >= 1 (reciprocal form)
+      }
     }
     __syncthreads();
     PT_LAP(P, 2)
@@ -1226,7 +1236,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
           dst[l] = s;
           if (gdst) gdst[l] = s;
         };
-        phi_rows_of<false>(P, i, psi, lam, x, out);
+        phi_rows_of<false>(P, i, psi, lam, x, out,
+                           (i >= own_lo && i < own_hi) ? P.row_invden + P.row_start[i] : nullptr);
       }
     } else {
       // from the per-unit dot partials of the last iteration (slot order);
@@ -1251,7 +1262,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
             own[u] = ei[10] != 0;
             ada[u] = pada[q];
             const double* pb = part_in + reinterpret_cast<const long long*>(e)[2] + l;
-            w[u] = __ldg(P.row_w + grow[u]); lo[u] = __ldg(P.row_lo + grow[u]); hi[u] = __ldg(P.row_hi + grow[u]);
+            w[u] = __ldcg(P.row_invden + grow[u]); lo[u] = __ldg(P.row_lo + grow[u]); hi[u] = __ldg(P.row_hi + grow[u]);
             c[u] = __ldcg(pb);
             for (int sl = 1; sl < np; ++sl) c[u] += __ldcg(pb + sl * nr);
           }
@@ -1259,9 +1270,9 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
 #pragma unroll
         for (int u = 0; u < kRB; ++u) {
           if (!ok[u]) continue;
-          const double y0 = __ddiv_rn(__dmul_rn(rho, c[u]), __dadd_rn(rho, __dmul_rn(__dmul_rn(2.0, w[u]), ada[u])));
-          const double y = fmin(fmax(y0, lo[u]), hi[u]);
-          const double sv = ada[u] > 0.0 ? __ddiv_rn(__dsub_rn(y, c[u]), ada[u]) : 0.0;
+          // w[] holds 1/(ρ + 2w·ada) (first iteration of the step), ada[] 1/ada
+          const double y = fmin(fmax(rho * c[u] * w[u], lo[u]), hi[u]);
+          const double sv = (y - c[u]) * ada[u];
           s_patch[r0 + u * kThreads] = sv;
           if (own[u]) P.s_row[grow[u]] = sv;
         }
