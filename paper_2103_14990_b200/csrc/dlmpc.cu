@@ -177,7 +177,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
     std::vector<int> cta_ptr(G + 1, 0), u_lo, u_hi, p_lo, p_hi, u_chunk(1, 0), ch_cls, ch_c0, ch_n;
     std::vector<int> part_first, part_n;
     std::vector<int64_t> part_off;
-    std::vector<int> st_unit_desc, st_chunk_desc;
+    std::vector<int> st_unit_desc, st_chunk_desc, st_cta_gop;
     std::vector<double> st_ptab;
     long long part_total = 0;
     long long prows_max = 0, np_max = 0;
@@ -289,10 +289,19 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         const bool bulk = P.s_pad % 16 == 4 || P.s_pad % 16 == 12;   // stream mode requires it
         const int ldk = bulk ? P.s_pad : ld_frag(s8_max), ldy = ld_frag(tc);
         const int sp_max = 1;   // GEMM 1 tile-parallel for every class (no partials buffer)
-        // operator region: every class's basis resident in shared memory
-        // (measured: reading a rare class's basis from L2 makes its CTAs the
-        // stragglers, N=3000: 31.2 vs 29.3 us/iter)
-        const long long opr_main = opr_need;
+        // operator region sized for the classes carrying >= 5% of the columns;
+        // CTAs holding a larger (rare, chain-end) class read it from L2 in a
+        // separate kernel instantiation (their work is a chunk or two)
+        long long opr_main = 0;
+        {
+          std::vector<long long> cnt(pr->n_classes, 0);
+          for (int c = 0; c < P.n_cols; ++c) cnt[pr->col_class[c]]++;
+          for (int k = 0; k < pr->n_classes; ++k)
+            if (cnt[k] * 20 >= P.n_cols)
+              opr_main = std::max<long long>(opr_main, (long long)((pr->class_s[k] + 7) & ~7) * pr->class_ldn[k]);
+          const char* e = getenv("DLMPC_OPR_ALL");
+          if (opr_main == 0 || (e && e[0] == '1')) opr_main = opr_need;
+        }
         // λ stash stride: 2*ldl % 16 in {4, 12} keeps the register epilogue conflict free
         int ldl = P.s_pad;
         while ((2 * ldl) % 16 != 4 && (2 * ldl) % 16 != 12) ldl += 2;
@@ -407,6 +416,18 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
             P.off_udesc = (int)off; off += 16;
             P.off_bar = (int)off; off += 4;
             P.bulk_copy = bulk ? 1 : 0;
+            // CTAs with a class operator larger than the region
+            st_cta_gop.assign(G, 0);
+            bool any_gop = false;
+            for (int q = 0; q < G; ++q)
+              for (int u = cta_ptr[q]; u < cta_ptr[q + 1]; ++u)
+                for (int ch = u_chunk[u]; ch < u_chunk[u + 1]; ++ch) {
+                  const int k = ch_cls[ch];
+                  if ((long long)((pr->class_s[k] + 7) & ~7) * pr->class_ldn[k] > opr_main) {
+                    st_cta_gop[q] = 1; any_gop = true;
+                  }
+                }
+            if (!any_gop) st_cta_gop.clear();
             P.cache_phi = 0; P.stash_bufs = 0; P.off_stash = (int)off; P.off_phimeta = (int)off;
             P.off_ex = (int)off;
             h->smem_bytes = (int)(off * 8);
@@ -501,7 +522,8 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           (rc = upload(h, ch_n.data(), ch_n.size(), &P.chunk_n)))
         return rc;
       if (h->mode == kStream) {
-        if ((rc = upload(h, st_unit_desc.data(), st_unit_desc.size(), &P.unit_desc)) ||
+        if ((rc = upload(h, st_cta_gop.data(), st_cta_gop.size(), &P.cta_gop)) ||
+            (rc = upload(h, st_unit_desc.data(), st_unit_desc.size(), &P.unit_desc)) ||
             (rc = upload(h, st_chunk_desc.data(), st_chunk_desc.size(), &P.chunk_desc)) ||
             (rc = upload(h, st_ptab.data(), st_ptab.size(), &P.unit_ptab)) ||
             (rc = upload(h, part_first.data(), part_first.size(), &P.part_first)) ||

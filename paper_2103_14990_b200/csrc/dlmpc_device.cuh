@@ -103,6 +103,7 @@ struct DevProblem {
   double* part_buf[2];
   int off_cpatch;
   double* row_invden;          // stream mode: 1/(ρ + 2w·||a||²) per row of the current MPC step
+  const int* cta_gop;          // stream mode: CTA reads its class operator from L2 (does not fit)
   int off_chtab, ch_cap;       // per-unit chunk table: [ch_cap][8] ints (k, c0, nt, S, n08, ldn)
   int off_ptab, np_cap;        // per-unit patch-subsystem table: [np_cap][6] doubles
   int off_rowq;                // per patch row: its patch-subsystem index (int)
@@ -1144,7 +1145,12 @@ struct LamWait {
   }
 };
 
-template <int TC>
+// OPS: class operators staged in shared memory (LDS fragments). CTAs holding
+// a class whose basis does not fit the region (the host flags them; on chains
+// only the few chain-end CTAs, which carry a chunk or two) run the OPS=false
+// instantiation and read the basis from L2 -- a separate instantiation, so
+// the common path keeps shared-memory fragment loads.
+template <int TC, bool OPS>
 __device__ void stream_iteration(const DevProblem& P, int b, const double* x, int it, double* smem, int& cur,
                                  unsigned (&ph)[3]) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1302,7 +1308,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       }
     };
     if (nch > 0) {   // first chunk: operator, ψ landed, K
-      stage_operator_sized(P, chtab[0], (chtab[3] + 7) & ~7, chtab[5], smem, cur);
+      if (OPS) stage_operator_sized(P, chtab[0], (chtab[3] + 7) & ~7, chtab[5], smem, cur);
       mbar_wait(bars + 0, ph[0]);
       ph[0] ^= 1u;
       k_pass(psi_st, meta0 + TC, reinterpret_cast<const double*>(meta0 + 3 * TC), chtab[3], chtab[2]);
@@ -1364,10 +1370,11 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
                    ce[CHW + 3], ce[CHW + 2], kCons, kProd);
           }
         } else {
-          gemm1<TC, NoHook, kCons, GroupBar<kCons>>(P, S4, n08, ldn, smem, kt, ldk, yb, P.ldy, yp);
+          const double* nop = OPS ? smem : P.null_pool + P.class_null_off[ce[0]];
+          gemm1<TC, NoHook, kCons, GroupBar<kCons>>(P, S4, n08, ldn, nop, kt, ldk, yb, P.ldy, yp);
           StreamEpi<TC> epi{P.psi[b ^ 1], P.lam[b ^ 1], P.q_pool, m_pos, m_s, m_q, m_x,
                             s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, bars + 2, ph[2], ce[6] != 0};
-          gemm2<TC, StreamEpi<TC>, kCons>(S8, n08, ldn, smem, yb, P.ldy, epi);
+          gemm2<TC, StreamEpi<TC>, kCons>(S8, n08, ldn, nop, yb, P.ldy, epi);
           pri_m = epi.pri_m; dual_m = epi.dual_m;
         }
         ph[2] ^= 1u;
@@ -1394,7 +1401,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       const int nt = ce[2], S = ce[3], S8 = (S + 7) & ~7, S4 = (S + 3) & ~3, n08 = ce[4], ldn = ce[5];
       double xn = 0.0;   // x of the next chunk's columns (meta written after GEMM 1)
       if (has_next && tid < ce[CHW + 2]) xn = ld_cg(x + ce[CHW + 1] + tid);
-      gemm1<TC>(P, S4, n08, ldn, smem, kt, ldk, yb, P.ldy, yp, LamWait{bars + 2, ph[2], true, has_next});
+      const double* nop = OPS ? smem : P.null_pool + P.class_null_off[ce[0]];
+      gemm1<TC>(P, S4, n08, ldn, nop, kt, ldk, yb, P.ldy, yp, LamWait{bars + 2, ph[2], true, has_next});
       ph[2] ^= 1u;
       if (has_next && tid < TC) {
         long long* mm = meta0 + (mb ^ 1) * 4 * TC;
@@ -1407,7 +1415,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       PT_LAP(P, 2)
       StreamEpi<TC> epi{P.psi[b ^ 1], P.lam[b ^ 1], P.q_pool, m_pos, m_s, m_q, m_x,
                         s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, nullptr, 0u, ce[6] != 0};
-      gemm2<TC>(S8, n08, ldn, smem, yb, P.ldy, epi);
+      gemm2<TC>(S8, n08, ldn, nop, yb, P.ldy, epi);
       pri_m = epi.pri_m; dual_m = epi.dual_m;
       __syncthreads();
       PT_LAP(P, 3)
@@ -1416,7 +1424,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       row_pass(m_s, m_x, S, nt, tid, kThreads, ce[6] != 0);
       if (has_next) {   // next chunk: operator, ψ landed, K
         const long long* mn = meta0 + (mb ^ 1) * 4 * TC;
-        stage_operator_sized(P, ce[CHW], (ce[CHW + 3] + 7) & ~7, ce[CHW + 5], smem, cur);
+        if (OPS) stage_operator_sized(P, ce[CHW], (ce[CHW + 3] + 7) & ~7, ce[CHW + 5], smem, cur);
         mbar_wait(bars + (mb ^ 1), ph[mb ^ 1]);
         ph[mb ^ 1] ^= 1u;
         k_pass(psi_st + (mb ^ 1) * TC * ldk, mn + TC, reinterpret_cast<const double*>(mn + 3 * TC),
@@ -1603,7 +1611,8 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
     while (MODE != kPatch && it < R.max_iters) {
       PT_DECL
       if (MODE == kStream) {
-        stream_iteration<TC>(P, b, x, it, smem, cur, ph);
+        if (P.cta_gop && P.cta_gop[blockIdx.x]) stream_iteration<TC, false>(P, b, x, it, smem, cur, ph);
+        else stream_iteration<TC, true>(P, b, x, it, smem, cur, ph);
         PT_START
       } else {
         PT_START
