@@ -189,6 +189,16 @@ def sweep(pb, hbm_peak, cpu_seconds=6.0):
                  "fp64_tflops": flops_it / s_it / 1e12, "fp64_frac": flops_it / s_it / 1e12 / FP64_DMMA_PEAK_TFLOPS,
                  "hbm_gbs": bytes_it / s_it / 1e9, "hbm_frac": bytes_it / s_it / 1e9 / hbm_peak,
                  "flops_per_iteration": flops_it, "bytes_per_iteration": bytes_it}
+        summ = os.path.join(ROOT, "profiles", f"ncu_stream_n1e{len(str(n)) - 1}_summary.json")
+        if os.path.exists(summ):   # ncu evidence for this size (one capture, committed)
+            try:
+                with open(summ) as fh:
+                    d = json.load(fh)
+                its = d.get("admm_iterations_in_launch") or 1
+                entry["traffic_per_iteration"] = d["dram_bytes_per_launch"] / its
+                entry["traffic_source"] = os.path.relpath(summ, ROOT)
+            except (OSError, ValueError, KeyError):
+                pass
         if n == 1000 and cpu_seconds > 0:
             from oracle import admm_ref
             tables = pb.LayoutTables(mask)
