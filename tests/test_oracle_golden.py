@@ -132,3 +132,38 @@ def test_kkt_oracle_restatement_matches_reference(n, t, d):
     states, inputs = kkt.kkt_closed_loop(system, spec, mask, g[f"n{n}_t{t}_d{d}_x0"], 8)
     np.testing.assert_allclose(states, g[f"n{n}_t{t}_d{d}_states"], rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(inputs, g[f"n{n}_t{t}_d{d}_inputs"], rtol=1e-9, atol=1e-12)
+
+
+def test_oracle_phi_rows_match_independent_minimiser():
+    """The oracle's closed-form Φ row solve against scipy's bounded scalar
+    minimiser (the reference's own independent check, test_admm.py:53-87):
+    for y = φ·a the row objective is w·y² + (ρ/2)(y - c)²/‖a‖² on [lo, hi],
+    and φ = v + (y - c)/‖a‖² · a."""
+    from scipy.optimize import minimize_scalar
+    g = golden("c1_step0")
+    b = chain_bundle(10, 5, 2)
+    s = admm_ref.OracleSolver(b["tables"], b["col_solvers"], b["spec"].rho)
+    w, lo, hi = b["spec"].row_arrays()
+    s.row_data, _ = admm_ref.row_data_for(g["x0"], b["tables"], w, lo, hi)
+    for _ in range(3):
+        s.iterate()
+    v = s.psi_r - s.lam_r
+    n = v.shape[0]
+    s._phi(0, n)
+    rd, rho = s.row_data, b["spec"].rho
+    checked = 0
+    for r in range(n):
+        a, ada = rd.a_pad[r], rd.a_dot_a[r]
+        if ada == 0.0:
+            assert np.array_equal(s.phi_r[r], v[r])
+            continue
+        c = float(v[r] @ a)
+        wr, l_, h_ = rd.weight[r], rd.lo[r], rd.hi[r]
+        f = lambda y: wr * y * y + 0.5 * rho * (y - c) ** 2 / ada
+        span = 10.0 * (abs(c) + 1.0)
+        res = minimize_scalar(f, bounds=(max(l_, c - span), min(h_, c + span)), method="bounded",
+                              options={"xatol": 1e-13})
+        phi = v[r] + (res.x - c) / ada * a
+        np.testing.assert_allclose(s.phi_r[r], phi, rtol=1e-6, atol=1e-7)   # Brent's accuracy
+        checked += 1
+    assert checked > 50
