@@ -415,7 +415,6 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
             off = (off + 1) & ~1LL;
             P.off_udesc = (int)off; off += 16;
             P.off_bar = (int)off; off += 4;
-            P.bulk_copy = bulk ? 1 : 0;
             // CTAs with a class operator larger than the region
             st_cta_gop.assign(G, 0);
             bool any_gop = false;

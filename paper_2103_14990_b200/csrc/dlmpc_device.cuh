@@ -1,24 +1,26 @@
 // dlmpc_device.cuh -- device code of the DLMPC ADMM hot path (sm_100a).
 //
-// Three persistent cooperative kernels, one launch per solve / closed loop:
+// One persistent cooperative kernel, dlmpc_persistent<TC, MODE>, runs a whole
+// solve or a whole closed loop (one launch); MODE selects the schedule:
 //
-//  dlmpc_patch<TC>     fast path for layouts whose d-hop balls are contiguous
-//                      subsystem-id ranges (chains, banded graphs). Each CTA
-//                      owns contiguous work units of subsystems. Per ADMM
-//                      iteration and unit it (1) recomputes the Φ scale s_r of
-//                      every row its columns touch -- own rows plus a d-hop
-//                      halo -- into shared memory (the paper's column patch,
-//                      §III-D; reference admm.py:155-170, 227-253), (2) runs
-//                      the Ψ projection of its columns as two FP64 tensor-core
-//                      GEMMs against the class null-space basis staged in
-//                      shared memory once per launch, then the Λ update and
-//                      the residual maxima (admm.py:174-217), writing (ψ',λ')
-//                      to the other ping-pong buffer. ONE grid barrier per
-//                      iteration, which also publishes the global (pri, dual).
-//  dlmpc_twophase<TC>  fast path for arbitrary graphs: a grid-wide Φ stage
-//                      writes s_r to global memory, barrier, column stage.
-//  dlmpc_exact         the reference's arithmetic bit for bit (dense
-//                      projector, numpy pairwise sums, no FMA), two-phase.
+//  kPatch     fast path, d-hop balls contiguous in subsystem ids (chains,
+//             banded graphs), small/medium networks. Each CTA owns contiguous
+//             units of subsystems; per ADMM iteration and unit it recomputes
+//             the Φ scale s_r of every row its columns touch -- own rows plus a
+//             d-hop halo (the paper's column patch, §III-D; reference
+//             admm.py:155-170, 227-253) -- then runs the Ψ projection of its
+//             columns as two FP64 tensor-core GEMMs against the class
+//             null-space basis staged in shared memory, the Λ update and the
+//             residual maxima (admm.py:174-217). ONE grid barrier per
+//             iteration, which also publishes the global (pri, dual).
+//  kStream    the same algorithm restructured for large networks (>= 2 chunks
+//             per CTA): Φ dots of the next iteration accumulated by the Ψ
+//             epilogues (per-unit slots, deterministic), ψ/λ staged by TMA
+//             bulk copies, register epilogue, hybrid warp split.
+//  kTwoPhase  fast path for arbitrary graphs: a grid-wide Φ stage writes s_r
+//             to global memory, barrier, class-sorted column tiles.
+//  kExact     the reference's arithmetic bit for bit (dense projector, numpy
+//             pairwise sums, no FMA), two-phase.
 //
 // φ is never stored: φ(r,c) = (ψ-λ)(r,c) + s_r·x_c is rebuilt where needed.
 #pragma once
@@ -118,7 +120,6 @@ struct DevProblem {
   //     s0 (row of support slot 0, unit-local) and q (particular-solution vector index)
   //   unit_ptab [pt_off + q][6] doubles: (rowoff, rows, slots, own slot) ints | part_off | - | r0 | (own, -)
   const int* unit_desc; const int* chunk_desc; const double* unit_ptab;
-  int bulk_copy;               // stream staging by TMA bulk copies (1) or cp.async (0)
   int ldl;                     // stream mode: row stride of the λ stash
   int warp_spec;               // stream mode: producer/consumer warp specialisation
   int small_gemv;              // patch mode: DFMA GEMV for GEMM 1 of chunks with <= 2 columns
@@ -1062,19 +1063,6 @@ __device__ __forceinline__ void stash_lam_bulk(const DevProblem& P, int c0, int 
   }
 }
 
-// Same with 16-byte cp.async copies from every thread (one commit group).
-__device__ __forceinline__ void stash_cols_issue(const DevProblem& P, int c0, int nt, const double* src,
-                                                 double* st) {
-  const int pairs = P.s_pad >> 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int t = warp; t < nt; t += kWarps) {
-    const double* g = src + static_cast<size_t>(c0 + t) * P.s_pad;
-    double* d = st + t * P.ldk;
-    for (int pr = lane; pr < pairs; pr += 32) cp_async16(d + 2 * pr, g + 2 * pr);
-  }
-  cp_async_commit();
-}
-
 // GEMM-2 epilogue of the stream kernel, all operands in shared memory:
 // kt holds K = φ + λ, lt holds λ (then receives v' = ψ' - λ').
 //   ψ' = q + O;  λ' = λ + (φ - ψ') = K - ψ';  pri: |λ' - λ| = |φ - ψ'|;
@@ -1134,15 +1122,10 @@ struct StreamEpi {
   }
 };
 
-// λ(ch) must have landed before GEMM 1's closing barrier: mbarrier phase
-// (bulk copies) or cp.async groups (allowing the younger ψ(ch+1) group).
+// λ(ch) must have landed before GEMM 1's closing barrier (mbarrier phase).
 struct LamWait {
-  unsigned long long* bar; unsigned phase; bool bulk, has_next;
-  __device__ __forceinline__ void operator()() const {
-    if (bulk) mbar_wait(bar, phase);
-    else if (has_next) cp_async_wait<1>();
-    else cp_async_wait<0>();
-  }
+  unsigned long long* bar; unsigned phase;
+  __device__ __forceinline__ void operator()() const { mbar_wait(bar, phase); }
 };
 
 // OPS: class operators staged in shared memory (LDS fragments). CTAs holding
@@ -1402,7 +1385,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       double xn = 0.0;   // x of the next chunk's columns (meta written after GEMM 1)
       if (has_next && tid < ce[CHW + 2]) xn = ld_cg(x + ce[CHW + 1] + tid);
       const double* nop = OPS ? smem : P.null_pool + P.class_null_off[ce[0]];
-      gemm1<TC>(P, S4, n08, ldn, nop, kt, ldk, yb, P.ldy, yp, LamWait{bars + 2, ph[2], true, has_next});
+      gemm1<TC>(P, S4, n08, ldn, nop, kt, ldk, yb, P.ldy, yp, LamWait{bars + 2, ph[2]});
       ph[2] ^= 1u;
       if (has_next && tid < TC) {
         long long* mm = meta0 + (mb ^ 1) * 4 * TC;

@@ -258,14 +258,22 @@ def test_stream_and_patch_kernels_agree(n, t_sim):
         b = pb.DlmpcSession(system, spec, mask, FAST)
     finally:
         os.environ.pop("DLMPC_NO_STREAM")
+    os.environ.update(DLMPC_FORCE_STREAM="1", DLMPC_WARP_SPEC="0")
+    try:
+        c = pb.DlmpcSession(system, spec, mask, FAST)   # lockstep chunk loop (no warp split)
+    finally:
+        os.environ.pop("DLMPC_FORCE_STREAM"); os.environ.pop("DLMPC_WARP_SPEC")
     assert a.device.info()["mode"] == "stream" and b.device.info()["mode"] == "patch"
     ta, _ = a.simulate(x0, t_sim)
     ta2, _ = a.simulate(x0, t_sim)
     tb, _ = b.simulate(x0, t_sim)
+    tc, _ = c.simulate(x0, t_sim)
     assert ta.step_iterations == tb.step_iterations
     assert rel_err(ta.states, tb.states) <= 1e-12
     assert np.array_equal(ta.states, ta2.states) and np.array_equal(ta.inputs, ta2.inputs)
-    a.close(); b.close()
+    # the warp split changes who computes, not what: bit for bit
+    assert np.array_equal(ta.states, tc.states) and np.array_equal(ta.inputs, tc.inputs)
+    a.close(); b.close(); c.close()
 
 
 @pytest.mark.slow
