@@ -280,6 +280,53 @@ def simulate_partitioned_inprocess(system, spec, mask, x0, t_sim, world, strateg
             rk.close()
 
 
+class DistExchange:
+    """The per-iteration collectives of one rank over torch.distributed:
+    all-reduce(max) of the (pri, dual) maxima and one point-to-point message
+    per neighbour rank (NCCL `batch_isend_irecv`; gloo works for host tests)."""
+
+    def __init__(self, rk: "RankSolver", group=None):
+        import torch
+        import torch.distributed as dist
+        self.dist, self.group, self.rk = dist, group, rk
+        self.nccl = dist.get_backend(group) == "nccl"
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if self.nccl else torch.device("cpu")
+        self.sbuf = torch.zeros(max(1, rk.send_doubles), dtype=torch.float64, device=self.dev)
+        self.rbuf = torch.zeros(max(1, rk.recv_doubles), dtype=torch.float64, device=self.dev)
+
+    def iteration(self):
+        """One partitioned ADMM iteration -> global (pri, dual)."""
+        import torch
+        dist, rk, group = self.dist, self.rk, self.group
+        loc = torch.tensor(rk.iterate(), dtype=torch.float64, device=self.dev)
+        dist.all_reduce(loc, op=dist.ReduceOp.MAX, group=group)
+        rk.pack(self.sbuf.data_ptr())
+        ops = [dist.P2POp(dist.isend, self.sbuf[rk.send_off[k]:rk.send_off[k + 1]], q, group)
+               for k, q in enumerate(rk.send_to)]
+        ops += [dist.P2POp(dist.irecv, self.rbuf[rk.recv_off[k]:rk.recv_off[k + 1]], q, group)
+                for k, q in enumerate(rk.recv_from)]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        if self.nccl:
+            torch.cuda.current_stream().synchronize()
+        rk.unpack(self.rbuf.data_ptr())
+        pri, dual = (float(v) for v in loc.cpu())
+        return pri, dual
+
+    def solve_step(self, x, cold, spec):
+        """One MPC step's ADMM solve -> residual history; NotConverged on failure."""
+        from .errors import NotConverged
+        self.rk.start_step(x, cold)
+        hist = []
+        for _ in range(spec.max_iters):
+            pri, dual = self.iteration()
+            hist.append((pri, dual))
+            if pri <= spec.eps_pri and dual <= spec.eps_dual:
+                return hist
+        raise NotConverged(hist)
+
+
 def simulate_partitioned(system, spec, mask, x0, t_sim, strategy="b200", warm_start=True, group=None):
     """The partitioned closed loop over torch.distributed ranks (one GPU per
     rank; NCCL over NVLink): per iteration an all-reduce(max) of the two
@@ -290,39 +337,19 @@ def simulate_partitioned(system, spec, mask, x0, t_sim, strategy="b200", warm_st
     import torch.distributed as dist
     from .errors import NotConverged
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    nccl = dist.get_backend(group) == "nccl"
-    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
     plans = plan_partition(mask, world)
     rk = RankSolver(system, spec, mask, plans, rank, strategy,
                     torch.cuda.current_device() if torch.cuda.is_available() else 0)
     try:
-        sbuf = torch.zeros(max(1, rk.send_doubles), dtype=torch.float64, device=dev)
-        rbuf = torch.zeros(max(1, rk.recv_doubles), dtype=torch.float64, device=dev)
+        ex = DistExchange(rk, group)
+        dev = ex.dev
         x = np.asarray(x0, dtype=np.float64)
         states, inputs, iters = [x], [], []
         for step in range(t_sim):
-            rk.start_step(x, cold=(step == 0 or not warm_start))
-            hist = []
-            for _ in range(spec.max_iters):
-                loc = torch.tensor(rk.iterate(), dtype=torch.float64, device=dev)
-                dist.all_reduce(loc, op=dist.ReduceOp.MAX, group=group)
-                rk.pack(sbuf.data_ptr())
-                ops = [dist.P2POp(dist.isend, sbuf[rk.send_off[k]:rk.send_off[k + 1]], q, group)
-                       for k, q in enumerate(rk.send_to)]
-                ops += [dist.P2POp(dist.irecv, rbuf[rk.recv_off[k]:rk.recv_off[k + 1]], q, group)
-                        for k, q in enumerate(rk.recv_from)]
-                if ops:
-                    for w in dist.batch_isend_irecv(ops):
-                        w.wait()
-                if nccl:
-                    torch.cuda.current_stream().synchronize()
-                rk.unpack(rbuf.data_ptr())
-                pri, dual = (float(v) for v in loc.cpu())
-                hist.append((pri, dual))
-                if pri <= spec.eps_pri and dual <= spec.eps_dual:
-                    break
-            else:
-                raise NotConverged(hist, step=step)
+            try:
+                hist = ex.solve_step(x, cold=(step == 0 or not warm_start), spec=spec)
+            except NotConverged as err:
+                raise NotConverged(err.residual_history, step=step) from None
             iid, uu, sid, xx = rk.finish_step()
             u = torch.zeros(system.n_inputs, dtype=torch.float64, device=dev)
             xn = torch.zeros(system.n_states, dtype=torch.float64, device=dev)

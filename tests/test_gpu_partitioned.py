@@ -101,3 +101,53 @@ def test_distributed_driver_single_rank_nccl():
         assert np.array_equal(states, g["states"])
     finally:
         dist.destroy_process_group()
+
+
+def _dist_worker(rank, world, port, name, variant, out_q):
+    """One torch.distributed rank (gloo) of the partitioned closed loop; all
+    ranks share cuda:0, their kernels never wait on one another (the
+    exchange is host-driven), so this checks the driver's choreography --
+    all-reduce, batch_isend_irecv halo messages, the step gathers."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        g = golden(name)
+        system, spec, mask, t_sim = loop_problem(g)
+        states, inputs, iters = simulate_partitioned(system, spec, mask, g["x0"], t_sim, variant)
+        out_q.put((rank, states, inputs, iters))
+    except Exception as exc:   # surfaced by the parent
+        out_q.put((rank, repr(exc), None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world", [("c1_loop_seed1", 2), ("c2_loop_seed1", 3)])
+def test_distributed_driver_gloo_multi_process(name, world):
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dist_worker, args=(r, world, port, name, EXACT, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        res = [q.get(timeout=300) for _ in range(world)]
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    g = golden(name)
+    for rank, states, inputs, iters in res:
+        assert not isinstance(states, str), states
+        assert iters == list(g["step_iters"]), rank
+        assert np.array_equal(states, g["states"]), rank
+        assert np.array_equal(inputs, g["inputs"]), rank
