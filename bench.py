@@ -222,6 +222,66 @@ def sweep(pb, hbm_peak, cpu_seconds=6.0):
     return out
 
 
+C5_N = 1000000
+
+
+def partitioned_c5(pb, dist, local, solves=2):
+    """SURVEY §8(e) C5 on all ranks: the chain N=10^6, d=3, T=10 step-0 solve,
+    graph-partitioned across the world (each rank: own subsystem range + 2d
+    halo; per iteration an all-reduce(max) of the residuals and one NCCL
+    message per neighbour). Strong scaling (total work fixed). Timed with
+    CUDA events on each rank's library stream around whole solves, max over
+    ranks; the single-GPU number is the sweep's N=10^6 point."""
+    import torch
+    from paper_2103_14990_b200.partition import DistExchange, RankSolver, halo_bytes_per_iteration, plan_partition
+    rank, world = dist.get_rank(), dist.get_world_size()
+    t0 = time.perf_counter()
+    rk, err = None, None
+    try:
+        system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=C5_N, d=D, horizon=T, t_sim=1, seed=1))
+        plans = plan_partition(mask, world)
+        rk = RankSolver(system, spec, mask, plans, rank, "b200", local)
+    except Exception as exc:
+        err = repr(exc)[:300]
+    setup_s = time.perf_counter() - t0
+    # no rank enters the per-iteration collectives unless every rank is set up
+    ok = torch.tensor([0.0 if err else 1.0], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if ok.item() < 1.0:
+        if rk is not None:
+            rk.close()
+        return {"error": err or "setup failed on another rank"}
+    try:
+        ex = DistExchange(rk)
+        ext = torch.cuda.ExternalStream(rk.session.stream, device=f"cuda:{local}")
+        ex.solve_step(x0, True, spec)                       # warm-up solve
+        dist.barrier()
+        torch.cuda.synchronize()
+        ms, its = 0.0, 0
+        for _ in range(solves):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            hist = ex.solve_step(x0, True, spec)
+            e1.record(ext)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+            its += len(hist)
+        # every rank runs the same (global) iterations: max over ranks for all three
+        t = torch.tensor([its, ms, setup_s], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        its_m, ms_m, setup_m = (float(v) for v in t.cpu())
+        hb = max(halo_bytes_per_iteration(plans, mask, rk.layout.s_pad))
+        return {"workload": "chain N=1e6 d=3 T=10 step-0 solve (C5), graph-partitioned, cold start",
+                "n_gpus": world, "scaling": "strong",
+                "value": C5_N * its_m / (ms_m * 1e-3), "unit": UNIT,
+                "ms_per_iteration": ms_m / its_m, "iterations_per_solve": its_m / solves,
+                "solves_timed": solves, "per_rank_kernel": rk.session.info()["mode"],
+                "halo_bytes_per_iteration_max_rank": hb, "setup_s_max_rank": setup_m,
+                "timing": "CUDA events on each rank's stream around whole solves, max over ranks"}
+    finally:
+        rk.close()
+
+
 def run_reference_arm(args):
     """`--impl reference`: the reference's CPU path (oracle port) on the host."""
     rank, world, _ = dist_env()
@@ -327,6 +387,19 @@ def run_device_arm(args):
     vals = np.array([timed_iters, total_ms, e2e_iters, e2e_s * 1e3], dtype=np.float64)
     if world > 1:
         vals = reduce_over_ranks(vals, dist, device=f"cuda:{local}")
+    part = None
+    force_part = os.environ.get("DLMPC_BENCH_PARTITIONED") == "1"   # exercise at world size 1
+    if (world > 1 or force_part) and not args.no_partitioned:
+        if world == 1:
+            import torch.distributed as dist
+            if not dist.is_initialized():
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29533")
+                dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+        try:
+            part = partitioned_c5(pb, dist, local)
+        except Exception as exc:   # reported, never fatal for the replica line
+            part = {"error": repr(exc)[:300]}
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -383,6 +456,8 @@ def run_device_arm(args):
     if not args.no_sweep and world == 1:
         sess.close()
         line["sweep"] = sweep(pb, hbm_peak, 0.0 if args.no_cpu else 6.0)
+    if part is not None:
+        line["partitioned"] = part
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -396,6 +471,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-sweep", action="store_true", help="skip the N=1e3..1e6 step-0 sweep")
+    ap.add_argument("--no-partitioned", action="store_true",
+                    help="N>1: skip the graph-partitioned C5 (N=1e6) measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -35,6 +35,7 @@ struct dlmpc_handle {
   double* d_scratch2 = nullptr;
   double* d_audit = nullptr;
   int mode = kPatch, n_units = 0;
+  int it_cont = 0;   // iterations run on the current state (reset by any state change)
   int64_t* d_send_cells = nullptr; int64_t n_send = 0;
   int64_t* d_recv_cells = nullptr; int64_t n_recv = 0;
   double* d_halo = nullptr;
@@ -669,6 +670,7 @@ void dlmpc_destroy(dlmpc_handle* h) {
 }
 
 int dlmpc_set_x(dlmpc_handle* h, const double* x, int64_t* bad_row) {
+  if (h) h->it_cont = 0;
   if (!h || !x) return fail(h, DLMPC_BAD_ARGUMENT, "null argument");
   cudaSetDevice(h->device);
   CUDA_OR_FAIL(h, cudaMemcpyAsync(h->P.x[0], x, sizeof(double) * h->P.n_cols, cudaMemcpyHostToDevice, h->stream));
@@ -690,6 +692,7 @@ static int run_iterations(dlmpc_handle* h, int max_iters, double eps_pri, double
   R.t_sim = 1; R.closed_loop = 0; R.warm_start = 1; R.cold_start = 0;
   R.max_iters = max_iters; R.stop_on_conv = stop; R.eps_pri = eps_pri; R.eps_dual = eps_dual;
   R.hist = h->d_hist; R.step_iters = h->d_step_iters; R.states = h->d_states; R.inputs = h->d_inputs;
+  R.it_base = h->it_cont;
   if (int rc = launch(h, R)) return rc;
   if (int rc = finish_timing(h)) return rc;
   CUDA_OR_FAIL(h, cudaGetLastError());
@@ -698,6 +701,7 @@ static int run_iterations(dlmpc_handle* h, int max_iters, double eps_pri, double
   int n = 0;
   CUDA_OR_FAIL(h, cudaMemcpy(&n, h->d_step_iters, sizeof(int), cudaMemcpyDeviceToHost));
   if (ctl[0] == DLMPC_NOT_CONVERGED) n = ctl[5];
+  h->it_cont += n;
   if (iters) *iters = n;
   if (hist && n > 0) CUDA_OR_FAIL(h, cudaMemcpy(hist, h->d_hist, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost));
   return ctl[0];
@@ -717,6 +721,7 @@ int dlmpc_iterate(dlmpc_handle* h, int n, double* hist) {
 int dlmpc_simulate_device(dlmpc_handle* h, const double* x0_dev, int t_sim, int warm_start, int cold_start,
                           int max_iters, double eps_pri, double eps_dual, double* states_dev,
                           double* inputs_dev, int* step_iters_dev, int* status_dev) {
+  if (h) h->it_cont = 0;
   if (!h || !x0_dev || t_sim < 1 || max_iters < 1) return fail(h, DLMPC_BAD_ARGUMENT, "bad argument");
   cudaSetDevice(h->device);
   if (int rc = ensure_run_buffers(h, max_iters, t_sim)) return rc;
@@ -738,6 +743,7 @@ int dlmpc_simulate_device(dlmpc_handle* h, const double* x0_dev, int t_sim, int 
 int dlmpc_simulate(dlmpc_handle* h, const double* x0, int t_sim, int warm_start, int cold_start,
                    int max_iters, double eps_pri, double eps_dual, double* states, double* inputs,
                    int* step_iters, int* fail_step, int64_t* bad_row, int* fail_iters, double* fail_hist) {
+  if (h) h->it_cont = 0;
   if (!h || !x0 || t_sim < 1) return fail(h, DLMPC_BAD_ARGUMENT, "bad argument");
   cudaSetDevice(h->device);
   if (int rc = ensure_run_buffers(h, max_iters, t_sim)) return rc;
@@ -793,6 +799,7 @@ int dlmpc_get(dlmpc_handle* h, int which, double* dst) {
 }
 
 int dlmpc_put(dlmpc_handle* h, int which, const double* src) {
+  if (h) h->it_cont = 0;
   if (!h || !src) return fail(h, DLMPC_BAD_ARGUMENT, "null argument");
   cudaSetDevice(h->device);
   int ctl[8];
@@ -827,6 +834,7 @@ int dlmpc_get_cols(dlmpc_handle* h, int which, int c0, int n, double* dst) {
 }
 
 int dlmpc_put_cols(dlmpc_handle* h, int which, int c0, int n, const double* src) {
+  if (h) h->it_cont = 0;
   if (!h || !src || c0 < 0 || n < 0 || c0 + n > h->P.n_cols) return fail(h, DLMPC_BAD_ARGUMENT, "bad column range");
   cudaSetDevice(h->device);
   int ctl[8];
@@ -887,6 +895,7 @@ int dlmpc_halo_pack(dlmpc_handle* h, double* out) {
 int dlmpc_halo_unpack(dlmpc_handle* h, const double* in) {
   if (!h || (h->n_recv && !in)) return fail(h, DLMPC_BAD_ARGUMENT, "null halo buffer");
   if (!h->n_recv) return DLMPC_OK;
+  h->it_cont = 0;   // halo columns changed under the stream kernel's Φ-dot partials
   cudaSetDevice(h->device);
   int ctl[8];
   if (int rc = read_ctl(h, ctl)) return rc;
@@ -922,6 +931,7 @@ int dlmpc_finish_step(dlmpc_handle* h, double* u_out, double* x_next_out) {
 }
 
 int dlmpc_zero(dlmpc_handle* h) {
+  if (h) h->it_cont = 0;
   if (!h) return fail(h, DLMPC_BAD_ARGUMENT, "null handle");
   cudaSetDevice(h->device);
   const size_t ncell = (size_t)h->P.n_cols * h->P.s_pad;

@@ -127,6 +127,8 @@ struct DevProblem {
 
 struct RunArgs {
   int t_sim, closed_loop, warm_start, cold_start, max_iters, stop_on_conv;
+  int it_base;         // iterations already run on this state (host-driven iterate calls): the
+                       // stream kernel continues its Φ-dot partials instead of a full Φ
   double eps_pri, eps_dual;
   double* hist;        // [2*max_iters] history of the current / failing step
   int* step_iters;     // [t_sim]
@@ -1134,8 +1136,8 @@ struct LamWait {
 // instantiation and read the basis from L2 -- a separate instantiation, so
 // the common path keeps shared-memory fragment loads.
 template <int TC, bool OPS>
-__device__ void stream_iteration(const DevProblem& P, int b, const double* x, int it, double* smem, int& cur,
-                                 unsigned (&ph)[3]) {
+__device__ void stream_iteration(const DevProblem& P, int b, const double* x, int it, int itg, double* smem,
+                                 int& cur, unsigned (&ph)[3]) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* s_patch = smem + P.off_patch;
   double* c_patch = smem + P.off_cpatch;
@@ -1153,8 +1155,9 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
   const int ldl = P.ldl;
   const double* psi = P.psi[b];
   const double* lam = P.lam[b];
-  double* part_out = P.part_buf[it & 1];
-  const double* part_in = P.part_buf[(it & 1) ^ 1];
+  // itg counts iterations on this state across launches (it + it_base)
+  double* part_out = P.part_buf[itg & 1];
+  const double* part_in = P.part_buf[(itg & 1) ^ 1];
   const double rho = P.rho;
   double pri_m = 0.0, dual_m = 0.0;
   PT_DECL
@@ -1216,7 +1219,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
     if (nch > 0 && tid < chtab[2]) x_first = ld_cg(x + chtab[1] + tid);   // consumed after the Φ loop
     PT_LAP(P, 3)
     // Φ scales of the patch rows
-    if (it == 0) {
+    if (itg == 0) {
       for (int i = plo + warp; i < phi_; i += kWarps) {
         const int r_off = static_cast<int>(P.row_start[i] - prow0);
         double* dst = s_patch + r_off;
@@ -1594,8 +1597,9 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
     while (MODE != kPatch && it < R.max_iters) {
       PT_DECL
       if (MODE == kStream) {
-        if (P.cta_gop && P.cta_gop[blockIdx.x]) stream_iteration<TC, false>(P, b, x, it, smem, cur, ph);
-        else stream_iteration<TC, true>(P, b, x, it, smem, cur, ph);
+        const int itg = it + (R.closed_loop ? 0 : R.it_base);
+        if (P.cta_gop && P.cta_gop[blockIdx.x]) stream_iteration<TC, false>(P, b, x, it, itg, smem, cur, ph);
+        else stream_iteration<TC, true>(P, b, x, it, itg, smem, cur, ph);
         PT_START
       } else {
         PT_START

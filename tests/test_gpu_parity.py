@@ -423,3 +423,27 @@ class TestVerifyFixedPoint:
             assert rep.audit_worst[key] <= 1e-3, key
         if variant == EXACT:
             assert np.array_equal(traj.states, g["states"])
+
+
+def test_stream_host_driven_iterations_equal_one_solve():
+    """Host-driven dlmpc_iterate(1) calls continue the stream kernel's Φ-dot
+    partials across launches (the partitioned driver's loop): bit for bit the
+    same iterates and residual history as one dlmpc_solve."""
+    from paper_2103_14990_b200.device import PSI, LAM
+    system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=2500, d=3, horizon=10, seed=3))
+    os.environ["DLMPC_FORCE_STREAM"] = "1"
+    try:
+        s = pb.DlmpcSession(system, spec, mask, FAST)
+    finally:
+        os.environ.pop("DLMPC_FORCE_STREAM")
+    dev = s.device
+    assert dev.info()["mode"] == "stream"
+    dev.zero(); dev.set_x(x0)
+    n, hist, ok = dev.solve(spec.max_iters, spec.eps_pri, spec.eps_dual)
+    assert ok
+    psi_a, lam_a = dev.get(PSI), dev.get(LAM)
+    dev.zero(); dev.set_x(x0)
+    hist_b = np.concatenate([dev.iterate(1) for _ in range(n)])
+    assert np.array_equal(hist, hist_b)
+    assert np.array_equal(dev.get(PSI), psi_a) and np.array_equal(dev.get(LAM), lam_a)
+    s.close()
