@@ -911,11 +911,21 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
   const double* lam = P.lam[b];
   double pri_m = 0.0, dual_m = 0.0;
   bool tested = it == 0;
+  // the two residual words: one load per CTA (thread 0), broadcast through
+  // shared memory at the Φ barrier -- every thread of every CTA loading the
+  // same L2 line is a hot spot of ~5k requests per iteration
   unsigned long long rp = 0, rd = 0;
-  if (!tested) { rp = __ldcg(P.resid + 2 * (it - 1)); rd = __ldcg(P.resid + 2 * (it - 1) + 1); }
+  unsigned long long* rbc = reinterpret_cast<unsigned long long*>(smem + P.off_red);
+  if (!tested && threadIdx.x == 0) { rp = __ldcg(P.resid + 2 * (it - 1)); rd = __ldcg(P.resid + 2 * (it - 1) + 1); }
   PT_DECL
   const int un_a = P.cta_unit_ptr[blockIdx.x];
-  if (un_a == P.cta_unit_ptr[blockIdx.x + 1] && !tested && patch_stop_test(P, R, it, rp, rd)) return true;
+  if (un_a == P.cta_unit_ptr[blockIdx.x + 1] && !tested) {
+    if (threadIdx.x == 0) { rbc[0] = rp; rbc[1] = rd; }
+    __syncthreads();
+    rp = rbc[0]; rd = rbc[1];
+    __syncthreads();   // every warp has read the slots before the publish reuses them
+    if (patch_stop_test(P, R, it, rp, rd)) return true;
+  }
   for (int un = un_a; un < P.cta_unit_ptr[blockIdx.x + 1]; ++un) {
     PT_START
     int own_lo, own_hi, plo, phi_, prows, ch_a, ch_b, k0 = 0, c00 = 0, nt0 = 0, S0 = 0, o_off, o_n;
@@ -962,10 +972,12 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
       else
         phi_rows_of<false>(P, i, psi, lam, x, out);
     }
+    if (!tested && threadIdx.x == 0) { rbc[0] = rp; rbc[1] = rd; }
     __syncthreads();
     PT_LAP(P, 0)
     if (!tested) {
       tested = true;
+      rp = rbc[0]; rd = rbc[1];
       if (patch_stop_test(P, R, it, rp, rd)) {
         cp_async_wait<0>();
         return true;
@@ -1614,8 +1626,13 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
       grid.sync();
       PT_LAP(P, 6)
       b ^= 1;
-      const double pri = __longlong_as_double(static_cast<long long>(__ldcg(P.resid + 2 * it)));
-      const double dual = P.rho * __longlong_as_double(static_cast<long long>(__ldcg(P.resid + 2 * it + 1)));
+      // one load of the residual words per CTA, broadcast through shared memory
+      unsigned long long* rbc = reinterpret_cast<unsigned long long*>(smem + P.off_red);
+      if (tid == 0) { rbc[0] = __ldcg(P.resid + 2 * it); rbc[1] = __ldcg(P.resid + 2 * it + 1); }
+      __syncthreads();
+      const double pri = __longlong_as_double(static_cast<long long>(rbc[0]));
+      const double dual = P.rho * __longlong_as_double(static_cast<long long>(rbc[1]));
+      __syncthreads();   // the slots are reused by the next iteration's residual publish
       if (leader) { R.hist[2 * it] = pri; R.hist[2 * it + 1] = dual; }
       ++it;
       if (R.stop_on_conv && pri <= R.eps_pri && dual <= R.eps_dual) { conv = true; break; }
