@@ -163,7 +163,7 @@ def cpu_baseline(pb, system, spec, mask, seconds_budget=20.0):
             "ms_per_mpc_step": 1e3 * dt / steps}
 
 
-SWEEP_NS = (1000, 10000, 100000, 1000000)
+SWEEP_NS = (100, 300, 1000, 3000, 10000, 100000, 1000000)
 
 
 def sweep(pb, hbm_peak, cpu_seconds=6.0):
