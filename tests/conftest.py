@@ -64,3 +64,28 @@ def random_graph_system(n, rng, p_edge=0.35, states_per=2):
         for j in graph.adjacency[i]:
             a[s, states_per * j:states_per * (j + 1)] = rng.uniform(-0.2, 0.2, (states_per, states_per))
     return pb.LtiSystem(a.tocsr(), b.tocsr(), part, graph)
+
+
+def grid_network(rows, cols):
+    """A 2-D grid of the chain's subsystems (2 states, 1 input; the chain's
+    self and coupling blocks, coupled to the 4 grid neighbours), built through
+    the generic LtiSystem / SubsystemGraph.from_edges path (SURVEY §8(d) C5:
+    'a grid ... through the generic path'). Balls are diamonds, not
+    contiguous id ranges: the two-phase kernel and the col_irow tables."""
+    import scipy.sparse as sp
+    import paper_2103_14990_b200 as pb
+    n = rows * cols
+    idx = lambda r, c: r * cols + c
+    edges = [(idx(r, c), idx(r, c + 1)) for r in range(rows) for c in range(cols - 1)]
+    edges += [(idx(r, c), idx(r + 1, c)) for r in range(rows - 1) for c in range(cols)]
+    graph = pb.SubsystemGraph.from_edges(n, edges)
+    part = pb.SubsystemPartition.uniform(n, 2, 1)
+    a = sp.lil_matrix((2 * n, 2 * n))
+    b = sp.lil_matrix((2 * n, n))
+    for i in range(n):
+        a[2 * i:2 * i + 2, 2 * i:2 * i + 2] = [[1.0, 0.1], [-0.3, 0.7]]
+        b[2 * i, i] = 1.0
+        b[2 * i + 1, i] = 1.0
+        for j in graph.adjacency[i]:
+            a[2 * i + 1, 2 * j:2 * j + 2] = [0.05, 0.05]
+    return pb.LtiSystem(a.tocsr(), b.tocsr(), part, graph)

@@ -447,3 +447,23 @@ def test_stream_host_driven_iterations_equal_one_solve():
     assert np.array_equal(hist, hist_b)
     assert np.array_equal(dev.get(PSI), psi_a) and np.array_equal(dev.get(LAM), lam_a)
     s.close()
+
+
+@pytest.mark.parametrize("variant", [EXACT, FAST])
+def test_grid_network_against_oracle(variant):
+    """A 5x6 grid (generic graph path: diamond balls, two-phase kernel)."""
+    from conftest import grid_network
+    system = grid_network(5, 6)
+    spec = pb.make_benchmark_spec(system, 4)
+    mask = pb.build_locality_mask(system, 2, 4)
+    tables = pb.LayoutTables(mask)
+    cs = pb.precompute_column_solvers(pb.build_dynamics_operator(system, 4), mask)
+    x0 = pb.sample_initial_state(system.partition, np.random.default_rng(8))
+    ref = admm_ref.simulate(system, spec, tables, cs, x0, 3)
+    traj, _ = pb.dlmpc_simulate(system, spec, mask, x0, 3, variant)
+    assert list(traj.step_iterations) == ref["step_iterations"]
+    if variant == EXACT:
+        assert np.array_equal(traj.states, ref["states"])
+        assert np.array_equal(traj.inputs, ref["inputs"])
+    else:
+        assert rel_err(traj.states, ref["states"]) <= FAST_RTOL

@@ -111,7 +111,7 @@ def test_null_space_form_equals_projector(rng):
         np.testing.assert_allclose(fast, ref, rtol=0, atol=1e-12)
 
 
-@pytest.mark.parametrize("case", ["chain30", "chain_r2", "chain_two_inputs", "random_graph"])
+@pytest.mark.parametrize("case", ["chain30", "chain_r2", "chain_two_inputs", "random_graph", "grid"])
 def test_structural_builder_equals_reference_builder(case):
     """build_column_classes_structural (fingerprints + window extraction, used
     by the device session at scale) yields the same operators, bit for bit,
@@ -124,6 +124,9 @@ def test_structural_builder_equals_reference_builder(case):
         system, t, d = pb.build_chain_network(12, 2), 4, 2
     elif case == "chain_two_inputs":
         system, t, d = pb.build_chain_network(10, 1, True), 5, 2
+    elif case == "grid":
+        from conftest import grid_network
+        system, t, d = grid_network(6, 7), 4, 2
     else:
         system, t, d = random_graph_system(9, np.random.default_rng(11)), 3, 2
     mask = pb.build_locality_mask(system, d, t)
