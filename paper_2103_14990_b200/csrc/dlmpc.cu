@@ -79,8 +79,9 @@ int alloc(dlmpc_handle* h, size_t n, T** dst) {
 
 using KernelFn = void (*)(DevProblem, RunArgs);
 
-KernelFn pick_kernel(int mode, int tc) {
+KernelFn pick_kernel(int mode, int tc, int rb = 0) {
   if (mode == kExact) return dlmpc_persistent<8, kExact>;
+  if (mode == kPatch && rb) return dlmpc_persistent<8, kPatchRb>;   // TC 8 only
   if (mode == kPatch) return tc == 16 ? dlmpc_persistent<16, kPatch> : dlmpc_persistent<8, kPatch>;
   if (mode == kStream) return tc == 16 ? dlmpc_persistent<16, kStream> : dlmpc_persistent<8, kStream>;
   return tc == 16 ? dlmpc_persistent<16, kTwoPhase> : dlmpc_persistent<8, kTwoPhase>;
@@ -113,7 +114,7 @@ int ensure_run_buffers(dlmpc_handle* h, int max_iters, int t_sim) {
 }
 
 int launch(dlmpc_handle* h, const RunArgs& R) {
-  KernelFn fn = pick_kernel(h->mode, h->P.tile_cols);
+  KernelFn fn = pick_kernel(h->mode, h->P.tile_cols, h->P.rb_gemv);
   DevProblem P = h->P;
   RunArgs Rc = R;
   void* args[] = {&P, &Rc};
@@ -443,6 +444,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
     }
     bool one_unit = true;
     for (int q = 0; q < G; ++q) one_unit = one_unit && (cta_ptr[q + 1] - cta_ptr[q] <= 1);
+    bool rb_off = false;   // the register-blocked GEMV pair was planned but did not fit
     for (; h->mode != kStream;) {
       const int ldk = ld_frag(s8_max), ldy = ld_frag(tc);
       int split_max = 1;
@@ -453,8 +455,26 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         split_max = std::max(split_max, sp);
       }
       const long long meta_phi = np_max * pr->d_pad * 2 + np_max + 3 * prows_max + (np_max + 1) / 2 + np_max + 8 + 2;
+      // patch mode, TC 8: room for the register-blocked GEMV pair (thread-major
+      // operator, 16 warps' Y partials) when the classes fit its blocking
+      // (every chunk <= 2 columns; measured on C2: 8.4 vs 9.6 us per ADMM
+      // iteration against the DFMA GEMV + DMMA GEMM pair). That path needs no K tile and stages
+      // two columns, which keeps the plan inside the 196 KB carveout (a larger
+      // one leaves too little L1 for the kernel's table loads: -25% measured).
+      bool rb = h->mode == kPatch && tc == 8 && !rb_off;
+      const int rb_al = RB_AL_MAX;
+      for (int n : ch_n) rb = rb && n <= 2;
+      for (int k = 0; k < pr->n_classes && rb; ++k) {
+        const int s8 = (pr->class_s[k] + 7) & ~7, n08 = (pr->class_n0[k] + 7) & ~7;
+        rb = s8 <= 32 * RB_PL && n08 <= 16 * RB_AL_MAX;
+      }
+      if (const char* e = getenv("DLMPC_RB_GEMV")) rb = rb && e[0] != '0';
+      const long long rb_opr = rb ? (long long)RB_PL * rb_al * kThreads : 0;
+      const long long rb_part = rb ? 2LL * 16 * rb_al * kWarps : 0;
+      const int kt_cols = rb ? 0 : tc, st_cols = rb ? 2 : tc;
+      auto part = [&](int sp) { return std::max<long long>(sp > 1 ? (long long)sp * n08_max * tc : 0, rb_part); };
       auto total = [&](long long opr, int sp, bool cache) {
-        return opr + (long long)tc * ldk + (long long)n08_max * ldy + (sp > 1 ? (long long)sp * n08_max * tc : 0)
+        return opr + (long long)kt_cols * ldk + (long long)n08_max * ldy + part(sp)
                + 32 + 4 * tc + prows_max + (cache ? meta_phi : 0) + 4;
       };
       while (split_max > 1 && total(0, split_max, false) > limit) split_max >>= 1;
@@ -462,21 +482,23 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         if (tc == 16) { tc = 8; continue; }
         return fail(h, DLMPC_BAD_ARGUMENT, "column tile does not fit in shared memory");
       }
-      const long long opr = total(opr_need, split_max, false) <= limit ? opr_need : 0;
+      long long opr = total(opr_need, split_max, false) <= limit ? opr_need : 0;
+      if (rb && opr > 0 && opr < rb_opr && total(rb_opr, split_max, false) <= limit) opr = rb_opr;
       const bool cache = h->mode == kPatch && one_unit && total(opr, split_max, true) <= limit;
       // cp.async staging buffers for chunk ψ,λ (patch mode): 2 if they fit, else 1, else none
-      const long long stash_one = 2LL * tc * ldk;
+      const long long stash_one = 2LL * st_cols * ldk;
       int stash_bufs = 0;
       if (h->mode == kPatch) {
         const long long base = total(opr, split_max, cache);
         stash_bufs = base + 2 * stash_one + 2 <= limit ? 2 : (base + stash_one + 2 <= limit ? 1 : 0);
       }
+      if (rb && (stash_bufs == 0 || opr < rb_opr)) { rb_off = true; continue; }
       long long off = (opr + 1) & ~1LL;
       P.opr_cap = (int)opr;
       P.s8_max = s8_max; P.n08_max = n08_max; P.ldk = ldk; P.ldy = ldy; P.split_max = split_max;
-      P.off_k = (int)off; off += (long long)tc * ldk;
+      P.off_k = (int)off; off += (long long)kt_cols * ldk;
       P.off_y = (int)off; off += (long long)n08_max * ldy;
-      P.off_yp = (int)off; off += split_max > 1 ? (long long)split_max * n08_max * tc : 0;
+      P.off_yp = (int)off; off += part(split_max);
       {   // GEMV partials of small chunks share the split-K partials region
         const char* e = getenv("DLMPC_SMALL_GEMV");
         P.small_gemv = (split_max > 1 && (long long)split_max * tc >= 10 && !(e && e[0] == '0')) ? 1 : 0;
@@ -491,6 +513,8 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       off = (off + 1) & ~1LL;   // 16-byte alignment for cp.async
       P.off_stash = (int)off; off += stash_bufs * stash_one;
       P.stash_bufs = stash_bufs;
+      P.stash_cols = st_cols;
+      P.rb_gemv = rb ? 1 : 0;
       P.off_ex = (int)off;
       h->smem_bytes = (int)(off * 8);
       P.tile_cols = tc;
@@ -509,6 +533,12 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       }
       ch_cls.swap(nc_cls); ch_c0.swap(nc_c0); ch_n.swap(nc_n); u_chunk.swap(nu);
     }
+    // patch mode, C2-sized networks: the register-blocked GEMV pair when every
+    // chunk has <= 2 columns and every class operator fits its thread blocking
+    // (measured on C2: GEMV pair 1.3 us vs 2.1 us for the DFMA GEMV + DMMA GEMM)
+    if (getenv("DLMPC_DEBUG_PLAN"))
+      fprintf(stderr, "plan: mode %d tc %d stash %d opr %d split %d n08 %d ldy %d rb %d chunks %zu cache %d smem %d\n", h->mode,
+              P.tile_cols, P.stash_bufs, P.opr_cap, P.split_max, P.n08_max, P.ldy, P.rb_gemv, ch_n.size(), P.cache_phi, h->smem_bytes);
     if (h->mode == kPatch || h->mode == kStream) {
       int rc;
       if ((rc = upload(h, cta_ptr.data(), cta_ptr.size(), &P.cta_unit_ptr)) ||
@@ -545,7 +575,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       }
     }
   }
-  KernelFn fn = pick_kernel(h->mode, P.tile_cols);
+  KernelFn fn = pick_kernel(h->mode, P.tile_cols, P.rb_gemv);
   CUDA_OR_FAIL(h, cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
   int per_sm = 0;
@@ -629,7 +659,7 @@ int dlmpc_create(const dlmpc_problem* pr, int device, dlmpc_handle** out) {
     if ((rc = alloc(h, (size_t)(pr->n_inputs ? pr->n_inputs : 1), &P.u)) != DLMPC_OK) goto bad;
     if ((rc = alloc(h, 8, &P.ctl)) != DLMPC_OK) goto bad;
     if ((rc = alloc(h, ncell, &h->d_scratch)) != DLMPC_OK) goto bad;
-    if ((rc = alloc(h, 8 * 1024, &P.phase_ns)) != DLMPC_OK) goto bad;
+    if ((rc = alloc(h, 16 * 1024, &P.phase_ns)) != DLMPC_OK) goto bad;
     if (cudaMemset(P.ctl + 2, 0x7f, sizeof(int) * 2) != cudaSuccess) { rc = fail(h, DLMPC_CUDA_ERROR, "memset"); goto bad; }
 
     if ((rc = plan(h, pr)) != DLMPC_OK) goto bad;
@@ -995,8 +1025,8 @@ int dlmpc_audit(dlmpc_handle* h, const double* phi_host, double* out3) {
 
 int dlmpc_phase_times(dlmpc_handle* h, uint64_t* out, int reset) {
   if (!h || !out) return DLMPC_BAD_ARGUMENT;
-  CUDA_OR_FAIL(h, cudaMemcpy(out, h->P.phase_ns, sizeof(uint64_t) * 8 * h->grid, cudaMemcpyDeviceToHost));
-  if (reset) CUDA_OR_FAIL(h, cudaMemset(h->P.phase_ns, 0, sizeof(uint64_t) * 8 * h->grid));
+  CUDA_OR_FAIL(h, cudaMemcpy(out, h->P.phase_ns, sizeof(uint64_t) * 16 * h->grid, cudaMemcpyDeviceToHost));
+  if (reset) CUDA_OR_FAIL(h, cudaMemset(h->P.phase_ns, 0, sizeof(uint64_t) * 16 * h->grid));
   return DLMPC_OK;
 }
 

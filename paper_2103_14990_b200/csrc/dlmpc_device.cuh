@@ -34,15 +34,15 @@ namespace cg = cooperative_groups;
 namespace dlmpc {
 
 // Optional per-phase timers (profiling build only: -DDLMPC_PHASE_TIMING).
-// Thread 0 of every CTA accumulates globaltimer deltas per phase into
-// P.phase_ns[blockIdx.x * 8 + phase].
+// Thread 0 of every CTA accumulates SM-cycle deltas per phase into
+// P.phase_ns[blockIdx.x * 16 + phase] (0-7 per iteration, 8-15 per MPC step).
 #ifdef DLMPC_PHASE_TIMING
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t;
+__device__ __forceinline__ unsigned long long gtimer() {   // SM cycles (globaltimer is too coarse)
+  return static_cast<unsigned long long>(clock64());
 }
 #define PT_DECL unsigned long long pt_t0 = 0;
 #define PT_START if (threadIdx.x == 0) pt_t0 = gtimer();
-#define PT_LAP(P, ph) if (threadIdx.x == 0) { unsigned long long t1_ = gtimer(); (P).phase_ns[blockIdx.x * 8 + (ph)] += t1_ - pt_t0; pt_t0 = t1_; }
+#define PT_LAP(P, ph) if (threadIdx.x == 0) { unsigned long long t1_ = gtimer(); (P).phase_ns[blockIdx.x * 16 + (ph)] += t1_ - pt_t0; pt_t0 = t1_; }
 #else
 #define PT_DECL
 #define PT_START
@@ -55,7 +55,8 @@ constexpr int kBadNone = 0x7f7f7f7f;   // cudaMemset(0x7f) pattern = "no infeasi
 constexpr int kMG1 = 4;                // m-tiles per GEMM-1 work unit
 constexpr int kMG2 = 2;                // m-tiles per GEMM-2 work unit
 
-enum Mode { kPatch = 0, kTwoPhase = 1, kExact = 2, kStream = 3 };
+enum Mode { kPatch = 0, kTwoPhase = 1, kExact = 2, kStream = 3,
+            kPatchRb = 4 };   // kPatch with the register-blocked GEMV pair (P.rb_gemv)
 
 struct DevProblem {
   int n_sub, n_rows, n_cols, n_inputs, s_pad, exact, contiguous, d_row;
@@ -91,7 +92,7 @@ struct DevProblem {
   double* psi[2]; double* lam[2]; double* s_row; double* ada; double* x[2]; double* u;
   unsigned long long* resid;   // [2 * cap] residual maxima per iteration (ordered bits)
   int* ctl;                    // 0 status, 1 fail step, 2/3 bad-row slots, 4 cur buffer, 5 fail iters
-  unsigned long long* phase_ns;   // [grid * 8] (profiling build only)
+  unsigned long long* phase_ns;   // [grid * 16] (profiling build only)
   // shared-memory plan (offsets in doubles)
   int opr_cap;                 // doubles of the per-CTA operator region at smem offset 0
   int s8_max, n08_max, ldk, ldy, split_max, patch_cap, cache_phi;
@@ -123,6 +124,8 @@ struct DevProblem {
   int ldl;                     // stream mode: row stride of the λ stash
   int warp_spec;               // stream mode: producer/consumer warp specialisation
   int small_gemv;              // patch mode: DFMA GEMV for GEMM 1 of chunks with <= 2 columns
+  int rb_gemv;                 // patch mode, TC 8: register-blocked GEMV pair for chunks of <= 2 columns
+  int stash_cols;              // columns per ψ,λ staging buffer (TC, or 2 with rb_gemv)
 };
 
 struct RunArgs {
@@ -556,6 +559,126 @@ __device__ __forceinline__ void gemv1_small(int S, int n08, int ldn, const doubl
   __syncthreads();
 }
 
+// Register-blocked GEMV pair for chunks of <= 2 live columns (C2-sized
+// networks), no tensor cores (north_star (4): warp shuffles for the small
+// dense mat-vecs). Thread (warp w, lane l = 16h + j) owns the operator block
+// rows p_i = w*PB + h*RB_PL + i (i < RB_PL) x columns a_c = j*RB_AL + c
+// (c < RB_AL), staged thread-major (`opT[(i*RB_AL + c)*kThreads + tid]`, see
+// stage_operator_rb) so each load is conflict free and the operator is read
+// exactly once per GEMV.
+//   GEMV 1  Y[a][t] = sum_p N[p][a] K[t][p]: 6 partials per thread, a
+//           reduce-scatter over the two p halves (one shuffle per value), then
+//           the 16 warps' partials summed in shared memory (`ypart`, 16*96).
+//   GEMV 2  O[t][p] = sum_a N[p][a] Y[a][t]: 14 partials per thread reduced
+//           over the 16 a lanes by a reduce-scatter (15 shuffles); lane j ends
+//           with O[t = j>>3][p_(j&7)] and calls epi(p, t, o) for valid p < S.
+// Requires S8 <= 16*2*RB_PL (PB = ceil(S8/16) <= 14) and n08 <= 16*RB_AL.
+constexpr int RB_PL = 7, RB_AL_MAX = 4;   // rows per thread; operator columns per lane (<= 4)
+
+__device__ __forceinline__ bool rb_fits(int S8, int n08) { return S8 <= 32 * RB_PL && n08 <= 16 * RB_AL_MAX; }
+
+// Thread-major operator copy for gemv_pair_rb (class k, at smem offset 0).
+template <int RB_AL>
+__device__ __forceinline__ void stage_operator_rb(const DevProblem& P, int k, double* opT) {
+  const int S = P.class_s[k], n0 = P.class_n0[k], ldn = P.class_ldn[k];
+  const int PB = (((S + 7) & ~7) + 15) >> 4;
+  const double* src = P.null_pool + P.class_null_off[k];
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, h = l >> 4, j = l & 15;
+#pragma unroll
+  for (int i = 0; i < RB_PL; ++i) {
+    const int pr = h * RB_PL + i, p = w * PB + pr;
+#pragma unroll
+    for (int c = 0; c < RB_AL; ++c) {
+      const int a = j * RB_AL + c;
+      opT[(i * RB_AL + c) * kThreads + tid] = (pr < PB && p < S && a < n0) ? __ldg(src + static_cast<size_t>(p) * ldn + a) : 0.0;
+    }
+  }
+}
+
+template <int RB_AL>
+__device__ __forceinline__ void load_operator_rb(const double* opT, double (&op)[RB_PL][RB_AL]) {
+#pragma unroll
+  for (int i = 0; i < RB_PL; ++i)
+#pragma unroll
+    for (int c = 0; c < RB_AL; ++c) op[i][c] = opT[(i * RB_AL + c) * kThreads + threadIdx.x];
+}
+
+// kf(t, p): K[t][p] for p < S (called for this thread's rows only).
+template <int RB_AL, class KF, class Epi>
+__device__ __forceinline__ void gemv_pair_rb(int S, const double (&op)[RB_PL][RB_AL], const KF& kf,
+                                             double* ypart, double* yb2, int nt, const Epi& epi) {
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, h = l >> 4, j = l & 15;
+  const int PB = (((S + 7) & ~7) + 15) >> 4;
+  const int prow0 = w * PB + h * RB_PL;   // first operator row of this thread
+  const int nrow = max(0, min(RB_PL, min(PB - h * RB_PL, S - prow0)));
+  // GEMV 1
+  double y0[RB_AL], y1[RB_AL];
+#pragma unroll
+  for (int c = 0; c < RB_AL; ++c) { y0[c] = 0.0; y1[c] = 0.0; }
+#pragma unroll
+  for (int i = 0; i < RB_PL; ++i) {
+    const double k0 = i < nrow ? kf(0, prow0 + i) : 0.0;
+    const double k1 = (i < nrow && nt > 1) ? kf(1, prow0 + i) : 0.0;
+#pragma unroll
+    for (int c = 0; c < RB_AL; ++c) { y0[c] = fma(op[i][c], k0, y0[c]); y1[c] = fma(op[i][c], k1, y1[c]); }
+  }
+  // reduce-scatter over the p halves: h = 0 keeps column 0, h = 1 column 1
+#pragma unroll
+  for (int c = 0; c < RB_AL; ++c) {
+    const double keep = h ? y1[c] : y0[c], send = h ? y0[c] : y1[c];
+    ypart[(w * 2 + h) * (16 * RB_AL) + j * RB_AL + c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  __syncthreads();
+  if (tid < 2 * 16 * RB_AL) {   // Y[t][a] = sum over the 16 warps (fixed order)
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+#pragma unroll
+    for (int q = 0; q < kWarps; q += 4) {
+      const int t = tid / (16 * RB_AL), a = tid - t * (16 * RB_AL);
+      v0 += ypart[((q + 0) * 2 + t) * (16 * RB_AL) + a];
+      v1 += ypart[((q + 1) * 2 + t) * (16 * RB_AL) + a];
+      v2 += ypart[((q + 2) * 2 + t) * (16 * RB_AL) + a];
+      v3 += ypart[((q + 3) * 2 + t) * (16 * RB_AL) + a];
+    }
+    yb2[tid] = (tid / (16 * RB_AL) < nt) ? (v0 + v1) + (v2 + v3) : 0.0;
+  }
+  __syncthreads();
+  // GEMV 2
+  double ya[RB_AL], yc[RB_AL];
+#pragma unroll
+  for (int c = 0; c < RB_AL; ++c) { ya[c] = yb2[j * RB_AL + c]; yc[c] = yb2[16 * RB_AL + j * RB_AL + c]; }
+  double v[16];
+#pragma unroll
+  for (int i = 0; i < RB_PL; ++i) {
+    double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+    for (int c = 0; c < RB_AL; ++c) { o0 = fma(op[i][c], ya[c], o0); o1 = fma(op[i][c], yc[c], o1); }
+    v[i] = o0; v[8 + i] = o1;
+  }
+  v[7] = 0.0; v[15] = 0.0;
+  // reduce-scatter over the 16 a lanes: lane j keeps index (j>>3)*8 + (j&7)
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const bool up = j & 8;
+    v[k] = (up ? v[8 + k] : v[k]) + __shfl_xor_sync(0xffffffffu, up ? v[k] : v[8 + k], 8);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool up = j & 4;
+    v[k] = (up ? v[4 + k] : v[k]) + __shfl_xor_sync(0xffffffffu, up ? v[k] : v[4 + k], 4);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const bool up = j & 2;
+    v[k] = (up ? v[2 + k] : v[k]) + __shfl_xor_sync(0xffffffffu, up ? v[k] : v[2 + k], 2);
+  }
+  {
+    const bool up = j & 1;
+    v[0] = (up ? v[1] : v[0]) + __shfl_xor_sync(0xffffffffu, up ? v[0] : v[1], 1);
+  }
+  const int t = j >> 3, i = j & 7;
+  if (i < nrow && t < nt) epi(prow0 + i, t, v[0]);
+}
+
 // GEMM-2 epilogue of the patch/two-phase kernels: O back into kt.
 struct StoreO {
   double* kt; int ldk;
@@ -734,6 +857,77 @@ __device__ __forceinline__ void run_chunk(const DevProblem& P, int k, int nt, co
     fast_chunk<TC, S_GLOBAL, false>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st);
 }
 
+// Patch-kernel chunk of <= 2 columns on the register-blocked GEMV pair
+// (P.rb_gemv): K = φ + λ is formed inside GEMV 1 from the staged ψ, λ and the
+// patch's Φ scales (no prologue pass), and every thread runs the epilogue of
+// the one (row, column) element GEMV 2 leaves it, with its operands fetched
+// before the GEMVs. Same formulas as fast_chunk (admm.py:183-186, 207,
+// 216-217); the operator is staged thread-major once per class.
+constexpr int kRbTag = 1 << 24;   // `cur` = k + AL * kRbTag: a thread-major staged operator
+template <int TC, int RB_AL>
+__device__ void rb_chunk_al(const DevProblem& P, int k, int nt, double* psi_n, double* lam_n, const double* s_src,
+                         double* smem, int& cur, double& pri_m, double& dual_m, const double* st) {
+  if (cur != k + RB_AL * kRbTag) {
+    __syncthreads();
+    stage_operator_rb<RB_AL>(P, k, smem);
+    __syncthreads();
+    cur = k + RB_AL * kRbTag;
+  }
+  const long long* m_pos = reinterpret_cast<const long long*>(smem + P.off_meta);
+  const long long* m_s = m_pos + TC;
+  const long long* m_q = m_pos + 2 * TC;
+  const double* m_x = smem + P.off_meta + 3 * TC;
+  const int S = P.class_s[k], ldk = P.ldk;
+  const int l = threadIdx.x & 31, w = threadIdx.x >> 5, h = l >> 4, j = l & 15;
+  const int PB = (((S + 7) & ~7) + 15) >> 4;
+  const int prow0 = w * PB + h * RB_PL;
+  const int nrow = max(0, min(RB_PL, min(PB - h * RB_PL, S - prow0)));
+  PT_DECL
+  PT_START
+  double op[RB_PL][RB_AL];
+  load_operator_rb<RB_AL>(smem, op);
+  // this thread's epilogue element (row prow0 + (j & 7), column j >> 3)
+  const int et = j >> 3, ep = prow0 + (j & 7);
+  const bool eok = (j & 7) < nrow && et < nt;
+  double e_ps = 0.0, e_lm = 0.0, e_sr = 0.0, e_q = 0.0, e_x = 0.0;
+  long long e_pos = 0;
+  if (eok) {
+    e_pos = m_pos[et]; e_x = m_x[et];
+    e_ps = st[(2 * et) * ldk + ep]; e_lm = st[(2 * et + 1) * ldk + ep];
+    e_sr = s_src[m_s[et] + ep];
+    e_q = P.q_pool[m_q[et] + ep];
+  }
+  const long long s00 = m_s[0], s01 = m_s[1];
+  const double x0 = m_x[0], x1 = m_x[1];
+  auto kf = [&](int t, int p) {   // K = φ + λ, one rounding more than φ (the fast_chunk prologue)
+    const double ps = st[(2 * t) * ldk + p], lm = st[(2 * t + 1) * ldk + p];
+    const double sr = s_src[(t ? s01 : s00) + p];
+    return __dadd_rn(make_phi<false>(__dsub_rn(ps, lm), sr, t ? x1 : x0), lm);
+  };
+  auto epi = [&](int, int, double o) {
+    const double phi = make_phi<false>(__dsub_rn(e_ps, e_lm), e_sr, e_x);
+    const double pn = e_q + o;
+    const double d = __dsub_rn(phi, pn);
+    psi_n[e_pos + ep] = pn;
+    lam_n[e_pos + ep] = __dadd_rn(e_lm, d);
+    pri_m = fmax(pri_m, fabs(d));
+    dual_m = fmax(dual_m, fabs(__dsub_rn(pn, e_ps)));
+  };
+  PT_LAP(P, 1)
+  gemv_pair_rb<RB_AL>(S, op, kf, smem + P.off_yp, smem + P.off_y, nt, epi);
+  PT_LAP(P, 2)
+}
+
+// One blocking (RB_AL = 4, n0 <= 64) for every class: a second, narrower
+// instantiation for the d=3 interior class (n0 = 47) saves its idle FMAs but
+// doubles the hot loop's code, and measured 10.6 vs 8.4 us/iteration on C2.
+template <int TC>
+__device__ __forceinline__ void rb_chunk(const DevProblem& P, int k, int nt, double* psi_n, double* lam_n,
+                                         const double* s_src, double* smem, int& cur, double& pri_m,
+                                         double& dual_m, const double* st) {
+  rb_chunk_al<TC, RB_AL_MAX>(P, k, nt, psi_n, lam_n, s_src, smem, cur, pri_m, dual_m, st);
+}
+
 // Column stage of the two-phase fast kernel (class-sorted tiles, generic graphs).
 template <int TC>
 __device__ void column_stage_tiles(const DevProblem& P, int b, const double* x, int it, double* smem,
@@ -900,7 +1094,7 @@ __device__ __forceinline__ bool patch_stop_test(const DevProblem& P, const RunAr
   return R.stop_on_conv && pri <= R.eps_pri && dual <= R.eps_dual;
 }
 
-template <int TC>
+template <int TC, bool RB>
 __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int it, double* smem,
                                 int& cur, const RunArgs& R) {
   double* s_patch = smem + P.off_patch;
@@ -953,7 +1147,7 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
     }
     // first chunk's ψ,λ start streaming into shared memory under the Φ stage
     double* stash = smem + P.off_stash;
-    const int stash_stride = 2 * TC * P.ldk;
+    const int stash_stride = 2 * P.stash_cols * P.ldk;
     if (P.stash_bufs > 0 && ch_a < ch_b) stash_issue(P, c00, nt0, S0, psi, lam, stash);
     // Φ scale of every row the unit's columns touch (own rows + d-hop halo);
     // before the stop test the own rows' s goes to shared memory only
@@ -1014,8 +1208,12 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
         m_pos[t] = pos; m_pos[TC + t] = s0; m_pos[2 * TC + t] = q0; m_x[t] = xc;
       }
       __syncthreads();
-      run_chunk<TC, false>(P, k, nt, psi, lam, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, nullptr, smem, cur,
-                           pri_m, dual_m, P.stash_bufs > 0 ? stash + sb * stash_stride : nullptr);
+      if (RB)
+        rb_chunk<TC>(P, k, nt, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, smem, cur, pri_m, dual_m,
+                     stash + sb * stash_stride);
+      else
+        run_chunk<TC, false>(P, k, nt, psi, lam, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, nullptr, smem, cur,
+                             pri_m, dual_m, P.stash_bufs > 0 ? stash + sb * stash_stride : nullptr);
       if (P.stash_bufs == 1 && ch + 1 < ch_b)   // single buffer: refill after the chunk is done
         stash_issue(P, P.chunk_col0[ch + 1], P.chunk_n[ch + 1], P.class_s[P.chunk_class[ch + 1]], psi, lam, stash);
     }
@@ -1555,6 +1753,7 @@ __device__ void zero_iterate(const DevProblem& P, int b) {
 template <int TC, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, RunArgs R) {
   constexpr bool EXACT = MODE == kExact;
+  constexpr bool PATCH = MODE == kPatch || MODE == kPatchRb;
   extern __shared__ __align__(16) double smem[];
   cg::grid_group grid = cg::this_grid();
   const int tid = threadIdx.x;
@@ -1568,6 +1767,8 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
   }
   const size_t gt = blockIdx.x * blockDim.x + tid, GT = gridDim.x * blockDim.x;
   for (int step = 0; step < R.t_sim; ++step) {
+    PT_DECL
+    PT_START
     const double* x = P.x[R.closed_loop ? (step & 1) : 0];
     int* bad_slot = P.ctl + 2 + (step & 1);
     for (size_t q = gt; q < static_cast<size_t>(2 * R.max_iters); q += GT) P.resid[q] = 0ull;
@@ -1584,10 +1785,12 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
       }
       if (leader) P.ctl[2 + ((step + 1) & 1)] = kBadNone;
     }
-    if (MODE == kPatch && P.cache_phi) cache_phi_meta<TC>(P, x, smem);
+    PT_LAP(P, 8)
+    if (PATCH && P.cache_phi) cache_phi_meta<TC>(P, x, smem);
+    PT_LAP(P, 9)
     int it = 0;
     bool conv = false;
-    if (MODE == kPatch) {
+    if (PATCH) {
       // stop test of iteration it-1 overlapped with iteration it's first Φ
       while (true) {
         PT_DECL
@@ -1598,7 +1801,7 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
           }
           break;
         }
-        if (patch_iteration<TC>(P, b, x, it, smem, cur, R)) { conv = true; break; }
+        if (patch_iteration<TC, MODE == kPatchRb>(P, b, x, it, smem, cur, R)) { conv = true; break; }
         PT_START
         grid.sync();
         PT_LAP(P, 6)
@@ -1606,7 +1809,7 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
         ++it;
       }
     }
-    while (MODE != kPatch && it < R.max_iters) {
+    while (!PATCH && it < R.max_iters) {
       PT_DECL
       if (MODE == kStream) {
         const int itg = it + (R.closed_loop ? 0 : R.it_base);
@@ -1637,6 +1840,7 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
       ++it;
       if (R.stop_on_conv && pri <= R.eps_pri && dual <= R.eps_dual) { conv = true; break; }
     }
+    PT_START
     if (leader) R.step_iters[step] = it;
     if (R.stop_on_conv && !conv) {
       if (leader) { P.ctl[0] = 1; P.ctl[1] = step; P.ctl[5] = it; P.ctl[4] = b; }
@@ -1647,14 +1851,18 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
         for (size_t q = gt; q < static_cast<size_t>(P.n_cols); q += GT) R.states[q] = x[q];
       }
       control_stage<EXACT>(P, b ^ 1, x);
+      PT_LAP(P, 10)
       grid.sync();
+      PT_LAP(P, 11)
       double* xn = P.x[(step + 1) & 1];
       plant_stage(P, x, xn);
       for (size_t q = gt; q < static_cast<size_t>(P.n_cols); q += GT)
         R.states[static_cast<size_t>(step + 1) * P.n_cols + q] = xn[q];
       for (size_t q = gt; q < static_cast<size_t>(P.n_inputs); q += GT)
         R.inputs[static_cast<size_t>(step) * P.n_inputs + q] = P.u[q];
+      PT_LAP(P, 12)
       grid.sync();
+      PT_LAP(P, 13)
     }
   }
   if (leader) { P.ctl[0] = 0; P.ctl[4] = b; }

@@ -324,12 +324,12 @@ class DeviceSession:
         return float(ms.value), int(n.value)
 
     def phase_times(self, reset=True):
-        """Per-CTA per-phase ns (profiling build), shape (grid, 8)."""
+        """Per-CTA per-phase SM cycles (profiling build), shape (grid, 16)."""
         g = self.info()["grid"]
-        out = np.zeros(8 * g, dtype=np.uint64)
+        out = np.zeros(16 * g, dtype=np.uint64)
         self._check(self._lib.dlmpc_phase_times(self._h, out.ctypes.data_as(_P(C.c_uint64)), int(reset)),
                     "dlmpc_phase_times")
-        return out.reshape(g, 8)
+        return out.reshape(g, 16)
 
     def info(self):
         out = np.zeros(9, dtype=np.int64)

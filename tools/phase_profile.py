@@ -13,10 +13,19 @@ sess.simulate(x0, t_sim)
 sess.device.phase_times(reset=True)
 traj, ms = sess.simulate(x0, t_sim)
 it = sum(traj.step_iterations)
-pt = sess.device.phase_times(reset=True).astype(np.float64) / it / 1e3   # us per iteration per CTA
+CLK_GHZ = float(os.environ.get('DLMPC_CLK_GHZ', '1.965'))   # timers count SM cycles
+raw = sess.device.phase_times(reset=True).astype(np.float64) / (1e3 * CLK_GHZ)
+pt = raw / it   # us per iteration per CTA
+st = raw[:, 8:14] / t_sim   # us per MPC step per CTA
 names = ["phi", "prologue", "gemm1", "gemm2", "epilogue", "publish", "barrier", "wait"]
 print(f"N={n} {sess.device.info()} iters {it} device {ms:.3f} ms = {1e3*ms/it:.2f} us/iter")
 for k, nm in enumerate(names):
     col = pt[:, k]
     print(f"  {nm:9s} max {col.max():7.2f} us  mean {col.mean():7.2f} us  min {col.min():7.2f}")
 print(f"  sum(max) {pt[:, :7].max(axis=0).sum():.2f}  per-CTA total max {pt[:, :7].sum(axis=1).max():.2f}")
+tot = pt[:, :8].sum(axis=1)
+for b in [int(np.argmax(tot)), int(np.argsort(tot)[len(tot) // 2])]:
+    print(f"  CTA {b}: " + " ".join(f"{nm}={pt[b, k]:.2f}" for k, nm in enumerate(names)) + f" total={tot[b]:.2f}")
+snames = ["rowdata+bar", "phimeta", "control", "bar", "plant", "bar"]
+print("  per MPC step (us): " + " ".join(f"{nm}={st[:, k].max():.2f}" for k, nm in enumerate(snames))
+      + f" total={st.sum(axis=1).max():.2f}  (device {1e3 * ms / t_sim:.2f} per step)")

@@ -1,6 +1,6 @@
 """Per-phase breakdown of the stream kernel (profiling build).
 usage: DLMPC_LIB=paper_2103_14990_b200/libdlmpc_timing.so python tools/phase_profile_stream.py N"""
-import sys
+import os, sys
 sys.path.insert(0, '.')
 import numpy as np
 import paper_2103_14990_b200 as pb
@@ -11,7 +11,7 @@ sess.simulate(x0, 1)
 sess.device.phase_times(reset=True)
 traj, ms = sess.simulate(x0, 1)
 it = sum(traj.step_iterations)
-pt = sess.device.phase_times(reset=True).astype(np.float64) / it / 1e3
+pt = sess.device.phase_times(reset=True).astype(np.float64) / it / (1e3 * float(os.environ.get("DLMPC_CLK_GHZ", "1.965")))   # SM cycles -> us
 names = ["phi loop", "chunks", "tables", "setup+stage", "first K", "publish", "barrier", "flush"]
 print(f"N={n} {sess.device.info()} iters {it} device {ms:.3f} ms = {1e3*ms/it:.2f} us/iter")
 for k, nm in enumerate(names):

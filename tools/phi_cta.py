@@ -1,4 +1,4 @@
-import sys
+import os, sys
 sys.path.insert(0, '.')
 import numpy as np
 import paper_2103_14990_b200 as pb
@@ -8,7 +8,7 @@ sess.simulate(x0, 20)
 sess.device.phase_times(reset=True)
 traj, ms = sess.simulate(x0, 20)
 it = sum(traj.step_iterations)
-pt = sess.device.phase_times(reset=True).astype(np.float64) / it / 1e3
+pt = sess.device.phase_times(reset=True).astype(np.float64) / it / (1e3 * float(os.environ.get("DLMPC_CLK_GHZ", "1.965")))   # SM cycles -> us
 L = sess.layout
 print("iters", it, "us/iter", 1e3 * ms / it)
 order = np.argsort(-pt[:, 0])
