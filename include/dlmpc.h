@@ -224,8 +224,7 @@ int dlmpc_synchronize(dlmpc_handle* h);
  * (-DDLMPC_PHASE_TIMING; zeros otherwise): out[grid*16] SM cycles; reset
  * clears them. Per iteration: 0 Φ, 1 Ψ prologue, 2 GEMM 1, 3 GEMM 2,
  * 4 epilogue, 5 residual publish, 6 grid barrier, 7 stop test; per MPC step:
- * 8 row data + barrier, 9 Φ metadata cache, 10 control, 11 barrier, 12 plant,
- * 13 barrier. */
+ * 8 row data + barrier, 9 Φ metadata cache, 10 control + plant, 11 barrier. */
 int dlmpc_phase_times(dlmpc_handle* h, uint64_t* out, int reset);
 /* Shape info: n_rows, n_cols, s_pad, n_sub, grid CTAs, tile_cols, smem bytes,
  * kernel mode (0 patch, 1 two-phase, 2 exact, 3 stream), work units. */

@@ -268,19 +268,39 @@ __device__ __forceinline__ void publish_residuals(const DevProblem& P, int it, d
   }
 }
 
+// Per-MPC-step stages run a few hundred latency-bound items (subsystems,
+// inputs, states): item q goes to CTA q % grid first, so they run one or two
+// per SM, and each item issues its loads in batches of kBatch before the
+// ordered arithmetic (the reference's summation order is kept).
+#ifndef DLMPC_KBATCH
+#define DLMPC_KBATCH 4   // 8 measured 30% slower on C2: the patch kernel sits at the 128-register cap
+#endif
+constexpr int kBatch = DLMPC_KBATCH;
+__device__ __forceinline__ long long spread_first() {
+  return static_cast<long long>(threadIdx.x) * gridDim.x + blockIdx.x;
+}
+__device__ __forceinline__ long long spread_step() { return static_cast<long long>(gridDim.x) * blockDim.x; }
+
 // ||a||^2 per subsystem (reference sls_core.py:338-339: all rows of a
 // subsystem share the support, hence a_pad and a_dot_a) and the RowInfeasible
 // scan of sls_core.py:346-348. Strict ascending order, no FMA, in all modes.
 __device__ void row_data_stage(const DevProblem& P, const double* x, int* bad_slot) {
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x, GT = gridDim.x * blockDim.x;
-  for (int i = gt; i < P.n_sub; i += GT) {
+  for (long long ii = spread_first(); ii < P.n_sub; ii += spread_step()) {
+    const int i = static_cast<int>(ii);
     const int D = P.supp_len[i];
     const int* sc = P.supp_col + static_cast<size_t>(i) * P.d_pad;
     double acc = 0.0;
-    for (int k = 0; k < D; ++k) {
-      const double xc = ld_cg(x + sc[k]);
-      const double pr = __dmul_rn(xc, xc);
-      acc = k == 0 ? pr : __dadd_rn(acc, pr);
+    for (int k0 = 0; k0 < D; k0 += kBatch) {
+      double xv[kBatch];
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) xv[u] = k0 + u < D ? ld_cg(x + sc[k0 + u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        if (k0 + u < D) {
+          const double pr = __dmul_rn(xv[u], xv[u]);
+          acc = k0 + u == 0 ? pr : __dadd_rn(acc, pr);
+        }
+      }
     }
     if (D < P.d_row) acc = __dadd_rn(acc, 0.0);   // the padded slots of a_pad
     P.ada[i] = acc;
@@ -1708,38 +1728,87 @@ __device__ void column_stage_exact(const DevProblem& P, int b, const double* x, 
 // u_k = ascending dot of φ_r[input row k, t=0] with x (admm.py:350-360);
 // φ is rebuilt from the iterate the last Φ stage read (buffer pb).
 template <bool EXACT>
-__device__ void control_stage(const DevProblem& P, int pb, const double* x) {
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x, GT = gridDim.x * blockDim.x;
-  for (int k = gt; k < P.n_inputs; k += GT) {
-    const int i = P.input_owner[k], l = P.input_local[k];
-    const double s = ld_cg(P.s_row + P.row_start[i] + l);
-    const int D = P.supp_len[i];
-    const int* sc = P.supp_col + static_cast<size_t>(i) * P.d_pad;
-    const int* so = P.supp_off + static_cast<size_t>(i) * P.d_pad;
-    double acc = 0.0;
-    for (int q = 0; q < D; ++q) {
-      const int c = sc[q];
-      const size_t pos = static_cast<size_t>(c) * P.s_pad + so[q] + l;
-      const double xc = ld_cg(x + c);
-      const double phi = make_phi<EXACT>(__dsub_rn(ld_cg(P.psi[pb] + pos), ld_cg(P.lam[pb] + pos)), s, xc);
-      const double pr = __dmul_rn(phi, xc);
-      acc = q == 0 ? pr : __dadd_rn(acc, pr);
+__device__ __forceinline__ double control_value(const DevProblem& P, int pb, const double* x, int k) {
+  const int i = P.input_owner[k], l = P.input_local[k];
+  const double s = ld_cg(P.s_row + P.row_start[i] + l);
+  const int D = P.supp_len[i];
+  const int* sc = P.supp_col + static_cast<size_t>(i) * P.d_pad;
+  const int* so = P.supp_off + static_cast<size_t>(i) * P.d_pad;
+  double acc = 0.0;
+  for (int q0 = 0; q0 < D; q0 += kBatch) {
+    double xv[kBatch], pv[kBatch], lv[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      xv[u] = pv[u] = lv[u] = 0.0;
+      if (q0 + u < D) {
+        const int c = sc[q0 + u];
+        const size_t pos = static_cast<size_t>(c) * P.s_pad + so[q0 + u] + l;
+        xv[u] = ld_cg(x + c);
+        pv[u] = ld_cg(P.psi[pb] + pos);
+        lv[u] = ld_cg(P.lam[pb] + pos);
+      }
     }
-    P.u[k] = acc;
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      if (q0 + u < D) {
+        const double phi = make_phi<EXACT>(__dsub_rn(pv[u], lv[u]), s, xv[u]);
+        const double pr = __dmul_rn(phi, xv[u]);
+        acc = q0 + u == 0 ? pr : __dadd_rn(acc, pr);
+      }
+    }
   }
+  return acc;
+}
+
+template <bool EXACT>
+__device__ void control_stage(const DevProblem& P, int pb, const double* x) {
+  for (long long k = spread_first(); k < P.n_inputs; k += spread_step())
+    P.u[k] = control_value<EXACT>(P, pb, x, static_cast<int>(k));
 }
 
 // x+ = A x + B u on the plant's CSR rows (admm.py:363-369: scipy csr_matvec
 // accumulates from 0 in stored order without FMA, then the two vectors add).
+// U(k) supplies input k: P.u after a control stage, or computed in place.
+template <class U>
+__device__ __forceinline__ double plant_row(const DevProblem& P, const double* x, int r, const U& uval) {
+  double ax = 0.0, bu = 0.0;
+  const long long a0 = P.a_ptr[r], a1 = P.a_ptr[r + 1];
+  for (long long q0 = a0; q0 < a1; q0 += kBatch) {
+    double av[kBatch], xv[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      av[u] = xv[u] = 0.0;
+      if (q0 + u < a1) { av[u] = P.a_val[q0 + u]; xv[u] = ld_cg(x + P.a_idx[q0 + u]); }
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (q0 + u < a1) ax = __dadd_rn(ax, __dmul_rn(av[u], xv[u]));
+  }
+  for (long long q = P.b_ptr[r]; q < P.b_ptr[r + 1]; ++q) bu = __dadd_rn(bu, __dmul_rn(P.b_val[q], uval(P.b_idx[q])));
+  return __dadd_rn(ax, bu);
+}
+
 __device__ void plant_stage(const DevProblem& P, const double* x, double* xn) {
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x, GT = gridDim.x * blockDim.x;
-  for (int r = gt; r < P.n_cols; r += GT) {
-    double ax = 0.0, bu = 0.0;
-    for (long long q = P.a_ptr[r]; q < P.a_ptr[r + 1]; ++q)
-      ax = __dadd_rn(ax, __dmul_rn(P.a_val[q], ld_cg(x + P.a_idx[q])));
-    for (long long q = P.b_ptr[r]; q < P.b_ptr[r + 1]; ++q)
-      bu = __dadd_rn(bu, __dmul_rn(P.b_val[q], ld_cg(P.u + P.b_idx[q])));
-    xn[r] = __dadd_rn(ax, bu);
+  for (long long r = spread_first(); r < P.n_cols; r += spread_step())
+    xn[r] = plant_row(P, x, static_cast<int>(r), [&](int k) { return ld_cg(P.u + k); });
+}
+
+// Closed loop, end of an MPC step: control extraction and the plant step in
+// one stage (no grid barrier between them). A state row computes the inputs
+// its B row references itself -- the same arithmetic as control_value, so
+// bitwise the u the input's own thread stores to P.u and the trajectory.
+template <bool EXACT>
+__device__ void control_plant_stage(const DevProblem& P, int pb, const double* x, double* xn, double* inputs_out,
+                                    double* states_out) {
+  for (long long k = spread_first(); k < P.n_inputs; k += spread_step()) {
+    const double u = control_value<EXACT>(P, pb, x, static_cast<int>(k));
+    P.u[k] = u;
+    inputs_out[k] = u;
+  }
+  for (long long r = spread_first(); r < P.n_cols; r += spread_step()) {
+    const double v = plant_row(P, x, static_cast<int>(r), [&](int k) { return control_value<EXACT>(P, pb, x, k); });
+    xn[r] = v;
+    states_out[r] = v;
   }
 }
 
@@ -1850,19 +1919,12 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
       if (step == 0) {
         for (size_t q = gt; q < static_cast<size_t>(P.n_cols); q += GT) R.states[q] = x[q];
       }
-      control_stage<EXACT>(P, b ^ 1, x);
+      double* xn = P.x[(step + 1) & 1];
+      control_plant_stage<EXACT>(P, b ^ 1, x, xn, R.inputs + static_cast<size_t>(step) * P.n_inputs,
+                                 R.states + static_cast<size_t>(step + 1) * P.n_cols);
       PT_LAP(P, 10)
       grid.sync();
       PT_LAP(P, 11)
-      double* xn = P.x[(step + 1) & 1];
-      plant_stage(P, x, xn);
-      for (size_t q = gt; q < static_cast<size_t>(P.n_cols); q += GT)
-        R.states[static_cast<size_t>(step + 1) * P.n_cols + q] = xn[q];
-      for (size_t q = gt; q < static_cast<size_t>(P.n_inputs); q += GT)
-        R.inputs[static_cast<size_t>(step) * P.n_inputs + q] = P.u[q];
-      PT_LAP(P, 12)
-      grid.sync();
-      PT_LAP(P, 13)
     }
   }
   if (leader) { P.ctl[0] = 0; P.ctl[4] = b; }

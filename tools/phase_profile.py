@@ -16,7 +16,7 @@ it = sum(traj.step_iterations)
 CLK_GHZ = float(os.environ.get('DLMPC_CLK_GHZ', '1.965'))   # timers count SM cycles
 raw = sess.device.phase_times(reset=True).astype(np.float64) / (1e3 * CLK_GHZ)
 pt = raw / it   # us per iteration per CTA
-st = raw[:, 8:14] / t_sim   # us per MPC step per CTA
+st = raw[:, 8:12] / t_sim   # us per MPC step per CTA
 names = ["phi", "prologue", "gemm1", "gemm2", "epilogue", "publish", "barrier", "wait"]
 print(f"N={n} {sess.device.info()} iters {it} device {ms:.3f} ms = {1e3*ms/it:.2f} us/iter")
 for k, nm in enumerate(names):
@@ -26,6 +26,6 @@ print(f"  sum(max) {pt[:, :7].max(axis=0).sum():.2f}  per-CTA total max {pt[:, :
 tot = pt[:, :8].sum(axis=1)
 for b in [int(np.argmax(tot)), int(np.argsort(tot)[len(tot) // 2])]:
     print(f"  CTA {b}: " + " ".join(f"{nm}={pt[b, k]:.2f}" for k, nm in enumerate(names)) + f" total={tot[b]:.2f}")
-snames = ["rowdata+bar", "phimeta", "control", "bar", "plant", "bar"]
+snames = ["rowdata+bar", "phimeta", "control+plant", "bar"]
 print("  per MPC step (us): " + " ".join(f"{nm}={st[:, k].max():.2f}" for k, nm in enumerate(snames))
       + f" total={st.sum(axis=1).max():.2f}  (device {1e3 * ms / t_sim:.2f} per step)")
