@@ -115,6 +115,11 @@ int ensure_run_buffers(dlmpc_handle* h, int max_iters, int t_sim) {
 
 int launch(dlmpc_handle* h, const RunArgs& R) {
   KernelFn fn = pick_kernel(h->mode, h->P.tile_cols, h->P.rb_gemv);
+  // the shared-memory limit is a per-function attribute: sessions of one
+  // instantiation with different plans (the ranks of a partitioned solve in
+  // one process) each set their own before launching
+  CUDA_OR_FAIL(h, cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
   DevProblem P = h->P;
   RunArgs Rc = R;
   void* args[] = {&P, &Rc};
@@ -284,7 +289,10 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       const char* nostream = getenv("DLMPC_NO_STREAM");
       const char* forcestream = getenv("DLMPC_FORCE_STREAM");
       const bool stream_pays = (long long)P.n_cols >= 2LL * tc * G || (forcestream && forcestream[0] == '1');
-      if (!(nostream && nostream[0] == '1') && stream_pays && o_lo == 0 && o_hi == P.n_sub) {
+      // (a partitioned sub-problem streams too: patch subsystems whose ball
+      // holds another rank's columns -- no unit here produces their partials
+      // -- recompute the full Φ every iteration, flagged in the patch table)
+      if (!(nostream && nostream[0] == '1') && stream_pays) {
         // ψ/λ staging: TMA bulk copies with smem rows at the global column
         // stride when s_pad % 16 is 4 or 12 (FP64 fragment loads stay conflict
         // free; one copy per chunk and array), else 16-byte cp.async
@@ -332,10 +340,19 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
             for (int i = u_lo[u]; i < u_hi[u]; ++i) unit_of[i] = (int)u;
           part_first.assign(P.n_sub, 0); part_n.assign(P.n_sub, 0); part_off.assign(P.n_sub, 0);
           long long tot = 0;
+          // slots of subsystem i: the units owning a subsystem of its ball
+          // (on a partitioned sub-problem only the owned part of the ball;
+          // subsystems outside every patch get none)
+          std::vector<char> in_patch(P.n_sub, 0);
+          for (size_t u = 0; u < u_lo.size(); ++u)
+            for (int i = p_lo[u]; i < p_hi[u]; ++i) in_patch[i] = 1;
           for (int i = 0; ok && i < P.n_sub; ++i) {
-            const int a = unit_of[bfirst(i)], z = unit_of[blast(i)];
+            part_off[i] = tot;
+            if (!in_patch[i]) continue;
+            const int f = std::max(bfirst(i), o_lo), l = std::min(blast(i), o_hi - 1);
+            const int a = f <= l ? unit_of[f] : -1, z = f <= l ? unit_of[l] : -1;
             ok = a >= 0 && z >= a;
-            part_first[i] = a; part_n[i] = z - a + 1; part_off[i] = tot;
+            part_first[i] = a; part_n[i] = z - a + 1;
             tot += (long long)(z - a + 1) * (pr->row_start[i + 1] - pr->row_start[i]);
           }
           part_total = tot;
@@ -383,6 +400,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
                 reinterpret_cast<long long*>(e)[2] = part_off[i];
                 reinterpret_cast<long long*>(e)[4] = pr->row_start[i];
                 ei[10] = (i >= u_lo[u] && i < u_hi[u]) ? 1 : 0;
+                ei[11] = (bfirst(i) < o_lo || blast(i) >= o_hi) ? 1 : 0;   // full Φ every iteration
                 st_ptab.insert(st_ptab.end(), e, e + 6);
                 ++pt_off;
               }
@@ -925,7 +943,9 @@ int dlmpc_halo_pack(dlmpc_handle* h, double* out) {
 int dlmpc_halo_unpack(dlmpc_handle* h, const double* in) {
   if (!h || (h->n_recv && !in)) return fail(h, DLMPC_BAD_ARGUMENT, "null halo buffer");
   if (!h->n_recv) return DLMPC_OK;
-  h->it_cont = 0;   // halo columns changed under the stream kernel's Φ-dot partials
+  // (the stream kernel's Φ-dot partials stay valid: they hold only owned
+  // columns' contributions, and rows reading halo columns recompute their
+  // full Φ every iteration)
   cudaSetDevice(h->device);
   int ctl[8];
   if (int rc = read_ctl(h, ctl)) return rc;

@@ -1462,6 +1462,22 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
                            (i >= own_lo && i < own_hi) ? P.row_invden + P.row_start[i] : nullptr);
       }
     } else {
+      // partitioned sub-problem: patch subsystems whose ball holds another
+      // rank's columns (flag ei[11]) get the full Φ from the exchanged ψ, λ
+      if (P.own_sub_lo > 0 || P.own_sub_hi < P.n_sub) {
+        for (int q = warp; q < npq; q += kWarps) {
+          const int* ei = reinterpret_cast<const int*>(ptab + 6 * q);
+          if (!ei[11]) continue;
+          const int i = plo + q;
+          double* dst = s_patch + ei[0];
+          double* gdst = ei[10] ? P.s_row + P.row_start[i] : nullptr;
+          auto out = [dst, gdst](int l, double s) {
+            dst[l] = s;
+            if (gdst) gdst[l] = s;
+          };
+          phi_rows_of<false>(P, i, psi, lam, x, out);
+        }
+      }
       // from the per-unit dot partials of the last iteration (slot order);
       // every thread issues the loads of up to kRB rows before using any
       constexpr int kRB = 3;
@@ -1472,7 +1488,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
 #pragma unroll
         for (int u = 0; u < kRB; ++u) {
           const int r = r0 + u * kThreads;
-          ok[u] = r < prows;
+          ok[u] = r < prows && !reinterpret_cast<const int*>(ptab + 6 * rowq[r < prows ? r : 0])[11];
           w[u] = lo[u] = hi[u] = c[u] = ada[u] = 0.0;
           grow[u] = 0; own[u] = false;
           if (ok[u]) {

@@ -66,6 +66,32 @@ def test_partitioned_fast_matches_single_domain_fast():
     assert rel_err(states, one.states) <= 1e-12
 
 
+@pytest.mark.parametrize("name,world", [("c2_loop_seed1", 2), ("c2_loop_seed1", 3), ("d4_loop_n20", 2)])
+def test_partitioned_stream_kernel_against_reference(name, world, monkeypatch):
+    """Rank sub-problems on the stream kernel (forced at this size): patch
+    subsystems whose ball holds another rank's columns recompute their full
+    Φ from the exchanged ψ, λ every iteration, the rest sum the owned units'
+    Φ-dot partials, which persist across the host-driven launches."""
+    from paper_2103_14990_b200 import device
+    g = golden(name)
+    system, spec, mask, t_sim = loop_problem(g)
+    modes = []
+    real = device.DeviceSession
+
+    def spy(*a, **k):
+        sess = real(*a, **k)
+        modes.append(sess.info()["mode"])
+        return sess
+
+    monkeypatch.setattr(device, "DeviceSession", spy)   # RankSolver imports it per rank
+    monkeypatch.setenv("DLMPC_FORCE_STREAM", "1")
+    states, inputs, iters = simulate_partitioned_inprocess(system, spec, mask, g["x0"], t_sim, world, FAST)
+    assert modes == ["stream"] * world
+    assert iters == list(g["step_iters"])
+    assert rel_err(states, g["states"]) <= 1e-9
+    assert rel_err(inputs, g["inputs"]) <= 1e-9
+
+
 @pytest.mark.parametrize("variant", [EXACT, FAST])
 def test_partitioned_generic_graph_against_oracle(variant):
     rng = np.random.default_rng(11)
