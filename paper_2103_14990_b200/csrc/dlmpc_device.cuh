@@ -643,29 +643,32 @@ __device__ __forceinline__ void gemv_pair_rb(int S, const double (&op)[RB_PL][RB
     for (int c = 0; c < RB_AL; ++c) { y0[c] = fma(op[i][c], k0, y0[c]); y1[c] = fma(op[i][c], k1, y1[c]); }
   }
   // reduce-scatter over the p halves: h = 0 keeps column 0, h = 1 column 1
+  // warp partials at [w][c][j][h] (h = the column kept): the 32 lanes store
+  // consecutive doubles (conflict free)
+  constexpr int WP = 2 * 16 * RB_AL;   // doubles per warp
 #pragma unroll
   for (int c = 0; c < RB_AL; ++c) {
     const double keep = h ? y1[c] : y0[c], send = h ? y0[c] : y1[c];
-    ypart[(w * 2 + h) * (16 * RB_AL) + j * RB_AL + c] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    ypart[w * WP + c * 32 + j * 2 + h] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
   }
   __syncthreads();
-  if (tid < 2 * 16 * RB_AL) {   // Y[t][a] = sum over the 16 warps (fixed order)
+  if (tid < WP) {   // Y = sum over the 16 warps (fixed order) -> yb2 [t][c][j]
     double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
 #pragma unroll
     for (int q = 0; q < kWarps; q += 4) {
-      const int t = tid / (16 * RB_AL), a = tid - t * (16 * RB_AL);
-      v0 += ypart[((q + 0) * 2 + t) * (16 * RB_AL) + a];
-      v1 += ypart[((q + 1) * 2 + t) * (16 * RB_AL) + a];
-      v2 += ypart[((q + 2) * 2 + t) * (16 * RB_AL) + a];
-      v3 += ypart[((q + 3) * 2 + t) * (16 * RB_AL) + a];
+      v0 += ypart[(q + 0) * WP + tid];
+      v1 += ypart[(q + 1) * WP + tid];
+      v2 += ypart[(q + 2) * WP + tid];
+      v3 += ypart[(q + 3) * WP + tid];
     }
-    yb2[tid] = (tid / (16 * RB_AL) < nt) ? (v0 + v1) + (v2 + v3) : 0.0;
+    const int c = tid >> 5, jj = (tid & 31) >> 1, t = tid & 1;
+    yb2[t * (16 * RB_AL) + c * 16 + jj] = t < nt ? (v0 + v1) + (v2 + v3) : 0.0;
   }
   __syncthreads();
-  // GEMV 2
+  // GEMV 2 (Y reads: 16 consecutive doubles per half-warp, conflict free)
   double ya[RB_AL], yc[RB_AL];
 #pragma unroll
-  for (int c = 0; c < RB_AL; ++c) { ya[c] = yb2[j * RB_AL + c]; yc[c] = yb2[16 * RB_AL + j * RB_AL + c]; }
+  for (int c = 0; c < RB_AL; ++c) { ya[c] = yb2[c * 16 + j]; yc[c] = yb2[16 * RB_AL + c * 16 + j]; }
   double v[16];
 #pragma unroll
   for (int i = 0; i < RB_PL; ++i) {
