@@ -13,6 +13,9 @@
 //             null-space basis staged in shared memory, the Λ update and the
 //             residual maxima (admm.py:174-217). ONE grid barrier per
 //             iteration, which also publishes the global (pri, dual).
+//  kPatchRb   kPatch whose chunks hold <= 2 columns (C2-sized networks): the
+//             Ψ projection as a register-blocked FP64 GEMV pair (gemv_pair_rb)
+//             instead of DMMA tiles that would be 3/4 empty.
 //  kStream    the same algorithm restructured for large networks (>= 2 chunks
 //             per CTA): Φ dots of the next iteration accumulated by the Ψ
 //             epilogues (per-unit slots, deterministic), ψ/λ staged by TMA
