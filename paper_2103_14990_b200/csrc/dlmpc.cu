@@ -569,6 +569,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           (rc = upload(h, ch_c0.data(), ch_c0.size(), &P.chunk_col0)) ||
           (rc = upload(h, ch_n.data(), ch_n.size(), &P.chunk_n)))
         return rc;
+      if (h->mode == kPatch && (rc = alloc(h, 1, &P.gbar))) return rc;
       if (h->mode == kStream) {
         if ((rc = upload(h, st_cta_gop.data(), st_cta_gop.size(), &P.cta_gop)) ||
             (rc = upload(h, st_unit_desc.data(), st_unit_desc.size(), &P.unit_desc)) ||

@@ -94,6 +94,7 @@ struct DevProblem {
   // mutable device state
   double* psi[2]; double* lam[2]; double* s_row; double* ada; double* x[2]; double* u;
   unsigned long long* resid;   // [2 * cap] residual maxima per iteration (ordered bits)
+  unsigned* gbar;              // patch modes: monotonic grid-barrier arrival counter (never reset)
   int* ctl;                    // 0 status, 1 fail step, 2/3 bad-row slots, 4 cur buffer, 5 fail iters
   unsigned long long* phase_ns;   // [grid * 16] (profiling build only)
   // shared-memory plan (offsets in doubles)
@@ -283,6 +284,45 @@ __device__ __forceinline__ long long spread_first() {
   return static_cast<long long>(threadIdx.x) * gridDim.x + blockIdx.x;
 }
 __device__ __forceinline__ long long spread_step() { return static_cast<long long>(gridDim.x) * blockDim.x; }
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Patch modes: the residual publish fused with the grid barrier. The block
+// reduction's __syncthreads doubles as the barrier's entry; thread 0 posts
+// the CTA's residual maxima, arrives on the launch-wide monotonic counter
+// (release: the CTA's ψ, λ stores, ordered by that __syncthreads, and the
+// two atomics become visible first) and polls it (acquire) until every CTA
+// has arrived `target` times in total (wrap-safe compare). One block barrier
+// less per iteration than publish_residuals + grid.sync(); the grid barrier
+// itself costs ~1.2 us either way on B200 (tools/microbench/barrier_bench.cu).
+__device__ __forceinline__ void publish_barrier(const DevProblem& P, int it, double pri_m, double dual_m,
+                                                double* red, unsigned target) {
+  for (int o = 16; o > 0; o >>= 1) {
+    pri_m = fmax(pri_m, __shfl_xor_sync(0xffffffffu, pri_m, o));
+    dual_m = fmax(dual_m, __shfl_xor_sync(0xffffffffu, dual_m, o));
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { red[2 * warp] = pri_m; red[2 * warp + 1] = dual_m; }
+  __syncthreads();
+  if (warp == 0) {
+    double p = lane < kWarps ? red[2 * lane] : 0.0, d = lane < kWarps ? red[2 * lane + 1] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      p = fmax(p, __shfl_xor_sync(0xffffffffu, p, o));
+      d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    }
+    if (lane == 0) {
+      atomicMax(P.resid + 2 * it, static_cast<unsigned long long>(__double_as_longlong(p)));
+      atomicMax(P.resid + 2 * it + 1, static_cast<unsigned long long>(__double_as_longlong(d)));
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" :: "l"(P.gbar) : "memory");
+      while (static_cast<int>(ld_acquire_u32(P.gbar) - target) < 0) {}
+    }
+  }
+  __syncthreads();
+}
 
 // ||a||^2 per subsystem (reference sls_core.py:338-339: all rows of a
 // subsystem share the support, hence a_pad and a_dot_a) and the RowInfeasible
@@ -1122,7 +1162,7 @@ __device__ __forceinline__ bool patch_stop_test(const DevProblem& P, const RunAr
 
 template <int TC, bool RB>
 __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int it, double* smem,
-                                int& cur, const RunArgs& R) {
+                                int& cur, const RunArgs& R, unsigned bar_target) {
   double* s_patch = smem + P.off_patch;
   long long* m_pos = reinterpret_cast<long long*>(smem + P.off_meta);
   double* m_x = smem + P.off_meta + 3 * TC;
@@ -1193,6 +1233,11 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
         phi_rows_of<false>(P, i, psi, lam, x, out);
     }
     if (!tested && threadIdx.x == 0) { rbc[0] = rp; rbc[1] = rd; }
+    // a unit of one chunk with cached metadata: its staged ψ, λ (issued
+    // before Φ) are waited for here, so this barrier also publishes them and
+    // the chunk needs no barrier of its own
+    const bool one_chunk = P.cache_phi && ch_b - ch_a == 1 && P.stash_bufs > 0;
+    if (one_chunk) cp_async_wait<0>();
     __syncthreads();
     PT_LAP(P, 0)
     if (!tested) {
@@ -1213,27 +1258,29 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
       const int c0 = ch == ch_a ? c00 : P.chunk_col0[ch];
       const int nt = ch == ch_a ? nt0 : P.chunk_n[ch];
       const int sb = P.stash_bufs == 2 ? ((ch - ch_a) & 1) : 0;
-      if (P.stash_bufs == 2 && ch + 1 < ch_b) {
-        stash_issue(P, P.chunk_col0[ch + 1], P.chunk_n[ch + 1], P.class_s[P.chunk_class[ch + 1]], psi, lam,
-                    stash + (sb ^ 1) * stash_stride);
-        cp_async_wait<1>();
-      } else if (P.stash_bufs > 0) {
-        cp_async_wait<0>();
-      }
-      if (!meta_cached && threadIdx.x < TC) {
-        const int t = threadIdx.x;
-        long long pos = 0, s0 = 0, q0 = 0;
-        double xc = 0.0;
-        if (t < nt) {
-          const int c = c0 + t;
-          pos = static_cast<long long>(c) * P.s_pad;
-          s0 = P.col_rowbase[c] - prow0;
-          q0 = static_cast<long long>(P.col_vec[c]) * P.s_pad;
-          xc = ld_cg(x + c);
+      if (!one_chunk) {
+        if (P.stash_bufs == 2 && ch + 1 < ch_b) {
+          stash_issue(P, P.chunk_col0[ch + 1], P.chunk_n[ch + 1], P.class_s[P.chunk_class[ch + 1]], psi, lam,
+                      stash + (sb ^ 1) * stash_stride);
+          cp_async_wait<1>();
+        } else if (P.stash_bufs > 0) {
+          cp_async_wait<0>();
         }
-        m_pos[t] = pos; m_pos[TC + t] = s0; m_pos[2 * TC + t] = q0; m_x[t] = xc;
+        if (!meta_cached && threadIdx.x < TC) {
+          const int t = threadIdx.x;
+          long long pos = 0, s0 = 0, q0 = 0;
+          double xc = 0.0;
+          if (t < nt) {
+            const int c = c0 + t;
+            pos = static_cast<long long>(c) * P.s_pad;
+            s0 = P.col_rowbase[c] - prow0;
+            q0 = static_cast<long long>(P.col_vec[c]) * P.s_pad;
+            xc = ld_cg(x + c);
+          }
+          m_pos[t] = pos; m_pos[TC + t] = s0; m_pos[2 * TC + t] = q0; m_x[t] = xc;
+        }
+        __syncthreads();
       }
-      __syncthreads();
       if (RB)
         rb_chunk<TC>(P, k, nt, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, smem, cur, pri_m, dual_m,
                      stash + sb * stash_stride);
@@ -1245,7 +1292,7 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
     }
   }
   PT_START
-  publish_residuals(P, it, pri_m, dual_m, smem + P.off_red);
+  publish_barrier(P, it, pri_m, dual_m, smem + P.off_red, bar_target);
   PT_LAP(P, 5)
   return false;
 }
@@ -1857,6 +1904,10 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
     __syncthreads();
   }
   const size_t gt = blockIdx.x * blockDim.x + tid, GT = gridDim.x * blockDim.x;
+  // patch modes: the iteration barrier's counter value at launch (stable: the
+  // previous launch has ended, and no CTA arrives before the first grid.sync)
+  const unsigned bar_base = (PATCH && tid == 0) ? ld_acquire_u32(P.gbar) : 0u;
+  unsigned bar_epoch = 0;
   for (int step = 0; step < R.t_sim; ++step) {
     PT_DECL
     PT_START
@@ -1892,10 +1943,12 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
           }
           break;
         }
-        if (patch_iteration<TC, MODE == kPatchRb>(P, b, x, it, smem, cur, R)) { conv = true; break; }
-        PT_START
-        grid.sync();
-        PT_LAP(P, 6)
+        bar_epoch += gridDim.x;
+        if (patch_iteration<TC, MODE == kPatchRb>(P, b, x, it, smem, cur, R, bar_base + bar_epoch)) {
+          bar_epoch -= gridDim.x;   // returned before arriving
+          conv = true;
+          break;
+        }
         b ^= 1;
         ++it;
       }
