@@ -1281,7 +1281,7 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
         }
         __syncthreads();
       }
-      if (RB)
+      if constexpr (RB)
         rb_chunk<TC>(P, k, nt, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, smem, cur, pri_m, dual_m,
                      stash + sb * stash_stride);
       else

@@ -41,5 +41,10 @@ for world in worlds:
     print(f"N={n} world={world} setup {setup:.1f}s modes {sorted(set(modes))} "
           f"rank-max {1e3 * steady.mean(axis=1).max():.1f} us/iter, rank-mean {1e3 * steady.mean():.1f} us/iter, "
           f"halo send max {8 * max(rk.send_doubles for rk in ranks) / 1e3:.1f} KB/iter", flush=True)
+    if True:   # per-rank detail
+        for r, rk in enumerate(ranks):
+            i = rk.session.info()
+            print(f"   rank {r}: own {rk.plan.own} {1e3 * steady[r].mean():.1f} us/iter units {i['units']} "
+                  f"smem {i['smem_bytes']} n_sub {i['n_sub']}", flush=True)
     for rk in ranks:
         rk.close()
