@@ -724,7 +724,7 @@ int dlmpc_set_x(dlmpc_handle* h, const double* x, int64_t* bad_row) {
   cudaSetDevice(h->device);
   CUDA_OR_FAIL(h, cudaMemcpyAsync(h->P.x[0], x, sizeof(double) * h->P.n_cols, cudaMemcpyHostToDevice, h->stream));
   CUDA_OR_FAIL(h, cudaMemsetAsync(h->P.ctl + 2, 0x7f, sizeof(int), h->stream));
-  set_x_kernel<<<(h->P.n_sub + 255) / 256, 256, 0, h->stream>>>(h->P);
+  set_x_kernel<<<std::max(1, std::min(h->sm_count * 8, (h->P.n_sub + 7) / 8)), 256, 0, h->stream>>>(h->P);   // a warp per subsystem
   CUDA_OR_FAIL(h, cudaGetLastError());
   int ctl[8];
   if (int rc = read_ctl(h, ctl)) return rc;
@@ -966,7 +966,7 @@ int dlmpc_finish_step(dlmpc_handle* h, double* u_out, double* x_next_out) {
   int ctl[8];
   if (int rc = read_ctl(h, ctl)) return rc;
   const int pb = ctl[4] ^ 1;
-  const int blocks = std::max(1, std::min(h->sm_count * 4, (std::max(h->P.n_cols, h->P.n_inputs) + 255) / 256));
+  const int blocks = std::max(1, std::min(h->sm_count * 8, (std::max(h->P.n_cols, h->P.n_inputs) + 7) / 8));   // a warp per item
   if (h->P.exact) control_kernel<true><<<blocks, 256, 0, h->stream>>>(h->P, pb);
   else control_kernel<false><<<blocks, 256, 0, h->stream>>>(h->P, pb);
   CUDA_OR_FAIL(h, cudaGetLastError());

@@ -272,19 +272,6 @@ __device__ __forceinline__ void publish_residuals(const DevProblem& P, int it, d
   }
 }
 
-// Per-MPC-step stages run a few hundred latency-bound items (subsystems,
-// inputs, states): item q goes to CTA q % grid first, so they run one or two
-// per SM, and each item issues its loads in batches of kBatch before the
-// ordered arithmetic (the reference's summation order is kept).
-#ifndef DLMPC_KBATCH
-#define DLMPC_KBATCH 4   // 8 measured 30% slower on C2: the patch kernel sits at the 128-register cap
-#endif
-constexpr int kBatch = DLMPC_KBATCH;
-__device__ __forceinline__ long long spread_first() {
-  return static_cast<long long>(threadIdx.x) * gridDim.x + blockIdx.x;
-}
-__device__ __forceinline__ long long spread_step() { return static_cast<long long>(gridDim.x) * blockDim.x; }
-
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
@@ -324,31 +311,50 @@ __device__ __forceinline__ void publish_barrier(const DevProblem& P, int it, dou
   __syncthreads();
 }
 
+// Per-MPC-step stages run a few hundred latency-bound items (subsystems,
+// inputs, state rows), one warp per item: the lanes load an item's operands
+// at once (one round trip), then the products are summed across the lanes in
+// the reference's sequential order (warp_ordered_sum). Item q goes to CTA
+// q % grid first, so the items spread over the SMs.
+__device__ __forceinline__ long long wspread_first() {
+  return static_cast<long long>(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+}
+__device__ __forceinline__ long long wspread_step() { return static_cast<long long>(gridDim.x) * (blockDim.x >> 5); }
+
+// acc (+)= v_0 + v_1 + ... + v_{n-1} over lanes 0..n-1, strictly in that
+// order with IEEE adds; `first`: acc is not yet set (the reference starts
+// from the first product, not from 0). Result in every lane.
+__device__ __forceinline__ double warp_ordered_sum(double acc, bool& first, double v, int n) {
+  for (int q = 0; q < n; ++q) {
+    const double t = __shfl_sync(0xffffffffu, v, q);
+    acc = first ? t : __dadd_rn(acc, t);
+    first = false;
+  }
+  return acc;
+}
+
 // ||a||^2 per subsystem (reference sls_core.py:338-339: all rows of a
 // subsystem share the support, hence a_pad and a_dot_a) and the RowInfeasible
 // scan of sls_core.py:346-348. Strict ascending order, no FMA, in all modes.
 __device__ void row_data_stage(const DevProblem& P, const double* x, int* bad_slot) {
-  for (long long ii = spread_first(); ii < P.n_sub; ii += spread_step()) {
+  const int lane = threadIdx.x & 31;
+  for (long long ii = wspread_first(); ii < P.n_sub; ii += wspread_step()) {
     const int i = static_cast<int>(ii);
     const int D = P.supp_len[i];
     const int* sc = P.supp_col + static_cast<size_t>(i) * P.d_pad;
     double acc = 0.0;
-    for (int k0 = 0; k0 < D; k0 += kBatch) {
-      double xv[kBatch];
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) xv[u] = k0 + u < D ? ld_cg(x + sc[k0 + u]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        if (k0 + u < D) {
-          const double pr = __dmul_rn(xv[u], xv[u]);
-          acc = k0 + u == 0 ? pr : __dadd_rn(acc, pr);
-        }
-      }
+    bool first = true;
+    for (int k0 = 0; k0 < D; k0 += 32) {
+      const int kn = min(32, D - k0);
+      const double xc = lane < kn ? ld_cg(x + sc[k0 + lane]) : 0.0;
+      acc = warp_ordered_sum(acc, first, __dmul_rn(xc, xc), kn);
     }
     if (D < P.d_row) acc = __dadd_rn(acc, 0.0);   // the padded slots of a_pad
-    P.ada[i] = acc;
-    if (acc == 0.0 && P.sub_first_bad[i] >= 0 && i >= P.own_sub_lo && i < P.own_sub_hi)
-      atomicMin(bad_slot, P.sub_first_bad[i]);
+    if (lane == 0) {
+      P.ada[i] = acc;
+      if (acc == 0.0 && P.sub_first_bad[i] >= 0 && i >= P.own_sub_lo && i < P.own_sub_hi)
+        atomicMin(bad_slot, P.sub_first_bad[i]);
+    }
   }
 }
 
@@ -1795,89 +1801,85 @@ __device__ void column_stage_exact(const DevProblem& P, int b, const double* x, 
 }
 
 // u_k = ascending dot of φ_r[input row k, t=0] with x (admm.py:350-360);
-// φ is rebuilt from the iterate the last Φ stage read (buffer pb).
+// φ is rebuilt from the iterate the last Φ stage read (buffer pb). One warp;
+// the result in every lane.
 template <bool EXACT>
 __device__ __forceinline__ double control_value(const DevProblem& P, int pb, const double* x, int k) {
+  const int lane = threadIdx.x & 31;
   const int i = P.input_owner[k], l = P.input_local[k];
   const double s = ld_cg(P.s_row + P.row_start[i] + l);
   const int D = P.supp_len[i];
   const int* sc = P.supp_col + static_cast<size_t>(i) * P.d_pad;
   const int* so = P.supp_off + static_cast<size_t>(i) * P.d_pad;
   double acc = 0.0;
-  for (int q0 = 0; q0 < D; q0 += kBatch) {
-    double xv[kBatch], pv[kBatch], lv[kBatch];
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      xv[u] = pv[u] = lv[u] = 0.0;
-      if (q0 + u < D) {
-        const int c = sc[q0 + u];
-        const size_t pos = static_cast<size_t>(c) * P.s_pad + so[q0 + u] + l;
-        xv[u] = ld_cg(x + c);
-        pv[u] = ld_cg(P.psi[pb] + pos);
-        lv[u] = ld_cg(P.lam[pb] + pos);
-      }
+  bool first = true;
+  for (int q0 = 0; q0 < D; q0 += 32) {
+    const int kn = min(32, D - q0);
+    double pr = 0.0;
+    if (lane < kn) {
+      const int c = sc[q0 + lane];
+      const size_t pos = static_cast<size_t>(c) * P.s_pad + so[q0 + lane] + l;
+      const double xc = ld_cg(x + c);
+      const double phi = make_phi<EXACT>(__dsub_rn(ld_cg(P.psi[pb] + pos), ld_cg(P.lam[pb] + pos)), s, xc);
+      pr = __dmul_rn(phi, xc);
     }
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      if (q0 + u < D) {
-        const double phi = make_phi<EXACT>(__dsub_rn(pv[u], lv[u]), s, xv[u]);
-        const double pr = __dmul_rn(phi, xv[u]);
-        acc = q0 + u == 0 ? pr : __dadd_rn(acc, pr);
-      }
-    }
+    acc = warp_ordered_sum(acc, first, pr, kn);
   }
   return acc;
 }
 
 template <bool EXACT>
 __device__ void control_stage(const DevProblem& P, int pb, const double* x) {
-  for (long long k = spread_first(); k < P.n_inputs; k += spread_step())
-    P.u[k] = control_value<EXACT>(P, pb, x, static_cast<int>(k));
+  for (long long k = wspread_first(); k < P.n_inputs; k += wspread_step()) {
+    const double u = control_value<EXACT>(P, pb, x, static_cast<int>(k));
+    if ((threadIdx.x & 31) == 0) P.u[k] = u;
+  }
 }
 
 // x+ = A x + B u on the plant's CSR rows (admm.py:363-369: scipy csr_matvec
 // accumulates from 0 in stored order without FMA, then the two vectors add).
-// U(k) supplies input k: P.u after a control stage, or computed in place.
+// U(k) supplies input k (warp-uniform): P.u after a control stage, or
+// computed in place. One warp; the result in every lane.
 template <class U>
 __device__ __forceinline__ double plant_row(const DevProblem& P, const double* x, int r, const U& uval) {
+  const int lane = threadIdx.x & 31;
   double ax = 0.0, bu = 0.0;
+  bool first = false;   // csr_matvec starts from 0
   const long long a0 = P.a_ptr[r], a1 = P.a_ptr[r + 1];
-  for (long long q0 = a0; q0 < a1; q0 += kBatch) {
-    double av[kBatch], xv[kBatch];
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      av[u] = xv[u] = 0.0;
-      if (q0 + u < a1) { av[u] = P.a_val[q0 + u]; xv[u] = ld_cg(x + P.a_idx[q0 + u]); }
-    }
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u)
-      if (q0 + u < a1) ax = __dadd_rn(ax, __dmul_rn(av[u], xv[u]));
+  for (long long q0 = a0; q0 < a1; q0 += 32) {
+    const int kn = static_cast<int>(min(32LL, a1 - q0));
+    const double pr = lane < kn ? __dmul_rn(P.a_val[q0 + lane], ld_cg(x + P.a_idx[q0 + lane])) : 0.0;
+    ax = warp_ordered_sum(ax, first, pr, kn);
   }
   for (long long q = P.b_ptr[r]; q < P.b_ptr[r + 1]; ++q) bu = __dadd_rn(bu, __dmul_rn(P.b_val[q], uval(P.b_idx[q])));
   return __dadd_rn(ax, bu);
 }
 
 __device__ void plant_stage(const DevProblem& P, const double* x, double* xn) {
-  for (long long r = spread_first(); r < P.n_cols; r += spread_step())
-    xn[r] = plant_row(P, x, static_cast<int>(r), [&](int k) { return ld_cg(P.u + k); });
+  for (long long r = wspread_first(); r < P.n_cols; r += wspread_step()) {
+    const double v = plant_row(P, x, static_cast<int>(r), [&](int k) { return ld_cg(P.u + k); });
+    if ((threadIdx.x & 31) == 0) xn[r] = v;
+  }
 }
 
 // Closed loop, end of an MPC step: control extraction and the plant step in
 // one stage (no grid barrier between them). A state row computes the inputs
 // its B row references itself -- the same arithmetic as control_value, so
-// bitwise the u the input's own thread stores to P.u and the trajectory.
+// bitwise the u the input's own warp stores to P.u and the trajectory.
 template <bool EXACT>
 __device__ void control_plant_stage(const DevProblem& P, int pb, const double* x, double* xn, double* inputs_out,
                                     double* states_out) {
-  for (long long k = spread_first(); k < P.n_inputs; k += spread_step()) {
-    const double u = control_value<EXACT>(P, pb, x, static_cast<int>(k));
-    P.u[k] = u;
-    inputs_out[k] = u;
-  }
-  for (long long r = spread_first(); r < P.n_cols; r += spread_step()) {
-    const double v = plant_row(P, x, static_cast<int>(r), [&](int k) { return control_value<EXACT>(P, pb, x, k); });
-    xn[r] = v;
-    states_out[r] = v;
+  const long long n_items = static_cast<long long>(P.n_inputs) + P.n_cols;
+  const bool lane0 = (threadIdx.x & 31) == 0;
+  for (long long w = wspread_first(); w < n_items; w += wspread_step()) {
+    if (w < P.n_inputs) {
+      const double u = control_value<EXACT>(P, pb, x, static_cast<int>(w));
+      if (lane0) { P.u[w] = u; inputs_out[w] = u; }
+    } else {
+      const long long r = w - P.n_inputs;
+      const double v = plant_row(P, x, static_cast<int>(r), [&](int k) { return control_value<EXACT>(P, pb, x, k); });
+      if (lane0) { xn[r] = v; states_out[r] = v; }
+    }
   }
 }
 
