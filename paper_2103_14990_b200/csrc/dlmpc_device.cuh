@@ -1043,10 +1043,15 @@ __device__ void column_stage_tiles(const DevProblem& P, int b, const double* x, 
 // iteration's control path touches no global memory.
 // ublk: has_unit, own_lo, own_hi, plo, phi, prows, prow0 (2 ints), ch_a, ch_b,
 //       k, c0, nt, S of the first chunk, own-row offset in the patch, own rows
+// `full` (first MPC step of a launch): also the step-invariant part (support
+// positions and lengths, row bounds, unit block, row info, the single
+// chunk's column positions); later steps refresh only what depends on x
+// (x of the supports and of the chunk's columns, 1/||a||², 1/(ρ + 2w·||a||²)).
 template <int TC>
-__device__ void cache_phi_meta(const DevProblem& P, const double* x, double* smem) {
+__device__ void cache_phi_meta(const DevProblem& P, const double* x, double* smem, bool full) {
   const int un0 = P.cta_unit_ptr[blockIdx.x];
   if (un0 == P.cta_unit_ptr[blockIdx.x + 1]) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int plo = P.unit_patch_lo[un0], phi_ = P.unit_patch_hi[un0];
   const int np = phi_ - plo;
   const long long prow0 = P.row_start[plo];
@@ -1057,57 +1062,65 @@ __device__ void cache_phi_meta(const DevProblem& P, const double* x, double* sme
   double* ada = xk + static_cast<size_t>(np) * P.d_pad;
   double* rw = ada + np;
   int* len = reinterpret_cast<int*>(rw + 3 * prows);
-  for (int q = threadIdx.x; q < np * P.d_pad; q += kThreads) {
-    const int i = plo + q / P.d_pad, k = q % P.d_pad;
-    if (k < P.supp_len[i]) {
-      const size_t e = static_cast<size_t>(i) * P.d_pad + k;
-      const int c = P.supp_col[e];
-      bk[q] = static_cast<long long>(c) * P.s_pad + P.supp_off[e];
-      xk[q] = ld_cg(x + c);
-    }
-  }
-  for (int q = threadIdx.x; q < np; q += kThreads) {
-    const double a = ld_cg(P.ada + plo + q);
-    ada[q] = a > 0.0 ? 1.0 / a : 0.0;
-    len[q] = P.supp_len[plo + q];
-  }
-  for (int q = threadIdx.x; q < prows; q += kThreads) {
-    int i = plo;
-    while (P.row_start[i + 1] <= prow0 + q) ++i;
-    const double a = ld_cg(P.ada + i);
-    rw[q] = 1.0 / (P.rho + 2.0 * P.row_w[prow0 + q] * a);
-    rw[prows + q] = P.row_lo[prow0 + q]; rw[2 * prows + q] = P.row_hi[prow0 + q];
-  }
   int* ublk = reinterpret_cast<int*>(smem + P.off_ublk);
   int2* rinfo = reinterpret_cast<int2*>(smem + P.off_ublk + 8);
-  for (int q = threadIdx.x; q < np; q += kThreads)
-    rinfo[q] = make_int2(static_cast<int>(P.row_start[plo + q] - prow0),
-                         static_cast<int>(P.row_start[plo + q + 1] - P.row_start[plo + q]));
-  const int own_lo = P.unit_sub_lo[un0], own_hi = P.unit_sub_hi[un0];
   const int ch_a = P.unit_chunk_ptr[un0], ch_b = P.unit_chunk_ptr[un0 + 1];
-  if (threadIdx.x == 0) {
-    ublk[0] = 1; ublk[1] = own_lo; ublk[2] = own_hi; ublk[3] = plo; ublk[4] = phi_; ublk[5] = prows;
-    ublk[6] = static_cast<int>(prow0 & 0xffffffffLL); ublk[7] = static_cast<int>(prow0 >> 32);
-    ublk[8] = ch_a; ublk[9] = ch_b;
-    const int k = P.chunk_class[ch_a];
-    ublk[10] = k; ublk[11] = P.chunk_col0[ch_a]; ublk[12] = P.chunk_n[ch_a]; ublk[13] = P.class_s[k];
-    ublk[14] = static_cast<int>(P.row_start[own_lo] - prow0);
-    ublk[15] = static_cast<int>(P.row_start[own_hi] - P.row_start[own_lo]);
-  }
-  if (ch_b - ch_a == 1 && threadIdx.x < TC) {   // the single chunk's column metadata
-    long long* m_pos = reinterpret_cast<long long*>(smem + P.off_meta);
-    double* m_x = smem + P.off_meta + 3 * TC;
-    const int t = threadIdx.x, c0 = P.chunk_col0[ch_a], nt = P.chunk_n[ch_a];
-    long long pos = 0, s0 = 0, q0 = 0;
-    double xc = 0.0;
-    if (t < nt) {
-      const int c = c0 + t;
-      pos = static_cast<long long>(c) * P.s_pad;
-      s0 = P.col_rowbase[c] - prow0;
-      q0 = static_cast<long long>(P.col_vec[c]) * P.s_pad;
-      xc = ld_cg(x + c);
+  const bool one_chunk = ch_b - ch_a == 1;
+  long long* m_pos = reinterpret_cast<long long*>(smem + P.off_meta);
+  double* m_x = smem + P.off_meta + 3 * TC;
+  if (full) {
+    for (int q = threadIdx.x; q < np * P.d_pad; q += kThreads) {
+      const int i = plo + q / P.d_pad, k = q % P.d_pad;
+      if (k < P.supp_len[i]) {
+        const size_t e = static_cast<size_t>(i) * P.d_pad + k;
+        bk[q] = static_cast<long long>(P.supp_col[e]) * P.s_pad + P.supp_off[e];
+      }
     }
-    m_pos[t] = pos; m_pos[TC + t] = s0; m_pos[2 * TC + t] = q0; m_x[t] = xc;
+    for (int q = threadIdx.x; q < np; q += kThreads) {
+      len[q] = P.supp_len[plo + q];
+      rinfo[q] = make_int2(static_cast<int>(P.row_start[plo + q] - prow0),
+                           static_cast<int>(P.row_start[plo + q + 1] - P.row_start[plo + q]));
+    }
+    for (int q = threadIdx.x; q < prows; q += kThreads) {
+      rw[prows + q] = P.row_lo[prow0 + q]; rw[2 * prows + q] = P.row_hi[prow0 + q];
+    }
+    const int own_lo = P.unit_sub_lo[un0], own_hi = P.unit_sub_hi[un0];
+    if (threadIdx.x == 0) {
+      ublk[0] = 1; ublk[1] = own_lo; ublk[2] = own_hi; ublk[3] = plo; ublk[4] = phi_; ublk[5] = prows;
+      ublk[6] = static_cast<int>(prow0 & 0xffffffffLL); ublk[7] = static_cast<int>(prow0 >> 32);
+      ublk[8] = ch_a; ublk[9] = ch_b;
+      const int k = P.chunk_class[ch_a];
+      ublk[10] = k; ublk[11] = P.chunk_col0[ch_a]; ublk[12] = P.chunk_n[ch_a]; ublk[13] = P.class_s[k];
+      ublk[14] = static_cast<int>(P.row_start[own_lo] - prow0);
+      ublk[15] = static_cast<int>(P.row_start[own_hi] - P.row_start[own_lo]);
+    }
+    if (one_chunk && threadIdx.x < TC) {   // the single chunk's column metadata
+      const int t = threadIdx.x, c0 = P.chunk_col0[ch_a], nt = P.chunk_n[ch_a];
+      long long pos = 0, s0 = 0, q0 = 0;
+      if (t < nt) {
+        const int c = c0 + t;
+        pos = static_cast<long long>(c) * P.s_pad;
+        s0 = P.col_rowbase[c] - prow0;
+        q0 = static_cast<long long>(P.col_vec[c]) * P.s_pad;
+      }
+      m_pos[t] = pos; m_pos[TC + t] = s0; m_pos[2 * TC + t] = q0;
+    }
+    __syncthreads();
+  }
+  // x-dependent part (every MPC step); a warp per patch subsystem
+  for (int q = warp; q < np; q += kWarps) {
+    const int i = plo + q;
+    const int D = len[q];
+    for (int k = lane; k < D; k += 32) xk[q * P.d_pad + k] = ld_cg(x + P.supp_col[static_cast<size_t>(i) * P.d_pad + k]);
+    const double a = ld_cg(P.ada + i);
+    if (lane == 0) ada[q] = a > 0.0 ? 1.0 / a : 0.0;
+    const int2 ri = rinfo[q];
+    for (int l = lane; l < ri.y; l += 32)
+      rw[ri.x + l] = 1.0 / (P.rho + 2.0 * P.row_w[prow0 + ri.x + l] * a);
+  }
+  if (one_chunk && threadIdx.x < TC) {
+    const int t = threadIdx.x;
+    m_x[t] = t < P.chunk_n[ch_a] ? ld_cg(x + P.chunk_col0[ch_a] + t) : 0.0;
   }
   __syncthreads();
 }
@@ -1930,7 +1943,7 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
       if (leader) P.ctl[2 + ((step + 1) & 1)] = kBadNone;
     }
     PT_LAP(P, 8)
-    if (PATCH && P.cache_phi) cache_phi_meta<TC>(P, x, smem);
+    if (PATCH && P.cache_phi) cache_phi_meta<TC>(P, x, smem, step == 0);
     PT_LAP(P, 9)
     int it = 0;
     bool conv = false;
