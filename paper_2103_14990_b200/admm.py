@@ -234,6 +234,25 @@ def verify_fixed_point(triple: PhiTriple, row_data: RowData, operator, spec: Pro
 # closed loop
 # ---------------------------------------------------------------------------
 
+_SPEC_ARRAYS = ("state_weights", "input_weights", "terminal_weights", "state_lo", "state_hi", "input_lo",
+                "input_hi")
+
+
+def _spec_arrays(spec: ProblemSpec):
+    """Copies of the spec's arrays and scalars a cached session was built for."""
+    return ([np.array(getattr(spec, n), dtype=np.float64, copy=True) for n in _SPEC_ARRAYS],
+            (spec.horizon, spec.rho))
+
+
+def _spec_unchanged(sess, spec: ProblemSpec) -> bool:
+    """The cached session still matches `spec` (an in-place edit of its arrays
+    invalidates it); array comparisons instead of re-hashing on every call."""
+    arrays, scalars = sess._spec_arrays
+    if scalars != (spec.horizon, spec.rho):
+        return False
+    return all(np.array_equal(a, getattr(spec, n)) for a, n in zip(arrays, _SPEC_ARRAYS))
+
+
 def _spec_fingerprint(spec: ProblemSpec) -> bytes:
     h = hashlib.blake2b(digest_size=16)
     for name in ("state_weights", "input_weights", "terminal_weights", "state_lo",
@@ -262,6 +281,7 @@ class DlmpcSession:
         self.device = DeviceSession(self.layout, strat.device)
         self.precompute_s = time.perf_counter() - t0
         self._fp = _spec_fingerprint(spec)
+        self._spec_arrays = _spec_arrays(spec)
 
     def simulate(self, x0, t_sim: int, warm_start: bool = True):
         """Closed loop on device; returns (Trajectory, device_ms)."""
@@ -305,7 +325,7 @@ def _cached_session(system, spec, mask, strat):
     if hit is not None:
         ref_sys, ref_spec, ref_mask, sess = hit
         if ref_sys() is system and ref_spec() is spec and ref_mask() is mask \
-                and sess._fp == _spec_fingerprint(spec):
+                and _spec_unchanged(sess, spec):
             return sess, True
         sess.close()
         del _SESSIONS[key]

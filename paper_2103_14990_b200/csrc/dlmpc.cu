@@ -39,6 +39,7 @@ struct dlmpc_handle {
   int64_t* d_send_cells = nullptr; int64_t n_send = 0;
   int64_t* d_recv_cells = nullptr; int64_t n_recv = 0;
   double* d_halo = nullptr;
+  char* h_stage = nullptr; size_t stage_cap = 0;   // pinned staging of dlmpc_simulate's host copies
 };
 
 namespace {
@@ -709,6 +710,7 @@ void dlmpc_destroy(dlmpc_handle* h) {
   if (h->d_recv_cells) cudaFree(h->d_recv_cells);
   if (h->d_halo) cudaFree(h->d_halo);
   if (h->P.resid) cudaFree(h->P.resid);
+  if (h->h_stage) cudaFreeHost(h->h_stage);
   if (h->d_step_iters) cudaFree(h->d_step_iters);
   if (h->d_states) cudaFree(h->d_states);
   if (h->d_inputs) cudaFree(h->d_inputs);
@@ -796,21 +798,38 @@ int dlmpc_simulate(dlmpc_handle* h, const double* x0, int t_sim, int warm_start,
   if (!h || !x0 || t_sim < 1) return fail(h, DLMPC_BAD_ARGUMENT, "bad argument");
   cudaSetDevice(h->device);
   if (int rc = ensure_run_buffers(h, max_iters, t_sim)) return rc;
-  CUDA_OR_FAIL(h, cudaMemcpyAsync(h->d_states, x0, sizeof(double) * h->P.n_cols, cudaMemcpyHostToDevice, h->stream));
+  // pinned staging: x0 in, then status, iteration counts, trajectory out in
+  // one batch of async copies and a single stream synchronisation
+  const size_t nc = (size_t)h->P.n_cols, ni = (size_t)h->P.n_inputs;
+  const size_t o_ctl = nc * 8, o_it = o_ctl + 64, o_st = o_it + (((size_t)t_sim * 4 + 15) & ~(size_t)15);
+  const size_t o_in = o_st + (size_t)(t_sim + 1) * nc * 8, need = o_in + (size_t)t_sim * ni * 8 + 8;
+  if (need > h->stage_cap) {
+    if (h->h_stage) cudaFreeHost(h->h_stage);
+    h->h_stage = nullptr; h->stage_cap = 0;
+    CUDA_OR_FAIL(h, cudaMallocHost(reinterpret_cast<void**>(&h->h_stage), need));
+    h->stage_cap = need;
+  }
+  char* hs = h->h_stage;
+  std::memcpy(hs, x0, nc * 8);
+  CUDA_OR_FAIL(h, cudaMemcpyAsync(h->d_states, hs, nc * 8, cudaMemcpyHostToDevice, h->stream));
   if (int rc = dlmpc_simulate_device(h, h->d_states, t_sim, warm_start, cold_start, max_iters, eps_pri, eps_dual,
                                      nullptr, nullptr, nullptr, nullptr)) return rc;
-  if (int rc = finish_timing(h)) return rc;
+  CUDA_OR_FAIL(h, cudaMemcpyAsync(hs + o_ctl, h->P.ctl, sizeof(int) * 8, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_OR_FAIL(h, cudaMemcpyAsync(hs + o_it, h->d_step_iters, sizeof(int) * t_sim, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_OR_FAIL(h, cudaMemcpyAsync(hs + o_st, h->d_states, (size_t)(t_sim + 1) * nc * 8, cudaMemcpyDeviceToHost, h->stream));
+  if (ni) CUDA_OR_FAIL(h, cudaMemcpyAsync(hs + o_in, h->d_inputs, (size_t)t_sim * ni * 8, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  CUDA_OR_FAIL(h, cudaEventElapsedTime(&h->last_ms, h->ev0, h->ev1));
   int ctl[8];
-  if (int rc = read_ctl(h, ctl)) return rc;
+  std::memcpy(ctl, hs + o_ctl, sizeof(ctl));
   int done = t_sim;
   if (ctl[0] != DLMPC_OK) done = ctl[1];
   if (fail_step) *fail_step = ctl[0] == DLMPC_OK ? -1 : ctl[1];
   if (bad_row) *bad_row = ctl[0] == DLMPC_ROW_INFEASIBLE ? ctl[2 + (ctl[1] & 1)] : -1;
   if (fail_iters) *fail_iters = ctl[0] == DLMPC_NOT_CONVERGED ? ctl[5] : 0;
-  if (states) CUDA_OR_FAIL(h, cudaMemcpy(states, h->d_states, sizeof(double) * (size_t)(done + 1) * h->P.n_cols, cudaMemcpyDeviceToHost));
-  if (inputs && done > 0 && h->P.n_inputs > 0)
-    CUDA_OR_FAIL(h, cudaMemcpy(inputs, h->d_inputs, sizeof(double) * (size_t)done * h->P.n_inputs, cudaMemcpyDeviceToHost));
-  if (step_iters && done > 0) CUDA_OR_FAIL(h, cudaMemcpy(step_iters, h->d_step_iters, sizeof(int) * done, cudaMemcpyDeviceToHost));
+  if (states) std::memcpy(states, hs + o_st, (size_t)(done + 1) * nc * 8);
+  if (inputs && done > 0 && ni) std::memcpy(inputs, hs + o_in, (size_t)done * ni * 8);
+  if (step_iters && done > 0) std::memcpy(step_iters, hs + o_it, sizeof(int) * done);
   if (fail_hist && ctl[0] == DLMPC_NOT_CONVERGED && ctl[5] > 0)
     CUDA_OR_FAIL(h, cudaMemcpy(fail_hist, h->d_hist, sizeof(double) * 2 * ctl[5], cudaMemcpyDeviceToHost));
   return ctl[0];
