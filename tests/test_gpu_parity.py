@@ -76,6 +76,28 @@ def test_closed_loops_against_reference(name, variant):
     assert rep.ledger.solve_launches == 1
 
 
+@pytest.mark.parametrize("name", ["c1_loop_seed1", "c2_loop_seed1"])
+def test_patch_schedules_against_reference(name, monkeypatch):
+    """The patch kernel's two Ψ schedules for chunks of <= 2 columns: the
+    register-blocked GEMV pair (kPatchRb, the default at this size) and the
+    DMMA tiles it replaces (DLMPC_RB_GEMV=0); both take the reference's
+    iteration counts with iterates within FAST_RTOL, and agree to rounding."""
+    g = golden(name)
+    system, spec, mask, t_sim = loop_problem(g)
+    out = {}
+    for rb in ("1", "0"):
+        monkeypatch.setenv("DLMPC_RB_GEMV", rb)
+        sess = pb.DlmpcSession(system, spec, mask, FAST)
+        traj, _ = sess.simulate(g["x0"], t_sim)
+        assert sess.device.info()["mode"] == "patch"
+        sess.close()
+        assert list(traj.step_iterations) == list(g["step_iters"])
+        assert rel_err(traj.states, g["states"]) <= FAST_RTOL
+        assert rel_err(traj.inputs, g["inputs"]) <= FAST_RTOL
+        out[rb] = traj.states
+    assert rel_err(out["1"], out["0"]) <= 1e-12
+
+
 def test_c1_band_holds():
     g = golden("c1_loop_seed1")
     system, spec, mask, t_sim = loop_problem(g)
