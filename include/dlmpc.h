@@ -204,6 +204,21 @@ int dlmpc_set_halo(dlmpc_handle* h, const int64_t* send_cells, int64_t n_send,
 int dlmpc_halo_pack(dlmpc_handle* h, double* out);
 int dlmpc_halo_unpack(dlmpc_handle* h, const double* in);
 
+/* Asynchronous forms for the multi-GPU driver (all enqueued on the handle's
+ * stream, no host synchronisation): n host-driven iterations without a stop
+ * test, the last iteration's (pri, dual) maxima copied to resid_dev (2
+ * doubles, device memory); pack / unpack of the halo with device buffers.
+ * Replace the per-iteration round trips of dlmpc_iterate / dlmpc_halo_pack /
+ * dlmpc_halo_unpack (reference: the coordinator's run_iteration ->
+ * reduce_convergence, strategies.py:178-183, 249-260). */
+int dlmpc_iterate_async(dlmpc_handle* h, int n, double* resid_dev);
+int dlmpc_halo_pack_async(dlmpc_handle* h, double* out_dev);
+int dlmpc_halo_unpack_async(dlmpc_handle* h, const double* in_dev);
+/* Run the handle's work on an external CUDA stream (e.g. the framework's
+ * current stream, so its collectives order against the kernels); NULL
+ * restores the handle's own stream. Synchronises the previous stream. */
+int dlmpc_set_stream(dlmpc_handle* h, void* stream);
+
 /* After host-driven iterations: control extraction (admm.py:350-360) and
  * plant step (admm.py:363-369) for the loaded x; u_out [n_inputs],
  * x_next_out [n_cols] (valid for owned states). */

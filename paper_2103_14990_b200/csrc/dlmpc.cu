@@ -40,6 +40,8 @@ struct dlmpc_handle {
   int64_t* d_recv_cells = nullptr; int64_t n_recv = 0;
   double* d_halo = nullptr;
   char* h_stage = nullptr; size_t stage_cap = 0;   // pinned staging of dlmpc_simulate's host copies
+  cudaStream_t own_stream = nullptr;   // the handle's stream; `stream` may be an external one (dlmpc_set_stream)
+  int cur_b = 0, b_valid = 1;          // current ψ/λ buffer as known on the host (ctl[4])
 };
 
 namespace {
@@ -129,6 +131,7 @@ int launch(dlmpc_handle* h, const RunArgs& R) {
                                               args, static_cast<size_t>(h->smem_bytes), h->stream));
   CUDA_OR_FAIL(h, cudaEventRecord(h->ev1, h->stream));
   h->last_launches = 1;
+  h->b_valid = 0;   // a stop test may end the launch on either buffer
   return DLMPC_OK;
 }
 
@@ -141,6 +144,18 @@ int finish_timing(dlmpc_handle* h) {
 int read_ctl(dlmpc_handle* h, int* ctl) {
   CUDA_OR_FAIL(h, cudaMemcpyAsync(ctl, h->P.ctl, sizeof(int) * 8, cudaMemcpyDeviceToHost, h->stream));
   CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  h->cur_b = ctl[4]; h->b_valid = 1;
+  return DLMPC_OK;
+}
+
+// The current buffer without a round trip when the host knows it (after
+// asynchronous iterations), else from the device.
+int current_buffer(dlmpc_handle* h, int* b) {
+  if (!h->b_valid) {
+    int ctl[8];
+    if (int rc = read_ctl(h, ctl)) return rc;
+  }
+  *b = h->cur_b;
   return DLMPC_OK;
 }
 
@@ -683,10 +698,11 @@ int dlmpc_create(const dlmpc_problem* pr, int device, dlmpc_handle** out) {
     if (cudaMemset(P.ctl + 2, 0x7f, sizeof(int) * 2) != cudaSuccess) { rc = fail(h, DLMPC_CUDA_ERROR, "memset"); goto bad; }
 
     if ((rc = plan(h, pr)) != DLMPC_OK) goto bad;
-    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
+    if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess) {
       rc = fail(h, DLMPC_CUDA_ERROR, "stream/event creation failed"); goto bad;
     }
+    h->stream = h->own_stream;
     if ((rc = ensure_run_buffers(h, 64, 1)) != DLMPC_OK) goto bad;
   }
 #undef UP
@@ -716,7 +732,7 @@ void dlmpc_destroy(dlmpc_handle* h) {
   if (h->d_inputs) cudaFree(h->d_inputs);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
-  if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
 }
 
@@ -948,15 +964,68 @@ int dlmpc_halo_pack(dlmpc_handle* h, double* out) {
   if (!h || (h->n_send && !out)) return fail(h, DLMPC_BAD_ARGUMENT, "null halo buffer");
   if (!h->n_send) return DLMPC_OK;
   cudaSetDevice(h->device);
-  int ctl[8];
-  if (int rc = read_ctl(h, ctl)) return rc;
-  const int b = ctl[4];
+  int b = 0;
+  if (int rc = current_buffer(h, &b)) return rc;
   const int blocks = (int)std::min<int64_t>(h->sm_count * 4, (h->n_send + 255) / 256);
   halo_pack_kernel<<<blocks, 256, 0, h->stream>>>(h->P.psi[b], h->P.lam[b], h->d_send_cells, h->n_send,
                                                   reinterpret_cast<double2*>(h->d_halo));
   CUDA_OR_FAIL(h, cudaGetLastError());
   CUDA_OR_FAIL(h, cudaMemcpyAsync(out, h->d_halo, sizeof(double) * 2 * h->n_send, cudaMemcpyDefault, h->stream));
   CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+  return DLMPC_OK;
+}
+
+int dlmpc_halo_pack_async(dlmpc_handle* h, double* out_dev) {
+  if (!h || (h->n_send && !out_dev)) return fail(h, DLMPC_BAD_ARGUMENT, "null halo buffer");
+  if (!h->n_send) return DLMPC_OK;
+  cudaSetDevice(h->device);
+  int b = 0;
+  if (int rc = current_buffer(h, &b)) return rc;
+  const int blocks = (int)std::min<int64_t>(h->sm_count * 4, (h->n_send + 255) / 256);
+  halo_pack_kernel<<<blocks, 256, 0, h->stream>>>(h->P.psi[b], h->P.lam[b], h->d_send_cells, h->n_send,
+                                                  reinterpret_cast<double2*>(out_dev));
+  CUDA_OR_FAIL(h, cudaGetLastError());
+  return DLMPC_OK;
+}
+
+int dlmpc_halo_unpack_async(dlmpc_handle* h, const double* in_dev) {
+  if (!h || (h->n_recv && !in_dev)) return fail(h, DLMPC_BAD_ARGUMENT, "null halo buffer");
+  if (!h->n_recv) return DLMPC_OK;
+  cudaSetDevice(h->device);
+  int b = 0;
+  if (int rc = current_buffer(h, &b)) return rc;
+  const int blocks = (int)std::min<int64_t>(h->sm_count * 4, (h->n_recv + 255) / 256);
+  halo_unpack_kernel<<<blocks, 256, 0, h->stream>>>(h->P.psi[b], h->P.lam[b], h->d_recv_cells, h->n_recv,
+                                                    reinterpret_cast<const double2*>(in_dev));
+  CUDA_OR_FAIL(h, cudaGetLastError());
+  return DLMPC_OK;
+}
+
+int dlmpc_iterate_async(dlmpc_handle* h, int n, double* resid_dev) {
+  if (!h || n < 1 || !resid_dev) return fail(h, DLMPC_BAD_ARGUMENT, "bad argument");
+  cudaSetDevice(h->device);
+  int b = 0;
+  if (int rc = current_buffer(h, &b)) return rc;   // (a round trip only after a stop-tested launch)
+  if (int rc = ensure_run_buffers(h, n, 1)) return rc;
+  RunArgs R{};
+  R.t_sim = 1; R.closed_loop = 0; R.warm_start = 1; R.cold_start = 0;
+  R.max_iters = n; R.stop_on_conv = 0;
+  R.hist = h->d_hist; R.step_iters = h->d_step_iters; R.states = h->d_states; R.inputs = h->d_inputs;
+  R.it_base = h->it_cont;
+  if (int rc = launch(h, R)) return rc;
+  CUDA_OR_FAIL(h, cudaMemcpyAsync(resid_dev, h->d_hist + 2 * (n - 1), sizeof(double) * 2, cudaMemcpyDeviceToDevice,
+                                  h->stream));
+  CUDA_OR_FAIL(h, cudaGetLastError());
+  h->it_cont += n;
+  h->cur_b = b ^ (n & 1); h->b_valid = 1;   // no stop test: exactly n buffer swaps
+  return DLMPC_OK;
+}
+
+int dlmpc_set_stream(dlmpc_handle* h, void* stream) {
+  if (!h) return fail(h, DLMPC_BAD_ARGUMENT, "null handle");
+  cudaSetDevice(h->device);
+  CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));   // work queued on the old stream first
+  h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own_stream;
   return DLMPC_OK;
 }
 
@@ -967,9 +1036,8 @@ int dlmpc_halo_unpack(dlmpc_handle* h, const double* in) {
   // columns' contributions, and rows reading halo columns recompute their
   // full Φ every iteration)
   cudaSetDevice(h->device);
-  int ctl[8];
-  if (int rc = read_ctl(h, ctl)) return rc;
-  const int b = ctl[4];
+  int b = 0;
+  if (int rc = current_buffer(h, &b)) return rc;
   CUDA_OR_FAIL(h, cudaMemcpyAsync(h->d_halo, in, sizeof(double) * 2 * h->n_recv, cudaMemcpyDefault, h->stream));
   const int blocks = (int)std::min<int64_t>(h->sm_count * 4, (h->n_recv + 255) / 256);
   halo_unpack_kernel<<<blocks, 256, 0, h->stream>>>(h->P.psi[b], h->P.lam[b], h->d_recv_cells, h->n_recv,

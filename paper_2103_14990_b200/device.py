@@ -58,7 +58,8 @@ EXPORTS = ("dlmpc_create", "dlmpc_destroy", "dlmpc_last_error", "dlmpc_global_er
            "dlmpc_simulate_device", "dlmpc_get", "dlmpc_put", "dlmpc_zero",
            "dlmpc_last_timing", "dlmpc_stream", "dlmpc_synchronize", "dlmpc_info",
            "dlmpc_phase_times", "dlmpc_audit", "dlmpc_get_cols", "dlmpc_put_cols",
-           "dlmpc_finish_step", "dlmpc_set_halo", "dlmpc_halo_pack", "dlmpc_halo_unpack")
+           "dlmpc_finish_step", "dlmpc_set_halo", "dlmpc_halo_pack", "dlmpc_halo_unpack",
+           "dlmpc_iterate_async", "dlmpc_halo_pack_async", "dlmpc_halo_unpack_async", "dlmpc_set_stream")
 
 _lib = None
 
@@ -106,6 +107,10 @@ def load_library():
     lib.dlmpc_set_halo.argtypes = [vp, _i64p, C.c_int64, _i64p, C.c_int64]
     lib.dlmpc_halo_pack.argtypes = [vp, vp]
     lib.dlmpc_halo_unpack.argtypes = [vp, vp]
+    lib.dlmpc_iterate_async.argtypes = [vp, C.c_int, vp]
+    lib.dlmpc_halo_pack_async.argtypes = [vp, vp]
+    lib.dlmpc_halo_unpack_async.argtypes = [vp, vp]
+    lib.dlmpc_set_stream.argtypes = [vp, vp]
     _lib = lib
     return lib
 
@@ -299,6 +304,27 @@ class DeviceSession:
 
     def halo_unpack(self, in_ptr):
         self._check(self._lib.dlmpc_halo_unpack(self._h, C.c_void_p(in_ptr)), "dlmpc_halo_unpack")
+
+    # asynchronous forms (device buffers, enqueued on the session's stream)
+    def iterate_async(self, n, resid_ptr):
+        """n iterations without a stop test; the last (pri, dual) to device
+        memory at `resid_ptr` (2 doubles). No host synchronisation."""
+        self._check(self._lib.dlmpc_iterate_async(self._h, int(n), C.c_void_p(resid_ptr)), "dlmpc_iterate_async")
+
+    def halo_pack_async(self, out_ptr):
+        self._check(self._lib.dlmpc_halo_pack_async(self._h, C.c_void_p(out_ptr)), "dlmpc_halo_pack_async")
+
+    def halo_unpack_async(self, in_ptr):
+        self._check(self._lib.dlmpc_halo_unpack_async(self._h, C.c_void_p(in_ptr)), "dlmpc_halo_unpack_async")
+
+    def set_stream(self, stream_ptr):
+        """Run on an external CUDA stream (int handle; None = the session's
+        own; 0, the legacy default stream, is passed as cudaStreamLegacy)."""
+        if stream_ptr is None:
+            h = None
+        else:
+            h = int(stream_ptr) or 1   # cudaStreamLegacy
+        self._check(self._lib.dlmpc_set_stream(self._h, C.c_void_p(h)), "dlmpc_set_stream")
 
     def finish_step(self):
         """(u, x_next) for the loaded x after host-driven iterations."""

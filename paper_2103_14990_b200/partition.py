@@ -293,11 +293,36 @@ class DistExchange:
         self.dev = torch.device("cuda", torch.cuda.current_device()) if self.nccl else torch.device("cpu")
         self.sbuf = torch.zeros(max(1, rk.send_doubles), dtype=torch.float64, device=self.dev)
         self.rbuf = torch.zeros(max(1, rk.recv_doubles), dtype=torch.float64, device=self.dev)
+        if self.nccl:
+            # the collectives run ordered on the solver's own stream (made
+            # torch's current stream around them): stream order replaces the
+            # host round trips
+            self.res = torch.zeros(2, dtype=torch.float64, device=self.dev)
+            self.stream = torch.cuda.ExternalStream(rk.session.stream, device=self.dev)
 
     def iteration(self):
         """One partitioned ADMM iteration -> global (pri, dual)."""
         import torch
         dist, rk, group = self.dist, self.rk, self.group
+        if self.nccl:
+            # everything enqueued on the solver's stream; one host sync (the
+            # residual read) per iteration
+            with torch.cuda.stream(self.stream):
+                rk.session.iterate_async(1, self.res.data_ptr())
+                if rk.send_to:
+                    rk.session.halo_pack_async(self.sbuf.data_ptr())
+                dist.all_reduce(self.res, op=dist.ReduceOp.MAX, group=group)
+                ops = [dist.P2POp(dist.isend, self.sbuf[rk.send_off[k]:rk.send_off[k + 1]], q, group)
+                       for k, q in enumerate(rk.send_to)]
+                ops += [dist.P2POp(dist.irecv, self.rbuf[rk.recv_off[k]:rk.recv_off[k + 1]], q, group)
+                        for k, q in enumerate(rk.recv_from)]
+                if ops:
+                    for w in dist.batch_isend_irecv(ops):
+                        w.wait()
+                if rk.recv_from:
+                    rk.session.halo_unpack_async(self.rbuf.data_ptr())
+                pri, dual = self.res.tolist()
+            return pri, dual
         loc = torch.tensor(rk.iterate(), dtype=torch.float64, device=self.dev)
         dist.all_reduce(loc, op=dist.ReduceOp.MAX, group=group)
         rk.pack(self.sbuf.data_ptr())

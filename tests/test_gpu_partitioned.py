@@ -129,6 +129,29 @@ def test_distributed_driver_single_rank_nccl():
         dist.destroy_process_group()
 
 
+def test_distributed_driver_async_exchange_matches_inprocess():
+    """The NCCL driver enqueues iteration, halo pack, all-reduce and unpack on
+    the solver's stream with one host read per iteration: on a network large
+    enough that a missing stream dependency would read a stale residual, it
+    takes the same iterations as the synchronous in-process driver and ends
+    bit-identical."""
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=20000, d=3, horizon=10, t_sim=2, seed=1))
+    ref = simulate_partitioned_inprocess(system, spec, mask, x0, 2, 1, FAST)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        states, inputs, iters = simulate_partitioned(system, spec, mask, x0, 2, FAST)
+    finally:
+        dist.destroy_process_group()
+    assert iters == ref[2]
+    assert np.array_equal(states, ref[0]) and np.array_equal(inputs, ref[1])
+
+
 def _dist_worker(rank, world, port, name, variant, out_q):
     """One torch.distributed rank (gloo) of the partitioned closed loop; all
     ranks share cuda:0, their kernels never wait on one another (the
