@@ -152,6 +152,68 @@ def test_distributed_driver_async_exchange_matches_inprocess():
     assert np.array_equal(states, ref[0]) and np.array_equal(inputs, ref[1])
 
 
+def test_async_exchange_entry_points_with_halos():
+    """dlmpc_iterate_async / dlmpc_halo_pack_async / dlmpc_halo_unpack_async
+    with real halos: three ranks in one process, messages moved between
+    device buffers on the sessions' streams, the global residual reduced on
+    the host; the closed loop equals the synchronous in-process driver bit
+    for bit (NCCL cannot run several ranks on one GPU, this covers the async
+    path the NCCL driver takes)."""
+    import torch
+    from paper_2103_14990_b200.errors import NotConverged
+    from paper_2103_14990_b200.partition import RankSolver, plan_partition
+    g = golden("c2_loop_seed1")
+    system, spec, mask, t_sim = loop_problem(g)
+    t_sim = 4
+    ref = simulate_partitioned_inprocess(system, spec, mask, g["x0"], t_sim, 3, FAST)
+    world = 3
+    plans = plan_partition(mask, world)
+    ranks = [RankSolver(system, spec, mask, plans, r, FAST, 0) for r in range(world)]
+    try:
+        dev = torch.device("cuda", 0)
+        sbuf = [torch.zeros(max(1, rk.send_doubles), dtype=torch.float64, device=dev) for rk in ranks]
+        rbuf = [torch.zeros(max(1, rk.recv_doubles), dtype=torch.float64, device=dev) for rk in ranks]
+        res = [torch.zeros(2, dtype=torch.float64, device=dev) for _ in ranks]
+        x = np.asarray(g["x0"], dtype=np.float64)
+        states, iters = [x], []
+        for step in range(t_sim):
+            for rk in ranks:
+                rk.start_step(x, cold=(step == 0))
+            for it in range(spec.max_iters):
+                for r, rk in enumerate(ranks):
+                    rk.session.iterate_async(1, res[r].data_ptr())
+                    rk.session.halo_pack_async(sbuf[r].data_ptr())
+                for rk in ranks:
+                    rk.session.synchronize()
+                for r, rk in enumerate(ranks):
+                    for k, src in enumerate(rk.recv_from):
+                        sk = ranks[src].send_to.index(r)
+                        a, b = int(ranks[src].send_off[sk]), int(ranks[src].send_off[sk + 1])
+                        rbuf[r][int(rk.recv_off[k]):int(rk.recv_off[k + 1])].copy_(sbuf[src][a:b])
+                torch.cuda.synchronize()
+                for r, rk in enumerate(ranks):
+                    rk.session.halo_unpack_async(rbuf[r].data_ptr())
+                pri = max(float(v[0]) for v in res)
+                dual = max(float(v[1]) for v in res)
+                if pri <= spec.eps_pri and dual <= spec.eps_dual:
+                    break
+            else:
+                raise NotConverged([], step=step)
+            iters.append(it + 1)
+            xn = np.zeros(system.n_states)
+            for rk in ranks:
+                rk.session.synchronize()
+                _, _, sid, xx = rk.finish_step()
+                xn[sid] = xx
+            x = xn
+            states.append(x)
+        assert iters == ref[2]
+        assert np.array_equal(np.array(states), ref[0])
+    finally:
+        for rk in ranks:
+            rk.close()
+
+
 def _dist_worker(rank, world, port, name, variant, out_q):
     """One torch.distributed rank (gloo) of the partitioned closed loop; all
     ranks share cuda:0, their kernels never wait on one another (the
