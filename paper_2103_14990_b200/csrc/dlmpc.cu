@@ -481,8 +481,14 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
     bool rb_off = false;   // the register-blocked GEMV pair was planned but did not fit
     for (; h->mode != kStream;) {
       const int ldk = ld_frag(s8_max), ldy = ld_frag(tc);
+      // 16-column tiles run GEMM 1 tile-parallel for every class: no split-K
+      // partials (measured on the C4 cells at N=1000: 8-16% faster than
+      // split-K for the classes with < 12 tiles)
       int split_max = 1;
+      const char* esk = getenv("DLMPC_SPLITK_ALL");
+      const bool no_split = tc == 16 && !(esk && esk[0] == '1');
       for (int k = 0; k < pr->n_classes; ++k) {
+        if (no_split) continue;
         const int groups1 = (((pr->class_n0[k] + 7) / 8) + kMG1 - 1) / kMG1;
         int sp = 1;
         while (groups1 * sp * 2 <= kWarps && sp < 4) sp <<= 1;
@@ -523,8 +529,12 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       const long long stash_one = 2LL * st_cols * ldk;
       int stash_bufs = 0;
       if (h->mode == kPatch) {
+        // staging buffers within ~200 KB of shared memory in all: a larger
+        // carveout leaves too little L1 for the kernel's table loads (d=3,
+        // T=10 at N=1000: 1.4% slower with a buffer that took it to 208 KB)
         const long long base = total(opr, split_max, cache);
-        stash_bufs = base + 2 * stash_one + 2 <= limit ? 2 : (base + stash_one + 2 <= limit ? 1 : 0);
+        const long long lim = std::min<long long>(limit, (no_split ? 200LL * 1024 : 1LL << 40) / 8);
+        stash_bufs = base + 2 * stash_one + 2 <= lim ? 2 : (base + stash_one + 2 <= lim ? 1 : 0);
       }
       if (rb && (stash_bufs == 0 || opr < rb_opr)) { rb_off = true; continue; }
       long long off = (opr + 1) & ~1LL;
