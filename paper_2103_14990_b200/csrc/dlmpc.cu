@@ -333,7 +333,9 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         while ((2 * ldl) % 16 != 4 && (2 * ldl) % 16 != 12) ldl += 2;
         const long long fixed = ((opr_main + 1) & ~1LL) + 2LL * tc * ldk + (long long)tc * ldl + (long long)n08_max * ldy +
                                 (sp_max > 1 ? (long long)sp_max * n08_max * tc : 0) + 32 + 8 * tc + 8;
-        long long cap = std::min<long long>(4096, (limit - fixed) / 2);
+        // patch rows per unit: 2048 measured 1.3% faster than 4096 at N=1e6
+        // (fewer, better-balanced units once the tables fit at the first try)
+        long long cap = std::min<long long>(2048, (limit - fixed) / 2);
         if (const char* e = getenv("DLMPC_STREAM_CAP")) cap = std::min<long long>(cap, atoll(e));
         long long ch_max = 0, extra = 0;
         bool ok = false;
