@@ -1439,7 +1439,7 @@ struct LamWait {
 // the common path keeps shared-memory fragment loads.
 template <int TC, bool OPS>
 __device__ void stream_iteration(const DevProblem& P, int b, const double* x, int it, int itg, double* smem,
-                                 int& cur, unsigned (&ph)[3]) {
+                                 int& cur, unsigned& ph) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* s_patch = smem + P.off_patch;
   double* c_patch = smem + P.off_cpatch;
@@ -1613,8 +1613,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
     };
     if (nch > 0) {   // first chunk: operator, ψ landed, K
       if (OPS) stage_operator_sized(P, chtab[0], (chtab[3] + 7) & ~7, chtab[5], smem, cur);
-      mbar_wait(bars + 0, ph[0]);
-      ph[0] ^= 1u;
+      mbar_wait(bars + 0, ph & 1u);
+      ph ^= 1u;
       k_pass(psi_st, meta0 + TC, reinterpret_cast<const double*>(meta0 + 3 * TC), chtab[3], chtab[2]);
       __syncthreads();
     }
@@ -1643,7 +1643,10 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       // epilogue of chunk ch (13 warps split GEMM 2's 26 m-tiles evenly), the
       // other warps -- idle in the GEMMs -- build K(ch+1). The row pass of ch
       // stays a whole-CTA phase (latency-bound, it needs every thread).
-      constexpr int kCons = 13, kProd = kWarps - kCons;
+#ifndef DLMPC_STREAM_CONS
+#define DLMPC_STREAM_CONS 13
+#endif
+      constexpr int kCons = DLMPC_STREAM_CONS, kProd = kWarps - kCons;
       const bool prod = warp >= kCons;
       const int ptid = tid - kCons * 32;
       for (int ch = ch_a; ch < ch_b; ++ch) {
@@ -1668,24 +1671,29 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
               reinterpret_cast<double*>(mm)[3 * TC + ptid] = ok ? ld_cg(x + ce[CHW + 1] + ptid) : 0.0;
             }
             nbar_sync(6, kProd * 32);
-            mbar_wait(bars + (mb ^ 1), ph[mb ^ 1]);
+            mbar_wait(bars + (mb ^ 1), (ph >> (mb ^ 1)) & 1u);
             const long long* mn = meta0 + (mb ^ 1) * 4 * TC;
             k_pass(psi_st + (mb ^ 1) * TC * ldk, mn + TC, reinterpret_cast<const double*>(mn + 3 * TC),
                    ce[CHW + 3], ce[CHW + 2], kCons, kProd);
           }
         } else {
           const double* nop = OPS ? smem : P.null_pool + P.class_null_off[ce[0]];
+          PT_LAP(P, 1)
           gemm1<TC, NoHook, kCons, GroupBar<kCons>>(P, S4, n08, ldn, nop, kt, ldk, yb, P.ldy, yp);
+          PT_LAP(P, 12)
           StreamEpi<TC> epi{P.psi[b ^ 1], P.lam[b ^ 1], P.q_pool, m_pos, m_s, m_q, m_x,
-                            s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, bars + 2, ph[2], ce[6] != 0};
+                            s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, bars + 2, (ph >> 2) & 1u, ce[6] != 0};
           gemm2<TC, StreamEpi<TC>, kCons>(S8, n08, ldn, nop, yb, P.ldy, epi);
           pri_m = epi.pri_m; dual_m = epi.dual_m;
+          PT_LAP(P, 13)
         }
-        ph[2] ^= 1u;
-        if (has_next) ph[mb ^ 1] ^= 1u;
+        ph ^= 4u;
+        if (has_next) ph ^= 1u << (mb ^ 1);
         __syncthreads();
+        PT_LAP(P, 14)
         row_pass(m_s, m_x, S, nt, tid, kThreads, ce[6] != 0);
         __syncthreads();
+        PT_LAP(P, 15)
         if (has_next) stash_lam_bulk(P, ce[CHW + 1], ce[CHW + 2], lam, lam_st, ldl, bars + 2);
         if (has_next2) stash_cols_bulk(P, ce[2 * CHW + 1], ce[2 * CHW + 2], psi, kt, bars + mb);
       }
@@ -1706,8 +1714,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       double xn = 0.0;   // x of the next chunk's columns (meta written after GEMM 1)
       if (has_next && tid < ce[CHW + 2]) xn = ld_cg(x + ce[CHW + 1] + tid);
       const double* nop = OPS ? smem : P.null_pool + P.class_null_off[ce[0]];
-      gemm1<TC>(P, S4, n08, ldn, nop, kt, ldk, yb, P.ldy, yp, LamWait{bars + 2, ph[2]});
-      ph[2] ^= 1u;
+      gemm1<TC>(P, S4, n08, ldn, nop, kt, ldk, yb, P.ldy, yp, LamWait{bars + 2, (ph >> 2) & 1u});
+      ph ^= 4u;
       if (has_next && tid < TC) {
         long long* mm = meta0 + (mb ^ 1) * 4 * TC;
         const bool ok = tid < ce[CHW + 2];
@@ -1729,8 +1737,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       if (has_next) {   // next chunk: operator, ψ landed, K
         const long long* mn = meta0 + (mb ^ 1) * 4 * TC;
         if (OPS) stage_operator_sized(P, ce[CHW], (ce[CHW + 3] + 7) & ~7, ce[CHW + 5], smem, cur);
-        mbar_wait(bars + (mb ^ 1), ph[mb ^ 1]);
-        ph[mb ^ 1] ^= 1u;
+        mbar_wait(bars + (mb ^ 1), (ph >> (mb ^ 1)) & 1u);
+        ph ^= 1u << (mb ^ 1);
         k_pass(psi_st + (mb ^ 1) * TC * ldk, mn + TC, reinterpret_cast<const double*>(mn + 3 * TC),
                ce[CHW + 3], ce[CHW + 2]);
       }
@@ -1913,7 +1921,7 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
   const bool leader = blockIdx.x == 0 && tid == 0;
   int cur = -1;   // class whose operator is staged at smem offset 0
   int b = P.ctl[4];
-  unsigned ph[3] = {0u, 0u, 0u};   // stream mode: mbarrier phases (ψ0, ψ1, λ)
+  unsigned ph = 0u;   // stream mode: mbarrier phase bits (ψ0, ψ1, λ) -- a register, not an indexed array
   if (MODE == kStream) {
     if (tid < 3) mbar_init(reinterpret_cast<unsigned long long*>(smem + P.off_bar) + tid, 1);
     __syncthreads();
