@@ -17,10 +17,10 @@ print(f"N={n} {sess.device.info()} iters {it} device {ms:.3f} ms = {1e3*ms/it:.2
 for k, nm in enumerate(names):
     col = pt[:, k]
     print(f"  {nm:12s} max {col.max():8.2f} us  mean {col.mean():8.2f} us")
-for k, nm in zip(range(12, 16), ["  gemm1", "  gemm2+epi", "  wait prod", "  row pass"]):
+for k, nm in zip([12, 9, 10, 13, 14, 15], ["  gemm1", "  gemm2 k", "  wait λ", "  epilogue", "  wait prod", "  row pass"]):
     col = pt[:, k]
     print(f"  {nm:12s} max {col.max():8.2f} us  mean {col.mean():8.2f} us")
-tot = pt[:, [0, 1, 2, 3, 4, 5, 7, 12, 13, 14, 15]].sum(axis=1)   # everything but the barrier wait
+tot = pt[:, [0, 1, 2, 3, 4, 5, 7, 9, 10, 12, 13, 14, 15]].sum(axis=1)   # everything but the barrier wait
 order = np.argsort(-tot)
 print("  slowest CTAs (work us/iter):", ", ".join(f"{c}:{tot[c]:.1f}" for c in order[:6]))
 print("  fastest CTAs (work us/iter):", ", ".join(f"{c}:{tot[c]:.1f}" for c in order[-4:]))
