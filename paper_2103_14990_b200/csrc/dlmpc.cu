@@ -344,7 +344,10 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           ch_max = 0;
           for (size_t u = 0; u + 1 < u_chunk.size(); ++u) ch_max = std::max<long long>(ch_max, u_chunk[u + 1] - u_chunk[u]);
           // chunk table [ch][8 ints], patch table [q][6 doubles], row map [rows] ints
-          extra = (long long)(ch_max + 1) * (8 + 2 * tc) / 2 + 6 * np_max + np_max + (cap + 2) / 2 + 32;
+          // the unit tables twice (the next unit's are prefetched), with the
+          // raw ‖a‖² copy beside the reciprocals
+          extra = 2 * (((((ch_max + 1) * (8 + 2 * tc) / 2 + 1) & ~1LL) + 6 * ((np_max + 1) & ~1LL) +
+                        2 * ((np_max + 1) & ~1LL) + 2)) + (cap + 2) / 2 + 32;
           const long long need = fixed + 2 * ((cap + 1) & ~1LL) + extra;
           if (need <= limit) { ok = prows_max <= cap; break; }
           cap -= (need - limit + 1) / 2 + 16;
@@ -446,9 +449,15 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
             P.off_patch = (int)off; off += (cap + 1) & ~1LL;
             P.off_cpatch = (int)off; off += (cap + 1) & ~1LL;
             P.patch_cap = (int)cap;
-            P.off_chtab = (int)off; off += ((ch_max + 1) * (8 + 2 * tc) / 2 + 1) & ~1LL; P.ch_cap = (int)(ch_max + 1);
-            P.off_ptab = (int)off; off += 6 * np_max; P.np_cap = (int)np_max;
-            P.off_pada = (int)off; off += np_max;
+            {   // unit tables [chunk table | patch table | 1/‖a‖² | raw ‖a‖²], two copies tab_alt apart
+              const long long np_e = (np_max + 1) & ~1LL;
+              const long long tab0 = off;
+              P.off_chtab = (int)off; off += ((ch_max + 1) * (8 + 2 * tc) / 2 + 1) & ~1LL; P.ch_cap = (int)(ch_max + 1);
+              P.off_ptab = (int)off; off += 6 * np_e; P.np_cap = (int)np_e;
+              P.off_pada = (int)off; off += 2 * np_e + 2;
+              P.tab_alt = (int)(off - tab0);
+              off += P.tab_alt;
+            }
             P.off_rowq = (int)off; off += (cap + 2) / 2;
             off = (off + 1) & ~1LL;
             P.off_udesc = (int)off; off += 16;
@@ -702,7 +711,7 @@ int dlmpc_create(const dlmpc_problem* pr, int device, dlmpc_handle** out) {
       if ((rc = alloc(h, (size_t)pr->n_cols, &P.x[q])) != DLMPC_OK) goto bad;
     }
     if ((rc = alloc(h, (size_t)pr->n_rows, &P.s_row)) != DLMPC_OK) goto bad;
-    if ((rc = alloc(h, (size_t)pr->n_sub, &P.ada)) != DLMPC_OK) goto bad;
+    if ((rc = alloc(h, (size_t)pr->n_sub + 2, &P.ada)) != DLMPC_OK) goto bad;
     if ((rc = alloc(h, (size_t)(pr->n_inputs ? pr->n_inputs : 1), &P.u)) != DLMPC_OK) goto bad;
     if ((rc = alloc(h, 8, &P.ctl)) != DLMPC_OK) goto bad;
     if ((rc = alloc(h, ncell, &h->d_scratch)) != DLMPC_OK) goto bad;

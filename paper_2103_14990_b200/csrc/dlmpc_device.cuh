@@ -113,6 +113,7 @@ struct DevProblem {
   const int* cta_gop;          // stream mode: CTA reads its class operator from L2 (does not fit)
   int off_chtab, ch_cap;       // per-unit chunk table: [ch_cap][8] ints (k, c0, nt, S, n08, ldn)
   int off_ptab, np_cap;        // per-unit patch-subsystem table: [np_cap][6] doubles
+  int tab_alt;                 // stream mode: doubles from the unit tables (chunk, patch, 1/‖a‖²) to their second copy
   int off_rowq;                // per patch row: its patch-subsystem index (int)
   int off_pada;                // per patch subsystem: ||a||^2 of this MPC step
   int off_udesc;               // two unit descriptors (16 ints each)
@@ -1455,10 +1456,10 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
   double* yb = smem + P.off_y;
   double* yp = smem + P.off_yp;
   long long* meta0 = reinterpret_cast<long long*>(smem + P.off_meta);   // [2][4][TC]
-  int* chtab = reinterpret_cast<int*>(smem + P.off_chtab);               // [ch][8]
-  double* ptab = smem + P.off_ptab;                                      // [q][6]
+  int* const chtab0 = reinterpret_cast<int*>(smem + P.off_chtab);       // [ch][8 + 2 TC], two copies
+  double* const ptab0 = smem + P.off_ptab;                               // [q][6], two copies
+  double* const pada0 = smem + P.off_pada;
   int* rowq = reinterpret_cast<int*>(smem + P.off_rowq);
-  double* pada = smem + P.off_pada;                                      // ||a||^2 per patch subsystem
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + P.off_bar);   // ψ0, ψ1, λ
   const int ldk = P.ldk;
   double* psi_st = smem + P.off_k;                  // [2][TC][ldk]
@@ -1504,8 +1505,14 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
     const int prows = ud1.z, ch_a = ud1.w, ch_b = ud2.x, pt_off = ud2.y;
     const int npq = phi_ - plo;
     const int nch = ch_b - ch_a;
-    // the unit's control tables in one coalesced round trip
-    {
+    // the unit's control tables: copy (un - un_a) & 1 of [chunk table | patch
+    // table | raw ‖a‖² (from the even index below plo)]; the first unit of
+    // the iteration loads its own, every later one was prefetched (cp.async)
+    // into its copy during the previous unit
+    const int tb = (un - un_a) & 1;
+    int* chtab = chtab0 + 2 * tb * P.tab_alt;
+    double* ptab = ptab0 + tb * P.tab_alt;
+    if (un == un_a) {
       const int4* src = reinterpret_cast<const int4*>(P.chunk_desc + static_cast<size_t>(ch_a) * CHW);
       int4* dst = reinterpret_cast<int4*>(chtab);
       for (int q = tid; q < nch * CHW / 4; q += kThreads) dst[q] = __ldg(src + q);
@@ -1514,9 +1521,16 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       for (int q = tid; q < npq * 3; q += kThreads) pd[q] = __ldg(ps + q);
       for (int q = tid; q < npq; q += kThreads) {
         const double a = ld_cg(P.ada + plo + q);
-        pada[q] = a > 0.0 ? 1.0 / a : 0.0;   // only read in iterations >= 1 (reciprocal form)
+        pada0[q] = a > 0.0 ? 1.0 / a : 0.0;   // only read in iterations >= 1 (reciprocal form)
+      }
+    } else {
+      const double* raw = pada0 + P.np_cap + tb * P.tab_alt + (plo & 1);
+      for (int q = tid; q < npq; q += kThreads) {
+        const double a = raw[q];
+        pada0[q] = a > 0.0 ? 1.0 / a : 0.0;
       }
     }
+    double* const pada = pada0;
     __syncthreads();
     PT_LAP(P, 2)
     for (int q = warp; q < npq; q += kWarps) {
@@ -1605,7 +1619,25 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       mm[2 * TC + tid] = ok ? static_cast<long long>(chtab[8 + TC + tid]) * P.s_pad : 0;
       reinterpret_cast<double*>(mm)[3 * TC + tid] = x_first;
     }
+    if (tid < 4) cp_async_wait<0>();   // the next unit's descriptor (read after the barrier)
     __syncthreads();
+    if (un + 1 < un_b) {
+      // the next unit's tables -> the other copy, under this unit's chunks
+      // (cp.async, waited at this unit's end)
+      const int* nd = udesc + 16 * (ub ^ 1);
+      const int n_plo = nd[2], n_np = nd[3] - nd[2], n_cha = nd[7], n_nch = nd[8] - nd[7], n_pt = nd[9];
+      int* cdst = chtab0 + 2 * (tb ^ 1) * P.tab_alt;
+      const int* csrc = P.chunk_desc + static_cast<size_t>(n_cha) * CHW;
+      for (int q = tid; q < n_nch * CHW / 4; q += kThreads)
+        cp_async16(reinterpret_cast<double*>(cdst + 4 * q), reinterpret_cast<const double*>(csrc + 4 * q));
+      double* pdst = ptab0 + (tb ^ 1) * P.tab_alt;
+      const double* psrc = P.unit_ptab + static_cast<size_t>(n_pt) * 6;
+      for (int q = tid; q < n_np * 3; q += kThreads) cp_async16(pdst + 2 * q, psrc + 2 * q);
+      double* adst = pada0 + P.np_cap + (tb ^ 1) * P.tab_alt;
+      const int a0 = n_plo & ~1;
+      for (int q = tid; 2 * q < n_plo + n_np - a0; q += kThreads) cp_async16(adst + 2 * q, P.ada + a0 + 2 * q);
+    }
+    cp_async_commit();
     PT_LAP(P, 0)
     // K = ψ + s·x (= φ + λ) in place, zero padded to TC x S4 (GEMM 1 k-steps
     // of 4); one warp per column
