@@ -36,6 +36,11 @@ namespace cg = cooperative_groups;
 
 namespace dlmpc {
 
+// GEMM 1: a warp takes a whole m-row of tiles when that costs no extra round
+#ifndef DLMPC_G1_MROW
+#define DLMPC_G1_MROW 1
+#endif
+
 // Optional per-phase timers (profiling build only: -DDLMPC_PHASE_TIMING).
 // Thread 0 of every CTA accumulates SM-cycle deltas per phase into
 // P.phase_ns[blockIdx.x * 16 + phase] (0-7 per iteration, 8-15 per MPC step).
@@ -464,7 +469,7 @@ struct GroupBar {   // barrier over the first NW warps
 };
 
 // NW warps (warp ids 0..NW-1) run the GEMMs; `sync` is their barrier.
-template <int TC, class Hook = NoHook, int NW = kWarps, class Sync = CtaBar>
+template <int TC, class Hook = NoHook, int NW = kWarps, class Sync = CtaBar, bool MROW = false>
 __device__ __forceinline__ void gemm1(const DevProblem& P, int SK, int n08, int ldn, const double* nop,
                                       const double* kt, int ldk, double* yb, int ldy, double* yp,
                                       const Hook& before_sync = Hook(), const Sync& sync = Sync()) {
@@ -472,6 +477,44 @@ __device__ __forceinline__ void gemm1(const DevProblem& P, int SK, int n08, int 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
   const int mt1 = n08 >> 3, ks1 = SK >> 2;   // SK: K extent, a multiple of 4
+  if (MROW && NTN > 1 && DLMPC_G1_MROW && mt1 >= NW && (mt1 + NW - 1) / NW * NTN <= (mt1 * NTN + NW - 1) / NW) {
+    // large bases (>= one m-tile per warp) and as many rounds with a whole
+    // m-row of tiles per warp as with one tile per warp: each basis fragment
+    // feeds all NTN tiles (0.75 instead of 1 fragment byte per FLOP at
+    // NTN = 2). C4 at N=1000: d=6,T=20 87.5 -> 77.1 us/iter, d=4,T=30 93.1 ->
+    // 83.1, d=6,T=30 250.9 -> 238.8 (patch mode only: MROW; the stream
+    // kernel measured 2-3% slower with this branch compiled in). Per tile the same two chains and
+    // order as below, so Y is bitwise the same
+    for (int mt = warp; mt < mt1; mt += NW) {
+      double ca[NTN][2], cb[NTN][2];
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) { ca[nn][0] = ca[nn][1] = cb[nn][0] = cb[nn][1] = 0.0; }
+      int ks = 0;
+      for (; ks + 1 < ks1; ks += 2) {
+        const int p0 = ks * 4 + tig, p1 = p0 + 4;
+        const double a0 = nop[p0 * ldn + mt * 8 + g], a1 = nop[p1 * ldn + mt * 8 + g];
+#pragma unroll
+        for (int nn = 0; nn < NTN; ++nn) {
+          dmma(ca[nn][0], ca[nn][1], a0, kt[(nn * 8 + g) * ldk + p0]);
+          dmma(cb[nn][0], cb[nn][1], a1, kt[(nn * 8 + g) * ldk + p1]);
+        }
+      }
+      if (ks < ks1) {
+        const int p0 = ks * 4 + tig;
+        const double a0 = nop[p0 * ldn + mt * 8 + g];
+#pragma unroll
+        for (int nn = 0; nn < NTN; ++nn) dmma(ca[nn][0], ca[nn][1], a0, kt[(nn * 8 + g) * ldk + p0]);
+      }
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) {
+        yb[(mt * 8 + g) * ldy + nn * 8 + 2 * tig] = ca[nn][0] + cb[nn][0];
+        yb[(mt * 8 + g) * ldy + nn * 8 + 2 * tig + 1] = ca[nn][1] + cb[nn][1];
+      }
+    }
+    before_sync();
+    sync();
+    return;
+  }
   if (mt1 * NTN >= 12 || P.split_max == 1) {
     // enough (m, n) tiles to keep the DMMA pipe busy (or no room for split-K
     // partials): one tile per warp over the full K with two interleaved
@@ -837,7 +880,7 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
   if (TC == 8 && nt <= 2 && P.small_gemv && n08 * 10 <= kThreads)
     gemv1_small<TC>(S, n08, ldn, nop, kt, ldk, yp, yb, ldy, nt);
   else
-    gemm1<TC>(P, S8, n08, ldn, nop, kt, ldk, yb, ldy, yp);
+    gemm1<TC, NoHook, kWarps, CtaBar, true>(P, S8, n08, ldn, nop, kt, ldk, yb, ldy, yp);
   PT_LAP(P, 2)
   // GEMM 2: O[t][p] = sum_a N[p][a] Y[a][t]  (M = S, N = TC, K = n0) -> kt
   StoreO epi{kt, ldk};

@@ -1,5 +1,6 @@
 """Per-phase device time breakdown (profiling build of the library).
-usage: DLMPC_LIB=paper_2103_14990_b200/libdlmpc_timing.so python tools/phase_profile.py N [t_sim] [twophase]"""
+usage: DLMPC_LIB=paper_2103_14990_b200/libdlmpc_timing.so python tools/phase_profile.py N [t_sim] [twophase]
+(locality and horizon from DLMPC_PP_D / DLMPC_PP_T, default d=3, T=10)"""
 import os, sys
 sys.path.insert(0, '.')
 import numpy as np
@@ -7,7 +8,8 @@ import paper_2103_14990_b200 as pb
 n = int(sys.argv[1]); t_sim = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 if len(sys.argv) > 3 and sys.argv[3] == "twophase":
     os.environ["DLMPC_FORCE_TWOPHASE"] = "1"
-system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=n, d=3, horizon=10, t_sim=t_sim, seed=1))
+system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=n, d=int(os.environ.get("DLMPC_PP_D", 3)),
+                                                      horizon=int(os.environ.get("DLMPC_PP_T", 10)), t_sim=t_sim, seed=1))
 sess = pb.DlmpcSession(system, spec, mask, "b200")
 sess.simulate(x0, t_sim)
 sess.device.phase_times(reset=True)
