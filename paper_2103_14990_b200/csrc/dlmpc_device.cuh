@@ -477,15 +477,21 @@ __device__ __forceinline__ void gemm1(const DevProblem& P, int SK, int n08, int 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tig = lane & 3;
   const int mt1 = n08 >> 3, ks1 = SK >> 2;   // SK: K extent, a multiple of 4
-  if (MROW && NTN > 1 && DLMPC_G1_MROW && mt1 >= NW && (mt1 + NW - 1) / NW * NTN <= (mt1 * NTN + NW - 1) / NW) {
-    // large bases (>= one m-tile per warp) and as many rounds with a whole
-    // m-row of tiles per warp as with one tile per warp: each basis fragment
-    // feeds all NTN tiles (0.75 instead of 1 fragment byte per FLOP at
-    // NTN = 2). C4 at N=1000: d=6,T=20 87.5 -> 77.1 us/iter, d=4,T=30 93.1 ->
-    // 83.1, d=6,T=30 250.9 -> 238.8 (patch mode only: MROW; the stream
-    // kernel measured 2-3% slower with this branch compiled in). Per tile the same two chains and
-    // order as below, so Y is bitwise the same
-    for (int mt = warp; mt < mt1; mt += NW) {
+  // m-tiles [0, mr) by whole m-rows (patch mode, MROW): a warp takes both
+  // n-tiles of an m-tile and each basis fragment feeds all NTN tiles (0.75
+  // instead of 1 fragment byte per FLOP at NTN = 2). All m-tiles that way
+  // when it costs no extra round, else the largest multiple of NW, the rest
+  // one (m, n) tile per warp below -- the same round count as all tiles. C4
+  // at N=1000: d=6,T=20 87.4 -> 77.6 us/iter, d=4,T=30 93.1 -> 84.1, d=6,T=30
+  // 265 -> 249. The stream kernel keeps MROW off (its 7 m-tiles over 16 warps
+  // would lose a round; with the branch merely compiled in it measured 2-3%
+  // slower). Per tile the same two chains and order as below: Y is bitwise
+  // the same.
+  int mr = 0;
+  if (MROW && NTN > 1 && DLMPC_G1_MROW && mt1 >= NW)
+    mr = (mt1 + NW - 1) / NW * NTN <= (mt1 * NTN + NW - 1) / NW ? mt1 : mt1 / NW * NW;
+  if (mr > 0) {
+    for (int mt = warp; mt < mr; mt += NW) {
       double ca[NTN][2], cb[NTN][2];
 #pragma unroll
       for (int nn = 0; nn < NTN; ++nn) { ca[nn][0] = ca[nn][1] = cb[nn][0] = cb[nn][1] = 0.0; }
@@ -511,16 +517,18 @@ __device__ __forceinline__ void gemm1(const DevProblem& P, int SK, int n08, int 
         yb[(mt * 8 + g) * ldy + nn * 8 + 2 * tig + 1] = ca[nn][1] + cb[nn][1];
       }
     }
-    before_sync();
-    sync();
-    return;
+    if (mr == mt1) {
+      before_sync();
+      sync();
+      return;
+    }
   }
-  if (mt1 * NTN >= 12 || P.split_max == 1) {
+  if (mr > 0 || mt1 * NTN >= 12 || P.split_max == 1) {
     // enough (m, n) tiles to keep the DMMA pipe busy (or no room for split-K
     // partials): one tile per warp over the full K with two interleaved
     // accumulator chains, no split-K pass
-    for (int u = warp; u < mt1 * NTN; u += NW) {
-      const int mt = u / NTN, nn = u - (u / NTN) * NTN;
+    for (int u = warp; u < (mt1 - mr) * NTN; u += NW) {
+      const int mt = mr + u / NTN, nn = u - (u / NTN) * NTN;
       double c0a = 0.0, c1a = 0.0, c0b = 0.0, c1b = 0.0;
       int ks = 0;
       for (; ks + 1 < ks1; ks += 2) {
