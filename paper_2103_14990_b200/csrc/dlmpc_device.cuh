@@ -40,6 +40,9 @@ namespace dlmpc {
 #ifndef DLMPC_G1_MROW
 #define DLMPC_G1_MROW 1
 #endif
+#ifndef DLMPC_STREAM_MROW
+#define DLMPC_STREAM_MROW 0
+#endif
 
 // Optional per-phase timers (profiling build only: -DDLMPC_PHASE_TIMING).
 // Thread 0 of every CTA accumulates SM-cycle deltas per phase into
@@ -469,7 +472,7 @@ struct GroupBar {   // barrier over the first NW warps
 };
 
 // NW warps (warp ids 0..NW-1) run the GEMMs; `sync` is their barrier.
-template <int TC, class Hook = NoHook, int NW = kWarps, class Sync = CtaBar, bool MROW = false>
+template <int TC, class Hook = NoHook, int NW = kWarps, class Sync = CtaBar, int MROW = 0>
 __device__ __forceinline__ void gemm1(const DevProblem& P, int SK, int n08, int ldn, const double* nop,
                                       const double* kt, int ldk, double* yb, int ldy, double* yp,
                                       const Hook& before_sync = Hook(), const Sync& sync = Sync()) {
@@ -490,6 +493,8 @@ __device__ __forceinline__ void gemm1(const DevProblem& P, int SK, int n08, int 
   int mr = 0;
   if (MROW && NTN > 1 && DLMPC_G1_MROW && mt1 >= NW)
     mr = (mt1 + NW - 1) / NW * NTN <= (mt1 * NTN + NW - 1) / NW ? mt1 : mt1 / NW * NW;
+  else if (MROW == 2 && NTN > 1)
+    mr = mt1;
   if (mr > 0) {
     for (int mt = warp; mt < mr; mt += NW) {
       double ca[NTN][2], cb[NTN][2];
@@ -888,7 +893,7 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
   if (TC == 8 && nt <= 2 && P.small_gemv && n08 * 10 <= kThreads)
     gemv1_small<TC>(S, n08, ldn, nop, kt, ldk, yp, yb, ldy, nt);
   else
-    gemm1<TC, NoHook, kWarps, CtaBar, true>(P, S8, n08, ldn, nop, kt, ldk, yb, ldy, yp);
+    gemm1<TC, NoHook, kWarps, CtaBar, 1>(P, S8, n08, ldn, nop, kt, ldk, yb, ldy, yp);
   PT_LAP(P, 2)
   // GEMM 2: O[t][p] = sum_a N[p][a] Y[a][t]  (M = S, N = TC, K = n0) -> kt
   StoreO epi{kt, ldk};
@@ -1813,7 +1818,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       double xn = 0.0;   // x of the next chunk's columns (meta written after GEMM 1)
       if (has_next && tid < ce[CHW + 2]) xn = ld_cg(x + ce[CHW + 1] + tid);
       const double* nop = OPS ? smem : P.null_pool + P.class_null_off[ce[0]];
-      gemm1<TC>(P, S4, n08, ldn, nop, kt, ldk, yb, P.ldy, yp, LamWait{bars + 2, (ph >> 2) & 1u});
+      gemm1<TC, LamWait, kWarps, CtaBar, DLMPC_STREAM_MROW>(P, S4, n08, ldn, nop, kt, ldk, yb, P.ldy, yp,
+                                                            LamWait{bars + 2, (ph >> 2) & 1u});
       ph ^= 4u;
       if (has_next && tid < TC) {
         long long* mm = meta0 + (mb ^ 1) * 4 * TC;
