@@ -486,12 +486,12 @@ __device__ __forceinline__ void gemm1(const DevProblem& P, int SK, int n08, int 
   // when it costs no extra round, else the largest multiple of NW, the rest
   // one (m, n) tile per warp below -- the same round count as all tiles. C4
   // at N=1000: d=6,T=20 87.4 -> 77.6 us/iter, d=4,T=30 93.1 -> 84.1, d=6,T=30
-  // 265 -> 249. The stream kernel keeps MROW off (its 7 m-tiles over 16 warps
+  // 265 -> 249, d=5,T=10 (12 m-tiles) 27.5 -> 25.6. The stream kernel keeps MROW off (its 7 m-tiles over 16 warps
   // would lose a round; with the branch merely compiled in it measured 2-3%
   // slower). Per tile the same two chains and order as below: Y is bitwise
   // the same.
   int mr = 0;
-  if (MROW && NTN > 1 && DLMPC_G1_MROW && mt1 >= NW)
+  if (MROW && NTN > 1 && DLMPC_G1_MROW)
     mr = (mt1 + NW - 1) / NW * NTN <= (mt1 * NTN + NW - 1) / NW ? mt1 : mt1 / NW * NW;
   else if (MROW == 2 && NTN > 1)
     mr = mt1;
