@@ -31,3 +31,9 @@ for b in [int(np.argmax(tot)), int(np.argsort(tot)[len(tot) // 2])]:
 snames = ["rowdata+bar", "phimeta", "control+plant", "bar"]
 print("  per MPC step (us): " + " ".join(f"{nm}={st[:, k].max():.2f}" for k, nm in enumerate(snames))
       + f" total={st.sum(axis=1).max():.2f}  (device {1e3 * ms / t_sim:.2f} per step)")
+if os.environ.get("DLMPC_PP_CTAS"):   # per-CTA compute (phases before the publish), slowest first
+    comp = pt[:, :5].sum(axis=1)
+    order = np.argsort(-comp)
+    print("  compute per CTA (us): " + " ".join(f"{b}:{comp[b]:.1f}" for b in order[:12]) + " ... "
+          + " ".join(f"{b}:{comp[b]:.1f}" for b in order[-6:]))
+    print("  compute quantiles (us): " + " ".join(f"{q}:{np.quantile(comp, q):.1f}" for q in (0, .1, .5, .9, 1)))
