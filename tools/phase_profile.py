@@ -37,3 +37,5 @@ if os.environ.get("DLMPC_PP_CTAS"):   # per-CTA compute (phases before the publi
     print("  compute per CTA (us): " + " ".join(f"{b}:{comp[b]:.1f}" for b in order[:12]) + " ... "
           + " ".join(f"{b}:{comp[b]:.1f}" for b in order[-6:]))
     print("  compute quantiles (us): " + " ".join(f"{q}:{np.quantile(comp, q):.1f}" for q in (0, .1, .5, .9, 1)))
+    for b in order[:3]:
+        print(f"  slow CTA {b}: " + " ".join(f"{nm}={pt[b, k]:.2f}" for k, nm in enumerate(names[:5])))
