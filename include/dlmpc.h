@@ -245,6 +245,11 @@ int dlmpc_phase_times(dlmpc_handle* h, uint64_t* out, int reset);
  * kernel mode (0 patch, 1 two-phase, 2 exact, 3 stream), work units. */
 int dlmpc_info(const dlmpc_handle* h, int64_t* out9);
 
+/* Measured FP64 tensor-core (DMMA m8n8k4) peak of `device` in TFLOP/s: the
+ * denominator of bench.py's FP64 roofline fraction (no reference counterpart;
+ * MEASURED_PEAKS.json has HBM and bf16 only). */
+int dlmpc_fp64_peak(int device, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,18 +51,32 @@ class OracleSolver:
         self.phi_c = np.zeros((n_c, d_c)); self.psi_c = np.zeros((n_c, d_c)); self.lam_c = np.zeros((n_c, d_c))
         self.psi_prev_c = np.zeros((n_c, d_c))
         self.pri_c = np.zeros(n_c); self.dual_c = np.zeros(n_c)
-        # group columns by operator shape; stack their operators once
+        # group columns by operator shape; stack their operators once. Columns
+        # whose precomps share ONE g / projector object (the class-built
+        # list of precompute_column_solvers) keep a single broadcast copy:
+        # the (cols x m x s) product is still materialised before the
+        # pairwise sum, so each column's reduction is unchanged, and N=10^4
+        # needs 0.5 MB instead of 10 GB of operators.
         groups = {}
         for c, pre in enumerate(col_solvers):
-            groups.setdefault(pre.g.shape, []).append(c)
+            groups.setdefault((pre.g.shape, id(pre.g), id(pre.projector)), []).append(c)
+        shared = len(groups) < len(col_solvers) // 2
+        if not shared:
+            groups = {}
+            for c, pre in enumerate(col_solvers):
+                groups.setdefault((pre.g.shape, 0, 0), []).append(c)
         self.groups = []
-        for shape in sorted(groups):
-            cols = np.asarray(groups[shape], dtype=np.int64)
-            n = shape[1]
+        for key in sorted(groups, key=lambda k: (k[0], groups[k][0])):
+            cols = np.asarray(groups[key], dtype=np.int64)
+            n = key[0][1]
+            if shared:
+                g = col_solvers[cols[0]].g[None]
+                P = col_solvers[cols[0]].projector[None]
+            else:
+                g = np.stack([col_solvers[c].g for c in cols])
+                P = np.stack([col_solvers[c].projector for c in cols])
             self.groups.append(dict(
-                cols=cols,
-                g=np.stack([col_solvers[c].g for c in cols]),
-                P=np.stack([col_solvers[c].projector for c in cols]),
+                cols=cols, shared=shared, g=g, P=P,
                 rhs=np.stack([col_solvers[c].rhs for c in cols]),
                 cells=cols[:, None] * d_c + np.arange(n)[None, :]))
         self.row_data = None
@@ -110,12 +124,15 @@ class OracleSolver:
         psi, prev = self.psi_c.ravel(), self.psi_prev_c.ravel()
         cells = grp["cells"][i0:i1]
         k = phi[cells] + lam[cells]
-        resid = grp["rhs"][i0:i1] - (grp["g"][i0:i1] * k[:, None, :]).sum(axis=2)
+        g = grp["g"] if grp["shared"] else grp["g"][i0:i1]
+        P = grp["P"] if grp["shared"] else grp["P"][i0:i1]
+        resid = grp["rhs"][i0:i1] - (g * k[:, None, :]).sum(axis=2)
         prev[cells] = psi[cells]
-        psi[cells] = k + (grp["P"][i0:i1] * resid[:, None, :]).sum(axis=2)
+        psi[cells] = k + (P * resid[:, None, :]).sum(axis=2)
 
     def _cols(self, lo, hi):
         for grp in self.groups:
+            # a group's columns are ascending but need not be contiguous
             i0 = int(np.searchsorted(grp["cols"], lo))
             i1 = int(np.searchsorted(grp["cols"], hi))
             # small chunks keep the (cols x m x s) product temporaries in cache
@@ -142,12 +159,47 @@ class OracleSolver:
         self.lam_r[:] = vals
         return float(self.pri_c.max()), float(self.dual_c.max())
 
-    def solve(self, row_data, max_iters, eps_pri, eps_dual):
+    def iterate_sequential(self):
+        """One iteration in the reference's `sequential` schedule
+        (strategies.py:262-281, the paper's single-thread "CPU ADMM"): every
+        stage called one row / one column at a time, stage after stage, on
+        one core. Same arithmetic as `iterate` (batching never changes an
+        item's reduction, admm.py:6-10); only the per-item call structure --
+        which is where that schedule's time goes -- differs."""
+        t = self.t
+        if not hasattr(self, "_col_slot"):
+            self._col_slot = {}
+            for grp in self.groups:
+                for i, c in enumerate(grp["cols"]):
+                    self._col_slot[int(c)] = (grp, i)
+        for r in range(t.n_rows):
+            self._phi(r, r + 1)
+        vals = self.phi_r.ravel()[self._phi_src]
+        vals[~t.col_valid] = 0.0
+        self.phi_c[:] = vals
+        for c in range(t.n_cols):
+            grp, i = self._col_slot[c]
+            self._psi_block(grp, i, i + 1)
+        for c in range(t.n_cols):
+            self.lam_c[c:c + 1] += self.phi_c[c:c + 1] - self.psi_c[c:c + 1]
+        for c in range(t.n_cols):
+            self.pri_c[c:c + 1] = np.abs(self.phi_c[c:c + 1] - self.psi_c[c:c + 1]).max(axis=-1)
+            self.dual_c[c:c + 1] = self.rho * np.abs(self.psi_c[c:c + 1] - self.psi_prev_c[c:c + 1]).max(axis=-1)
+        vals = self.psi_c.ravel()[self._row_src]
+        vals[~t.row_valid] = 0.0
+        self.psi_r[:] = vals
+        vals = self.lam_c.ravel()[self._row_src]
+        vals[~t.row_valid] = 0.0
+        self.lam_r[:] = vals
+        return float(self.pri_c.max()), float(self.dual_c.max())
+
+    def solve(self, row_data, max_iters, eps_pri, eps_dual, sequential=False):
         """admm.py:315-347: returns (iterations, history, converged)."""
         self.row_data = row_data
         hist = []
+        step = self.iterate_sequential if sequential else self.iterate
         for _ in range(max_iters):
-            pri, dual = self.iterate()
+            pri, dual = step()
             hist.append((pri, dual))
             if pri <= eps_pri and dual <= eps_dual:
                 return len(hist), hist, True
@@ -183,7 +235,7 @@ def step_dynamics(a, b, x, u):
 
 
 def simulate(system, spec, tables, col_solvers, x0, t_sim, warm_start=True, workers=1,
-             solver=None):
+             solver=None, sequential=False):
     """Closed loop of admm.py:437-540 (recurring phases). Returns dict with
     states, inputs, step_iterations, histories; raises nothing -- failures are
     reported as `status` ('ok' | 'not_converged' | 'row_infeasible') + `step`."""
@@ -206,7 +258,7 @@ def simulate(system, spec, tables, col_solvers, x0, t_sim, warm_start=True, work
                 break
             if not warm_start:
                 solver.zero_()
-            n_it, hist, ok = solver.solve(rd, spec.max_iters, spec.eps_pri, spec.eps_dual)
+            n_it, hist, ok = solver.solve(rd, spec.max_iters, spec.eps_pri, spec.eps_dual, sequential)
             hists.append(hist)
             if not ok:
                 status, at = "not_converged", (step, None)
@@ -219,5 +271,5 @@ def simulate(system, spec, tables, col_solvers, x0, t_sim, warm_start=True, work
     finally:
         if own:
             solver.close()
-    return dict(states=np.array(states), inputs=np.array(inputs).reshape(len(inputs), -1),
+    return dict(states=np.array(states), inputs=np.array(inputs).reshape(len(inputs), system.n_inputs),
                 step_iterations=iters, histories=hists, status=status, at=at, solver=solver)

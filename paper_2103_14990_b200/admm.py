@@ -262,6 +262,32 @@ def _spec_fingerprint(spec: ProblemSpec) -> bytes:
     return h.digest()
 
 
+def _plant_views(system: LtiSystem, mask: LocalityMask):
+    arrs = []
+    for m in (system.a, system.b):
+        arrs += [m.data, m.indices, m.indptr]
+    if mask.compact is not None:   # explicit masks hold immutable support tuples
+        arrs += [mask.compact["ball_ptr"], mask.compact["ball_idx"]]
+    return arrs, (mask.n_rows, mask.n_cols, mask.d, mask.d_row, mask.d_col)
+
+
+def _plant_arrays(system: LtiSystem, mask: LocalityMask):
+    """Copies of what a cached session was built from besides the spec: the
+    plant's CSR arrays (A, B) and the locality structure. The reference
+    rebuilds its operators on every dlmpc_simulate call (admm.py:470-475), so
+    an in-place edit of any of these between calls must not hit a stale
+    session."""
+    arrs, key = _plant_views(system, mask)
+    return [np.array(a, copy=True) for a in arrs], key
+
+
+def _plant_unchanged(sess, system: LtiSystem, mask: LocalityMask) -> bool:
+    arrs, key = sess._plant
+    cur, cur_key = _plant_views(system, mask)
+    return key == cur_key and len(arrs) == len(cur) and \
+        all(a.shape == np.shape(b) and np.array_equal(a, b) for a, b in zip(arrs, cur))
+
+
 class DlmpcSession:
     """Precomputed closed-loop session on one GPU: the reference's
     `precompute_global` (dynamics operator, column solvers) plus the device
@@ -282,6 +308,7 @@ class DlmpcSession:
         self.precompute_s = time.perf_counter() - t0
         self._fp = _spec_fingerprint(spec)
         self._spec_arrays = _spec_arrays(spec)
+        self._plant = _plant_arrays(system, mask)
 
     def simulate(self, x0, t_sim: int, warm_start: bool = True):
         """Closed loop on device; returns (Trajectory, device_ms)."""
@@ -325,7 +352,7 @@ def _cached_session(system, spec, mask, strat):
     if hit is not None:
         ref_sys, ref_spec, ref_mask, sess = hit
         if ref_sys() is system and ref_spec() is spec and ref_mask() is mask \
-                and _spec_unchanged(sess, spec):
+                and _spec_unchanged(sess, spec) and _plant_unchanged(sess, system, mask):
             return sess, True
         sess.close()
         del _SESSIONS[key]

@@ -96,21 +96,41 @@ int ld_frag(int n) {   // smallest ld >= n with ld % 16 in {4, 12}: conflict-fre
   return ld;
 }
 
+// Grow-only run buffers. The replacements are allocated first and swapped in
+// only when every allocation succeeded: a failed grow leaves the handle with
+// its old (valid) buffers and capacities, never with freed pointers.
+template <class T>
+void swap_in(T** field, T* fresh) {
+  if (*field) cudaFree(*field);
+  *field = fresh;
+}
+
 int ensure_run_buffers(dlmpc_handle* h, int max_iters, int t_sim) {
   if (max_iters > h->max_iters_cap) {
-    if (h->d_hist) cudaFree(h->d_hist);
-    if (h->P.resid) cudaFree(h->P.resid);
-    CUDA_OR_FAIL(h, cudaMalloc(&h->d_hist, sizeof(double) * 2 * max_iters));
-    CUDA_OR_FAIL(h, cudaMalloc(&h->P.resid, sizeof(unsigned long long) * 2 * max_iters));
+    double* hist = nullptr; unsigned long long* resid = nullptr;
+    cudaError_t e = cudaMalloc(&hist, sizeof(double) * 2 * max_iters);
+    if (e == cudaSuccess) e = cudaMalloc(&resid, sizeof(unsigned long long) * 2 * max_iters);
+    if (e != cudaSuccess) {
+      if (hist) cudaFree(hist);
+      return fail(h, DLMPC_CUDA_ERROR, std::string("run buffers: ") + cudaGetErrorString(e));
+    }
+    swap_in(&h->d_hist, hist);
+    swap_in(&h->P.resid, resid);
     h->max_iters_cap = max_iters;
   }
   if (t_sim > h->states_cap) {
-    if (h->d_step_iters) cudaFree(h->d_step_iters);
-    if (h->d_states) cudaFree(h->d_states);
-    if (h->d_inputs) cudaFree(h->d_inputs);
-    CUDA_OR_FAIL(h, cudaMalloc(&h->d_step_iters, sizeof(int) * t_sim));
-    CUDA_OR_FAIL(h, cudaMalloc(&h->d_states, sizeof(double) * (size_t)(t_sim + 1) * h->P.n_cols));
-    CUDA_OR_FAIL(h, cudaMalloc(&h->d_inputs, sizeof(double) * (size_t)t_sim * (h->P.n_inputs ? h->P.n_inputs : 1)));
+    int* it = nullptr; double* st = nullptr; double* in = nullptr;
+    cudaError_t e = cudaMalloc(&it, sizeof(int) * t_sim);
+    if (e == cudaSuccess) e = cudaMalloc(&st, sizeof(double) * (size_t)(t_sim + 1) * h->P.n_cols);
+    if (e == cudaSuccess) e = cudaMalloc(&in, sizeof(double) * (size_t)t_sim * (h->P.n_inputs ? h->P.n_inputs : 1));
+    if (e != cudaSuccess) {
+      if (it) cudaFree(it);
+      if (st) cudaFree(st);
+      return fail(h, DLMPC_CUDA_ERROR, std::string("closed-loop buffers: ") + cudaGetErrorString(e));
+    }
+    swap_in(&h->d_step_iters, it);
+    swap_in(&h->d_states, st);
+    swap_in(&h->d_inputs, in);
     h->states_cap = t_sim;
   }
   return DLMPC_OK;
@@ -176,6 +196,10 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
   const long long limit = (optin - 1024) / 8;   // doubles
   const int G = h->sm_count;
   h->grid = G;
+  {
+    const char* e = getenv("DLMPC_G1_MROW");
+    P.g1_mrow = (e && e[0] == '0') ? 0 : 1;
+  }
   const char* force = getenv("DLMPC_FORCE_TWOPHASE");
   h->mode = pr->exact ? kExact : ((pr->contiguous && !(force && force[0] == '1')) ? kPatch : kTwoPhase);
   if (h->mode == kExact) {
@@ -1156,6 +1180,55 @@ int dlmpc_phase_times(dlmpc_handle* h, uint64_t* out, int reset) {
   if (!h || !out) return DLMPC_BAD_ARGUMENT;
   CUDA_OR_FAIL(h, cudaMemcpy(out, h->P.phase_ns, sizeof(uint64_t) * 16 * h->grid, cudaMemcpyDeviceToHost));
   if (reset) CUDA_OR_FAIL(h, cudaMemset(h->P.phase_ns, 0, sizeof(uint64_t) * 16 * h->grid));
+  return DLMPC_OK;
+}
+
+// FP64 tensor-core peak of this GPU, measured live (the roofline denominator
+// of the FP64 fraction; MEASURED_PEAKS.json carries HBM and bf16 only): every
+// warp runs 8 independent m8n8k4 DMMA accumulation chains, 4 CTAs x 256
+// threads per SM, best of 3 launches of ~20 ms.
+__global__ void fp64_dmma_probe_kernel(double* out, int iters) {
+  const double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { c[i][0] = 0.0; c[i][1] = 0.0; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma(c[i][0], c[i][1], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[0] = s;   // keeps the chains live
+}
+
+int dlmpc_fp64_peak(int device, double* tflops) {
+  if (!tflops) return fail(nullptr, DLMPC_BAD_ARGUMENT, "null argument");
+  if (cudaSetDevice(device) != cudaSuccess) return fail(nullptr, DLMPC_NO_DEVICE, "cudaSetDevice failed");
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+    return fail(nullptr, DLMPC_CUDA_ERROR, "device attribute");
+  double* out = nullptr;
+  cudaEvent_t e0, e1;
+  if (cudaMalloc(&out, 64) != cudaSuccess) return fail(nullptr, DLMPC_CUDA_ERROR, "cudaMalloc");
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int blocks = sms * 4, threads = 256, iters = 4000;
+  fp64_dmma_probe_kernel<<<blocks, threads>>>(out, 64);
+  double best = 0.0;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0);
+    fp64_dmma_probe_kernel<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    if (cudaEventSynchronize(e1) != cudaSuccess) break;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flop = 2.0 * 256 * 8 * (double)iters * blocks * (threads / 32);   // 8x8x4 MACs per DMMA
+    best = std::max(best, flop / (ms * 1e-3) / 1e12);
+  }
+  const cudaError_t err = cudaGetLastError();
+  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaFree(out);
+  if (err != cudaSuccess || best <= 0.0) return fail(nullptr, DLMPC_CUDA_ERROR, "fp64 probe failed");
+  *tflops = best;
   return DLMPC_OK;
 }
 

@@ -139,6 +139,7 @@ struct DevProblem {
   int small_gemv;              // patch mode: DFMA GEMV for GEMM 1 of chunks with <= 2 columns
   int rb_gemv;                 // patch mode, TC 8: register-blocked GEMV pair for chunks of <= 2 columns
   int stash_cols;              // columns per ψ,λ staging buffer (TC, or 2 with rb_gemv)
+  int g1_mrow;                 // GEMM 1 by whole m-rows where it pays (DLMPC_G1_MROW=0 disables: A/B tests)
 };
 
 struct RunArgs {
@@ -187,6 +188,11 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
                :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// Generic-proxy global stores (the stream epilogue's ψ', λ') that other CTAs
+// read with TMA bulk copies (async proxy) after the next grid barrier: the
+// writers order them for the async proxy before arriving (PTX memory model,
+// proxy fences).
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
 
 // Stage ψ,λ of nt consecutive columns starting at c0 into `st`
 // ([t][ψ|λ][ldk]) with 16-byte cp.async copies (bypassing L1, like ld.cg);
@@ -245,8 +251,20 @@ struct ProdRow {   // row[j] * v[j]
   __device__ double operator()(int j) const { return __dmul_rn(row[j], v[j]); }
 };
 
+// Max of residual magnitudes that lets NaN win, as np.max does (reference
+// admm.py:216-217, strategies.py:178-183): the operands are compared as their
+// bit patterns with the sign cleared, so NaN > +inf > every finite value and
+// a diverging iterate publishes NaN (the stop test `NaN <= eps` then fails
+// and the solve ends in NotConverged) instead of fmax silently dropping it.
+// Also |b| for free: rmax(acc, d) == max(acc, |d|) for acc >= 0.
+__device__ __forceinline__ double rmax(double a, double b) {
+  const long long ia = __double_as_longlong(a) & 0x7fffffffffffffffLL;
+  const long long ib = __double_as_longlong(b) & 0x7fffffffffffffffLL;
+  return __longlong_as_double(ia > ib ? ia : ib);
+}
+
 __device__ __forceinline__ double block_max(double v, double* red) {
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 16; o > 0; o >>= 1) v = rmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __syncthreads();
   if (lane == 0) red[warp] = v;
@@ -254,7 +272,7 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   double m = 0.0;
   if (threadIdx.x < 32) {
     m = threadIdx.x < kWarps ? red[threadIdx.x] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    for (int o = 16; o > 0; o >>= 1) m = rmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   }
   return m;   // valid in thread 0
 }
@@ -262,8 +280,8 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 __device__ __forceinline__ void publish_residuals(const DevProblem& P, int it, double pri_m,
                                                   double dual_m, double* red) {
   for (int o = 16; o > 0; o >>= 1) {
-    pri_m = fmax(pri_m, __shfl_xor_sync(0xffffffffu, pri_m, o));
-    dual_m = fmax(dual_m, __shfl_xor_sync(0xffffffffu, dual_m, o));
+    pri_m = rmax(pri_m, __shfl_xor_sync(0xffffffffu, pri_m, o));
+    dual_m = rmax(dual_m, __shfl_xor_sync(0xffffffffu, dual_m, o));
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) { red[2 * warp] = pri_m; red[2 * warp + 1] = dual_m; }
@@ -271,8 +289,8 @@ __device__ __forceinline__ void publish_residuals(const DevProblem& P, int it, d
   if (warp == 0) {
     double p = lane < kWarps ? red[2 * lane] : 0.0, d = lane < kWarps ? red[2 * lane + 1] : 0.0;
     for (int o = 16; o > 0; o >>= 1) {
-      p = fmax(p, __shfl_xor_sync(0xffffffffu, p, o));
-      d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+      p = rmax(p, __shfl_xor_sync(0xffffffffu, p, o));
+      d = rmax(d, __shfl_xor_sync(0xffffffffu, d, o));
     }
     if (lane == 0) {
       atomicMax(P.resid + 2 * it, static_cast<unsigned long long>(__double_as_longlong(p)));
@@ -298,8 +316,8 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 __device__ __forceinline__ void publish_barrier(const DevProblem& P, int it, double pri_m, double dual_m,
                                                 double* red, unsigned target) {
   for (int o = 16; o > 0; o >>= 1) {
-    pri_m = fmax(pri_m, __shfl_xor_sync(0xffffffffu, pri_m, o));
-    dual_m = fmax(dual_m, __shfl_xor_sync(0xffffffffu, dual_m, o));
+    pri_m = rmax(pri_m, __shfl_xor_sync(0xffffffffu, pri_m, o));
+    dual_m = rmax(dual_m, __shfl_xor_sync(0xffffffffu, dual_m, o));
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) { red[2 * warp] = pri_m; red[2 * warp + 1] = dual_m; }
@@ -307,8 +325,8 @@ __device__ __forceinline__ void publish_barrier(const DevProblem& P, int it, dou
   if (warp == 0) {
     double p = lane < kWarps ? red[2 * lane] : 0.0, d = lane < kWarps ? red[2 * lane + 1] : 0.0;
     for (int o = 16; o > 0; o >>= 1) {
-      p = fmax(p, __shfl_xor_sync(0xffffffffu, p, o));
-      d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+      p = rmax(p, __shfl_xor_sync(0xffffffffu, p, o));
+      d = rmax(d, __shfl_xor_sync(0xffffffffu, d, o));
     }
     if (lane == 0) {
       atomicMax(P.resid + 2 * it, static_cast<unsigned long long>(__double_as_longlong(p)));
@@ -491,7 +509,7 @@ __device__ __forceinline__ void gemm1(const DevProblem& P, int SK, int n08, int 
   // slower). Per tile the same two chains and order as below: Y is bitwise
   // the same.
   int mr = 0;
-  if (MROW && NTN > 1 && DLMPC_G1_MROW)
+  if (MROW && NTN > 1 && DLMPC_G1_MROW && P.g1_mrow)   // P.g1_mrow: runtime switch (tests: bitwise A/B)
     mr = (mt1 + NW - 1) / NW * NTN <= (mt1 * NTN + NW - 1) / NW ? mt1 : mt1 / NW * NW;
   else if (MROW == 2 && NTN > 1)
     mr = mt1;
@@ -933,8 +951,8 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
             const double d = __dsub_rn(phi, pn);
             psi_n[pos0 + p] = pn;
             lam_n[pos0 + p] = __dadd_rn(lm[u], d);
-            pri_m = fmax(pri_m, fabs(d));
-            dual_m = fmax(dual_m, fabs(__dsub_rn(pn, ps[u])));
+            pri_m = rmax(pri_m, fabs(d));
+            dual_m = rmax(dual_m, fabs(__dsub_rn(pn, ps[u])));
           }
         }
       }
@@ -1039,8 +1057,8 @@ __device__ void rb_chunk_al(const DevProblem& P, int k, int nt, double* psi_n, d
     const double d = __dsub_rn(phi, pn);
     psi_n[e_pos + ep] = pn;
     lam_n[e_pos + ep] = __dadd_rn(e_lm, d);
-    pri_m = fmax(pri_m, fabs(d));
-    dual_m = fmax(dual_m, fabs(__dsub_rn(pn, e_ps)));
+    pri_m = rmax(pri_m, fabs(d));
+    dual_m = rmax(dual_m, fabs(__dsub_rn(pn, e_ps)));
   };
   PT_LAP(P, 1)
   gemv_pair_rb<RB_AL>(S, op, kf, smem + P.off_yp, smem + P.off_y, nt, epi);
@@ -1479,8 +1497,8 @@ struct StreamEpi {
         const long long pos = m_pos[t] + p;
         psi_n[pos] = pn;
         lam_n[pos] = ln;
-        pri_m = fmax(pri_m, fabs(__dsub_rn(ln, lm)));
-        dual_m = fmax(dual_m, fabs(__dsub_rn(pn, ps)));
+        pri_m = rmax(pri_m, fabs(__dsub_rn(ln, lm)));
+        dual_m = rmax(dual_m, fabs(__dsub_rn(pn, ps)));
         const double v = __dsub_rn(pn, ln);
         if (paired) contrib = e ? fma(v, m_x[t], contrib) : __dmul_rn(v, m_x[t]);
         else lt[t * ldl + p] = v;
@@ -1918,8 +1936,8 @@ __device__ void column_stage_exact(const DevProblem& P, int b, const double* x, 
       const double d = __dsub_rn(phi_s[p], pn);
       psi_n[pos] = pn;
       lam_n[pos] = __dadd_rn(lam_s[p], d);
-      pri_m = fmax(pri_m, fabs(d));
-      dual_m = fmax(dual_m, fabs(__dsub_rn(pn, psi_s[p])));
+      pri_m = rmax(pri_m, fabs(d));
+      dual_m = rmax(dual_m, fabs(__dsub_rn(pn, psi_s[p])));
     }
     __syncthreads();
   }
@@ -2046,6 +2064,7 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
       row_data_stage(P, x, bad_slot);
       if ((R.cold_start && step == 0) || !R.warm_start) zero_iterate(P, b);
     }
+    if (MODE == kStream) fence_proxy_async_global();   // zeroed ψ, λ are read by TMA
     grid.sync();
     if (R.closed_loop) {
       const int bad = *reinterpret_cast<volatile int*>(bad_slot);
@@ -2087,6 +2106,7 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
         const int itg = it + (R.closed_loop ? 0 : R.it_base);
         if (P.cta_gop && P.cta_gop[blockIdx.x]) stream_iteration<TC, false>(P, b, x, it, itg, smem, cur, ph);
         else stream_iteration<TC, true>(P, b, x, it, itg, smem, cur, ph);
+        fence_proxy_async_global();
         PT_START
       } else {
         PT_START
@@ -2187,18 +2207,18 @@ __global__ void audit_entries_kernel(DevProblem P, int b, const double* x, const
     const double phi = phi_given ? phi_given[q]
                                  : make_phi<EXACT>(__dsub_rn(P.psi[b ^ 1][q], P.lam[b ^ 1][q]), P.s_row[ir], xc);
     const double fresh = make_phi<EXACT>(__dsub_rn(P.psi[b][q], P.lam[b][q]), s_fresh[ir], xc);
-    res = fmax(res, fabs(__dsub_rn(fresh, phi)));
-    gap = fmax(gap, fabs(__dsub_rn(phi, P.psi[b][q])));
+    res = rmax(res, fabs(__dsub_rn(fresh, phi)));
+    gap = rmax(gap, fabs(__dsub_rn(phi, P.psi[b][q])));
   }
   for (int o = 16; o > 0; o >>= 1) {
-    res = fmax(res, __shfl_xor_sync(0xffffffffu, res, o));
-    gap = fmax(gap, __shfl_xor_sync(0xffffffffu, gap, o));
+    res = rmax(res, __shfl_xor_sync(0xffffffffu, res, o));
+    gap = rmax(gap, __shfl_xor_sync(0xffffffffu, gap, o));
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) { red[2 * warp] = res; red[2 * warp + 1] = gap; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < (blockDim.x >> 5); ++w) { res = fmax(res, red[2 * w]); gap = fmax(gap, red[2 * w + 1]); }
+    for (int w = 1; w < (blockDim.x >> 5); ++w) { res = rmax(res, red[2 * w]); gap = rmax(gap, red[2 * w + 1]); }
     atomic_max_nonneg(out + 1, res);
     atomic_max_nonneg(out + 2, gap);
   }
@@ -2223,14 +2243,14 @@ __global__ void audit_dynamics_kernel(DevProblem P, int b, double* out) {
         if (v != 0.0) acc = __dadd_rn(acc, __dmul_rn(v, psi[perm[j]]));
       }
       if (i == P.col_pin[c]) acc = __dsub_rn(acc, 1.0);
-      worst = fmax(worst, fabs(acc));
+      worst = rmax(worst, fabs(acc));
     }
   }
-  for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+  for (int o = 16; o > 0; o >>= 1) worst = rmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = worst;
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < (blockDim.x >> 5); ++w) worst = fmax(worst, red[w]);
+    for (int w = 1; w < (blockDim.x >> 5); ++w) worst = rmax(worst, red[w]);
     atomic_max_nonneg(out, worst);
   }
 }

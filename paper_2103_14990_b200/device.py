@@ -59,7 +59,8 @@ EXPORTS = ("dlmpc_create", "dlmpc_destroy", "dlmpc_last_error", "dlmpc_global_er
            "dlmpc_last_timing", "dlmpc_stream", "dlmpc_synchronize", "dlmpc_info",
            "dlmpc_phase_times", "dlmpc_audit", "dlmpc_get_cols", "dlmpc_put_cols",
            "dlmpc_finish_step", "dlmpc_set_halo", "dlmpc_halo_pack", "dlmpc_halo_unpack",
-           "dlmpc_iterate_async", "dlmpc_halo_pack_async", "dlmpc_halo_unpack_async", "dlmpc_set_stream")
+           "dlmpc_iterate_async", "dlmpc_halo_pack_async", "dlmpc_halo_unpack_async", "dlmpc_set_stream",
+           "dlmpc_fp64_peak")
 
 _lib = None
 
@@ -111,8 +112,18 @@ def load_library():
     lib.dlmpc_halo_pack_async.argtypes = [vp, vp]
     lib.dlmpc_halo_unpack_async.argtypes = [vp, vp]
     lib.dlmpc_set_stream.argtypes = [vp, vp]
+    lib.dlmpc_fp64_peak.argtypes = [C.c_int, _f64p]
     _lib = lib
     return lib
+
+
+def fp64_peak_tflops(device: int = 0) -> float:
+    """Measured FP64 DMMA peak of `device` (TFLOP/s), for roofline fractions."""
+    lib = load_library()
+    out = C.c_double(0.0)
+    if lib.dlmpc_fp64_peak(int(device), C.byref(out)) != 0:
+        raise DeviceError("dlmpc_fp64_peak: " + lib.dlmpc_global_error().decode())
+    return float(out.value)
 
 
 def _ptr(a, ctype):

@@ -103,8 +103,26 @@ def setup_fixture(lm, n, t, d):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the N=1000 one-step fixture (~3 min)")
+    ap.add_argument("--c2-seeds", action="store_true",
+                    help="only the C2 closed loops for seeds 1..20 (the bench's timed seeds, ~6 min)")
+    ap.add_argument("--c3", type=int, default=0,
+                    help="only the chain N=<c3>, d=3, T=10 step-0 solve (N=3000: ~15 min, 3 GB)")
     args = ap.parse_args()
     lm = import_reference()
+    if args.c2_seeds:
+        # every seed bench.py cycles through (bench.py: seeds 1..max(8, steps))
+        out = {}
+        for seed in range(1, 21):
+            r = closed_loop(lm, 100, 3, 10, 20, seed)
+            out[f"s{seed}_x0"], out[f"s{seed}_states"] = r["x0"], r["states"]
+            out[f"s{seed}_inputs"], out[f"s{seed}_iters"] = r["inputs"], r["step_iters"]
+            out[f"s{seed}_cost"] = r["cost"]
+            print("seed", seed, list(r["step_iters"]), flush=True)
+        save("c2_loops_seeds1_20", **out)
+        return
+    if args.c3:
+        save(f"c3_n{args.c3}_step0", **closed_loop(lm, args.c3, 3, 10, 1, 1))
+        return
 
     # C1 step 0 known answers + full 20-step loops
     system, spec, mask, tables, op, cs, metas = bundle(lm, 10, 5, 2)

@@ -167,3 +167,17 @@ def test_oracle_phi_rows_match_independent_minimiser():
         np.testing.assert_allclose(s.phi_r[r], phi, rtol=1e-6, atol=1e-7)   # Brent's accuracy
         checked += 1
     assert checked > 50
+
+
+def test_sequential_schedule_restatement_bitwise():
+    """The oracle's `sequential` schedule (one row / column per stage call,
+    the reference's strategies.py:262-281, timed by bench.py as the 1-core
+    "CPU ADMM" baseline) reproduces the reference's C1 closed loop bit for
+    bit."""
+    g = golden("c1_loop_seed1")
+    b = chain_bundle(10, 5, 2)
+    res = admm_ref.simulate(b["system"], b["spec"], b["tables"], b["col_solvers"], g["x0"], 20,
+                            sequential=True)
+    assert res["step_iterations"] == list(g["step_iters"])
+    assert np.array_equal(res["states"], g["states"])
+    assert np.array_equal(res["inputs"], g["inputs"])

@@ -71,10 +71,62 @@ __global__ void my_barrier_kernel(int iters, unsigned* bar, int* sink) {
   if (threadIdx.x == 0 && blockIdx.x == 0) sink[0] = iters;
 }
 
-__global__ void __cluster_dims__(16, 1, 1) cluster_barrier_kernel(int iters, int* sink) {
+// Cluster barrier: no compile-time cluster shape; the launch sets it
+// (cudaLaunchKernelEx + cudaLaunchAttributeClusterDimension). 16-CTA clusters
+// are non-portable and need cudaFuncAttributeNonPortableClusterSizeAllowed.
+__global__ void cluster_barrier_kernel(int iters, int* sink) {
   cg::cluster_group cl = cg::this_cluster();
   for (int i = 0; i < iters; ++i) cl.sync();
+  if (threadIdx.x == 0 && blockIdx.x == 0) sink[0] = iters + (int)cl.num_blocks();
+}
+
+// Split cluster barrier as a persistent kernel would use it: arrive.release
+// by every thread, wait.acquire.
+__global__ void cluster_split_barrier_kernel(int iters, int* sink) {
+  for (int i = 0; i < iters; ++i) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  }
   if (threadIdx.x == 0 && blockIdx.x == 0) sink[0] = iters;
+}
+
+// DSMEM round trip: thread 0 of CTA 0 chases a pointer ring that lives in
+// the shared memory of CTA `peer` of its cluster (ld.shared::cluster).
+__global__ void dsmem_latency_kernel(int iters, int peer, long long* out) {
+  __shared__ unsigned ring[256];
+  cg::cluster_group cl = cg::this_cluster();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) ring[i] = (i * 97 + 13) & 255;
+  cl.sync();
+  if (cl.block_rank() == 0 && threadIdx.x == 0) {
+    unsigned* remote = cl.map_shared_rank(ring, peer);
+    unsigned idx = 0;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) idx = remote[idx];
+    long long t1 = clock64();
+    out[0] = (t1 - t0) / iters;
+    out[1] = idx;
+  }
+  cl.sync();
+}
+
+// L2 round trip for comparison: the same chase over a global ring (ld.cg).
+__global__ void l2_latency_kernel(const unsigned* ring, int iters, long long* out) {
+  unsigned idx = 0;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) idx = __ldcg(ring + idx);
+  long long t1 = clock64();
+  out[0] = (t1 - t0) / iters;
+  out[1] = idx;
+}
+
+static cudaError_t launch_cluster(const void* fn, int grid, int block, int cluster, void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid); cfg.blockDim = dim3(block); cfg.dynamicSmemBytes = 0; cfg.stream = 0;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr; cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 int main() {
@@ -121,12 +173,53 @@ int main() {
     cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
     printf("hand barrier blocks %d: %.3f us/barrier\n", nblk, ms * 1e3 / iters);
   }
+  // cluster barriers (sizes 2..16; 16 is non-portable), one cluster and a
+  // full machine of clusters, 512 threads per CTA like the persistent kernel
+  CK(cudaFuncSetAttribute((const void*)cluster_barrier_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute((const void*)cluster_split_barrier_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute((const void*)dsmem_latency_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  for (int cs : {2, 4, 8, 16}) {
+    for (int full : {0, 1}) {
+      int grid = full ? (sms / cs) * cs : cs;
+      int iters = 20000;
+      void* args[] = {&iters, &sink};
+      CK(launch_cluster((const void*)cluster_barrier_kernel, grid, 512, cs, args));
+      CK(cudaGetLastError()); CK(cudaDeviceSynchronize());
+      int h = 0; CK(cudaMemcpy(&h, sink, 4, cudaMemcpyDeviceToHost));
+      if (h != iters + cs) { printf("cluster(%d) kernel did not run (sink %d)\n", cs, h); continue; }
+      cudaEventRecord(e0);
+      CK(launch_cluster((const void*)cluster_barrier_kernel, grid, 512, cs, args));
+      cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1);
+      cudaEventRecord(e0);
+      CK(launch_cluster((const void*)cluster_split_barrier_kernel, grid, 512, cs, args));
+      cudaEventRecord(e1); CK(cudaEventSynchronize(e1)); float ms2; cudaEventElapsedTime(&ms2, e0, e1);
+      printf("cluster(%d) x %d clusters: cg cluster.sync %.3f us/barrier, arrive.release/wait.acquire %.3f us\n",
+             cs, grid / cs, ms * 1e3 / iters, ms2 * 1e3 / iters);
+    }
+  }
   {
-    int iters = 20000;
-    cluster_barrier_kernel<<<16, 256>>>(iters, sink); CK(cudaDeviceSynchronize());
-    cudaEventRecord(e0); cluster_barrier_kernel<<<16, 256>>>(iters, sink); cudaEventRecord(e1);
-    CK(cudaEventSynchronize(e1)); float ms; cudaEventElapsedTime(&ms, e0, e1);
-    printf("cluster(16) sync: %.3f us/barrier\n", ms * 1e3 / iters);
+    long long* lat; CK(cudaMalloc(&lat, 64));
+    for (int cs : {2, 16}) {
+      for (int peer : {0, 1, cs - 1}) {
+        int iters = 4096;
+        void* args[] = {&iters, &peer, &lat};
+        CK(launch_cluster((const void*)dsmem_latency_kernel, cs, 128, cs, args));
+        CK(cudaGetLastError()); CK(cudaDeviceSynchronize());
+        long long h[2]; CK(cudaMemcpy(h, lat, 16, cudaMemcpyDeviceToHost));
+        printf("DSMEM load round trip, cluster %d, peer rank %d: %lld cycles\n", cs, peer, h[0]);
+      }
+    }
+    unsigned* ring; CK(cudaMalloc(&ring, 1 << 22));
+    unsigned hr[1 << 12];
+    for (int i = 0; i < (1 << 12); ++i) hr[i] = ((i * 1021 + 17) & ((1 << 12) - 1)) * 64;   // 256 B apart
+    unsigned* big = new unsigned[1 << 20]();
+    for (int i = 0; i < (1 << 12); ++i) big[i * 64] = hr[i];
+    CK(cudaMemcpy(ring, big, 1 << 22, cudaMemcpyHostToDevice));
+    l2_latency_kernel<<<1, 1>>>(ring, 4096, lat); CK(cudaDeviceSynchronize());
+    l2_latency_kernel<<<1, 1>>>(ring, 4096, lat); CK(cudaDeviceSynchronize());
+    long long h[2]; CK(cudaMemcpy(h, lat, 16, cudaMemcpyDeviceToHost));
+    printf("L2 load round trip (ld.cg, 1 MB ring, warm): %lld cycles\n", h[0]);
+    delete[] big;
   }
   // launch latency
   {
