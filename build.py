@@ -15,7 +15,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.join(ROOT, "paper_2103_14990_b200")
 SRC_DIR = os.path.join(PKG, "csrc")
 SOURCES = [os.path.join(SRC_DIR, "dlmpc.cu")]
-DEPS = SOURCES + [os.path.join(SRC_DIR, "dlmpc_device.cuh"), os.path.join(ROOT, "include", "dlmpc.h")]
+DEPS = SOURCES + [os.path.join(SRC_DIR, "dlmpc_device.cuh"), os.path.join(SRC_DIR, "dlmpc_schedules.cuh"),
+        os.path.join(ROOT, "include", "dlmpc.h")]
 OUT = os.path.join(PKG, "libdlmpc.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]

@@ -245,6 +245,104 @@ int dlmpc_phase_times(dlmpc_handle* h, uint64_t* out, int reset);
  * kernel mode (0 patch, 1 two-phase, 2 exact, 3 stream), work units. */
 int dlmpc_info(const dlmpc_handle* h, int64_t* out9);
 
+/* ------------------------------------------------------------------------
+ * The reference's device schedules (strategies.py:44-314: naive, padded,
+ * fused, patch-local), executed on the GPU over the reference's own dual
+ * padded layout (sls_core.py:352-518) with the reference's arithmetic bit for
+ * bit. The host (strategies.Executor) drives one iteration as the reference's
+ * coordinator does; every stage is one kernel launch on the handle's stream,
+ * dlmpc_sched_sync is a host sync and dlmpc_sched_read_residuals the flag
+ * read, so the reference's SyncLedger counts real events.
+ * ---------------------------------------------------------------------- */
+typedef struct dlmpc_sched dlmpc_sched;
+
+typedef struct dlmpc_sched_problem {
+  int32_t n_rows, n_cols, d_row, d_col;
+  int64_t n_elems;
+  double rho;
+  const int32_t* row_len;        /* [n_rows]  LayoutTables.row_len                     */
+  const int32_t* col_len;        /* [n_cols]  LayoutTables.col_len                     */
+  const int64_t* rs;             /* [n_rows*d_row] column of each row slot, -1 past the support */
+  const int64_t* c2r_flat;       /* [n_cols*d_col] row-layout twin, -1 past the support */
+  const int64_t* r2c_flat;       /* [n_rows*d_row] column-layout twin, -1 past the support */
+  const int64_t* elem_flat_col;  /* [n_elems] valid column-layout cells                */
+  int32_t n_classes;
+  const int32_t* col_class;      /* [n_cols] operator class                           */
+  const int32_t* class_m;        /* [n_classes] constraint rows                       */
+  const int32_t* class_s;        /* [n_classes] support length                        */
+  const int64_t* class_g_off; const double* g_pool;   /* g [m x s] per class           */
+  const int64_t* class_p_off; const double* p_pool;   /* projector [s x m] per class   */
+  const int64_t* col_rhs_off; const double* rhs_pool; /* [n_cols+1] offsets, rhs [m]   */
+  int64_t n_patch;               /* 0: no patch tables (patch-local unavailable)      */
+  const int64_t* patch_off;      /* [n_cols+1] (admm.py:139-151)                      */
+  const int64_t* patch_rows;     /* member rows of each column patch                  */
+  const int32_t* patch_slot;     /* the column's slot in each member row               */
+  const int32_t* patch_owned;    /* 1: the column publishes the row (owner_col)        */
+  const double* row_w; const double* row_lo; const double* row_hi;   /* [n_rows] or NULL (put later) */
+} dlmpc_sched_problem;
+
+enum {   /* arrays of dlmpc_sched_get / dlmpc_sched_put */
+  DLMPC_SCHED_PHI_R = 0, DLMPC_SCHED_PSI_R = 1, DLMPC_SCHED_LAM_R = 2, DLMPC_SCHED_PHI_C = 3,
+  DLMPC_SCHED_PSI_C = 4, DLMPC_SCHED_LAM_C = 5, DLMPC_SCHED_PSI_PREV_C = 6, DLMPC_SCHED_PRI_C = 7,
+  DLMPC_SCHED_DUAL_C = 8, DLMPC_SCHED_A_PAD = 9, DLMPC_SCHED_ADA = 10, DLMPC_SCHED_ROW_W = 11,
+  DLMPC_SCHED_ROW_LO = 12, DLMPC_SCHED_ROW_HI = 13   /* row data of the current step (RowData) */
+};
+
+enum {   /* stage kernels of dlmpc_sched_stage (AdmmWorkspace, admm.py:153-270) */
+  DLMPC_STAGE_PHI_ROWS = 0,          /* phi_rows, exact-size items (naive)             */
+  DLMPC_STAGE_PHI_ROWS_PADDED = 1,   /* phi_rows, longest-vector items (padded)        */
+  DLMPC_STAGE_EXCHANGE_PHI = 2,      /* exchange_phi_to_col                            */
+  DLMPC_STAGE_PSI_COLS = 3,          /* psi_cols                                       */
+  DLMPC_STAGE_LAMBDA_COLS = 4,       /* lambda_cols                                    */
+  DLMPC_STAGE_LAMBDA_ELEMS = 5,      /* lambda_elems                                   */
+  DLMPC_STAGE_CONV_COLS = 6,         /* conv_cols (+ the global maxima)                */
+  DLMPC_STAGE_EXCHANGE_PSI_LAM = 7,  /* exchange_psi_lam_to_row                        */
+  DLMPC_STAGE_FUSED_COLS = 8,        /* fused_cols (paper §III-C)                      */
+  DLMPC_STAGE_PATCH_COLS = 9,        /* patch_cols (paper §III-D)                      */
+  DLMPC_STAGE_PATCH_COLS_PADDED = 10
+};
+
+int dlmpc_sched_create(const dlmpc_sched_problem* prob, int device, dlmpc_sched** out);
+void dlmpc_sched_destroy(dlmpc_sched* h);
+const char* dlmpc_sched_last_error(const dlmpc_sched* h);
+int dlmpc_sched_put(dlmpc_sched* h, int which, const double* src);
+int dlmpc_sched_get(dlmpc_sched* h, int which, double* dst);
+/* precompute_row_data (sls_core.py:330-349) on device: a_pad, ||a||^2 for x;
+ * DLMPC_ROW_INFEASIBLE with *bad_row = the lowest infeasible row */
+int dlmpc_sched_set_x(dlmpc_sched* h, const double* x, int64_t n_x, int64_t* bad_row);
+/* one stage launch over items [lo, hi) (rows, columns or elements), async */
+int dlmpc_sched_stage(dlmpc_sched* h, int stage, int64_t lo, int64_t hi);
+int dlmpc_sched_sync(dlmpc_sched* h);
+/* the reduced (pri, dual) of the residual stages since the last read
+ * (reduce_residuals, admm.py:269-270); resets the maxima */
+int dlmpc_sched_read_residuals(dlmpc_sched* h, double* pri_dual);
+/* AdmmWorkspace._phi_compute (admm.py:155-166): rows [lo, hi) into out, state untouched */
+int dlmpc_sched_phi_compute(dlmpc_sched* h, int64_t lo, int64_t hi, double* out);
+/* swap_row_buffers (admm.py:255-259): the patch scatter's buffers become current */
+int dlmpc_sched_swap_rows(dlmpc_sched* h);
+
+/* The reference's scalar stage functions as device operators over n
+ * independent items (host pointers, synchronous):
+ *   dlmpc_op_phi_rows     phi_row_solve     admm.py:28-51   (items of length len[i], stride d)
+ *   dlmpc_op_psi_cols     psi_column_solve  admm.py:54-60   (per item g [m x s], P [s x m], rhs [m], k [s])
+ *   dlmpc_op_lambda       lambda_update     admm.py:63-67
+ *   dlmpc_op_residuals    column_residuals  admm.py:69-74   (out2: pri, dual per item)
+ *   dlmpc_op_row_dots     extract_control   admm.py:350-360 (ascending gather-dots)
+ *   dlmpc_op_plant_step   step_dynamics     admm.py:363-369 (CSR A x + B u, scipy's order) */
+int dlmpc_op_phi_rows(int device, int n, int d, const int32_t* len, const double* a, const double* v,
+                      const double* ada, const double* w, const double* lo, const double* hi, double rho,
+                      double* out);
+int dlmpc_op_psi_cols(int device, int n, int m, int s, const double* g, const double* P, const double* rhs,
+                      const double* k, double* out);
+int dlmpc_op_lambda(int device, int64_t n, const double* lam, const double* phi, const double* psi, double* out);
+int dlmpc_op_residuals(int device, int n, int d, const int32_t* len, const double* phi, const double* psi,
+                       const double* prev, double rho, double* out2);
+int dlmpc_op_row_dots(int device, int n, int d, const int32_t* len, const double* vals, const int64_t* idx,
+                      int64_t n_x, const double* x, double* out);
+int dlmpc_op_plant_step(int device, int n_x, int n_u, const int64_t* a_ptr, const int32_t* a_idx,
+                        const double* a_val, const int64_t* b_ptr, const int32_t* b_idx, const double* b_val,
+                        const double* x, const double* u, double* out);
+
 /* Measured FP64 tensor-core (DMMA m8n8k4) peak of `device` in TFLOP/s: the
  * denominator of bench.py's FP64 roofline fraction (no reference counterpart;
  * MEASURED_PEAKS.json has HBM and bf16 only). */

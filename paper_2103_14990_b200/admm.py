@@ -30,8 +30,8 @@ import numpy as np
 from .devlayout import DeviceLayout
 from .device import DeviceSession, PSI, LAM, PSI_PREV, PHI
 from .errors import NotConverged, RowInfeasible
-from .sls_core import (ColumnClasses, LayoutTables, PhiTriple, ProblemSpec, RowData,
-                       build_column_classes_structural)
+from .sls_core import (ColumnClasses, ColumnPrecomp, LayoutTables, PhiTriple, ProblemSpec, RowData,
+                       RowPrecomp, build_column_classes_structural)
 from .strategies import ExecStrategy, Executor
 from .system_model import LocalityMask, LtiSystem
 
@@ -53,6 +53,82 @@ class Trajectory:
     states: np.ndarray        # (t_sim + 1, n_states)
     inputs: np.ndarray        # (t_sim, n_inputs)
     step_iterations: list
+
+
+# ---------------------------------------------------------------------------
+# the reference's scalar stage functions (admm.py:28-74), as device operators
+# ---------------------------------------------------------------------------
+def phi_row_solve(row: RowPrecomp, v: np.ndarray, rho: float = 1.0) -> np.ndarray:
+    """Explicit minimiser of one row subproblem (reference admm.py:28-51):
+    min_p w (p.a)^2 + rho/2 ||p - v||^2 s.t. lo <= p.a <= hi, on the device."""
+    from .schedules import op_phi_rows
+    v = np.asarray(v, dtype=np.float64)
+    if v.shape != row.a.shape:
+        raise ValueError("v must match the row support length")
+    if row.a_dot_a == 0.0 and (row.lo > 0.0 or row.hi < 0.0):
+        raise RowInfeasible(row.row)
+    if v.size == 0:
+        return v.copy()
+    return op_phi_rows(row.a[None], v[None], row.a_dot_a, row.weight, row.lo, row.hi, rho)[0]
+
+
+def psi_column_solve(col: ColumnPrecomp, k: np.ndarray) -> np.ndarray:
+    """Minimum-norm correction of k onto the column's dynamics constraint
+    (reference admm.py:54-60), numpy pairwise sums, on the device."""
+    from .schedules import op_psi_cols
+    k = np.asarray(k, dtype=np.float64)
+    if k.shape != (np.asarray(col.support).size,):
+        raise ValueError("k must match the column support length")
+    g = np.atleast_2d(np.asarray(col.g, dtype=np.float64))
+    return op_psi_cols(g[None], np.asarray(col.projector, dtype=np.float64)[None],
+                       np.atleast_1d(np.asarray(col.rhs, dtype=np.float64))[None], k[None])[0]
+
+
+def lambda_update(lam: np.ndarray, phi: np.ndarray, psi: np.ndarray) -> np.ndarray:
+    """Dual ascent step lam + (phi - psi) (reference admm.py:63-67), on the device."""
+    from .schedules import op_lambda
+    if not (np.shape(lam) == np.shape(phi) == np.shape(psi)):
+        raise ValueError("support mismatch in dual update")
+    return op_lambda(lam, phi, psi)
+
+
+def column_residuals(triple: PhiTriple, c: int, psi_prev: np.ndarray, rho: float):
+    """Per-column (max |phi - psi|, rho * max |psi - psi_prev|) (reference
+    admm.py:69-74), on the device."""
+    from .schedules import op_residuals
+    n = int(triple.tables.col_len[c])
+    out = op_residuals(triple.phi_c[c:c + 1, :n], triple.psi_c[c:c + 1, :n],
+                       np.asarray(psi_prev, dtype=np.float64)[None, :n], [n], rho)
+    return float(out[0, 0]), float(out[0, 1])
+
+
+def extract_control(triple: PhiTriple, x_tau: np.ndarray, row_metas) -> np.ndarray:
+    """First-block input gains applied to the measured state (reference
+    admm.py:350-360): ascending gather-dots on the device."""
+    from .schedules import op_row_dots
+    from .sls_core import INPUT
+    tb = triple.tables
+    x_tau = np.asarray(x_tau, dtype=np.float64)
+    first = [(r, m.signal) for r, m in enumerate(row_metas) if m.kind == INPUT and m.time == 0]
+    u = np.zeros(len(first))
+    if not first:
+        return u
+    rows = np.array([r for r, _ in first], dtype=np.int64)
+    sig = np.array([q for _, q in first], dtype=np.int64)
+    vals = op_row_dots(triple.phi_r[rows], np.where(tb.row_valid[rows], tb.rs[rows], 0), tb.row_len[rows], x_tau)
+    u[sig] = vals
+    return u
+
+
+def step_dynamics(system: LtiSystem, x: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """One plant step x+ = A x + B u (reference admm.py:363-369), CSR
+    products in scipy's accumulation order, on the device."""
+    from .schedules import op_plant_step
+    x = np.asarray(x, dtype=np.float64)
+    u = np.asarray(u, dtype=np.float64)
+    if x.shape != (system.n_states,) or u.shape != (system.n_inputs,):
+        raise ValueError("state/input dimensions do not match the system")
+    return op_plant_step(system.a, system.b, x, u)
 
 
 def closed_loop_cost(traj: Trajectory) -> float:
@@ -120,9 +196,131 @@ class AdmmWorkspace:
         self._sessions = {}
         self._maps = None
         self.last_device_ms = 0.0
+        self.pri_c = np.zeros(self.n_cols)
+        self.dual_c = np.zeros(self.n_cols)
+        self._engine = None
+        self._resident = False       # the schedule engine holds the current state (inside a solve)
+        self._rd_pushed = None       # row data last uploaded to the engine
 
     def set_row_data(self, row_data: RowData):
         self.row_data = row_data
+
+    # -- the reference's schedules on the device (schedules.py) ----------------------
+    def schedule_engine(self, device: int = 0):
+        from .schedules import ScheduleEngine
+        if self._engine is None:
+            self._engine = ScheduleEngine(self.tables, self.col_solvers, self.rho, self.patches, device)
+            if self.patches is None:
+                from .strategies import build_patches
+                self.patches = build_patches(self.tables)
+        return self._engine
+
+    def push_schedule_state(self, eng):
+        eng.push_triple(self.triple)
+        if self.row_data is not None and self._rd_pushed is not self.row_data:
+            eng.push_row_data(self.row_data)
+            self._rd_pushed = self.row_data
+
+    def pull_schedule_state(self, eng):
+        from .schedules import A_DUAL_C, A_PRI_C
+        eng.pull_triple(self.triple)
+        eng.get(A_PRI_C, self.pri_c)
+        eng.get(A_DUAL_C, self.dual_c)
+
+    def _stage(self, stage, n_items, idx):
+        """One stage kernel over `idx` (slice or index array; contiguous runs
+        are launched separately -- batching never changes an item's
+        arithmetic, admm.py:6-10), triple synced around it."""
+        eng = self.schedule_engine()
+        if not self._resident:
+            self.push_schedule_state(eng)
+        for lo, hi in _index_runs(idx, n_items):
+            eng.stage(stage, lo, hi)
+        if not self._resident:
+            self.pull_schedule_state(eng)
+
+    @property
+    def duplicated_rows_per_iter(self) -> int:
+        if self.patches is None:
+            return 0
+        from .strategies import patch_duplication
+        if not hasattr(self, "_dup"):
+            self._dup = patch_duplication(self.patches)
+        return self._dup
+
+    def _phi_compute(self, idx) -> np.ndarray:
+        """Row solve for a batch of rows on the device; returns the padded
+        values, writes nothing (reference admm.py:155-166)."""
+        eng = self.schedule_engine()
+        if not self._resident:
+            self.push_schedule_state(eng)
+        if isinstance(idx, slice):
+            lo, hi, step = idx.indices(self.n_rows)
+            if step == 1:
+                return eng.phi_compute(lo, max(lo, hi))
+            idx = np.arange(lo, hi, step)
+        arr = np.asarray(idx, dtype=np.int64) % max(1, self.n_rows)
+        flat = arr.ravel()
+        if flat.size == 0:
+            return np.zeros(arr.shape + (self.tables.d_row,))
+        lo = int(flat.min())
+        block = eng.phi_compute(lo, int(flat.max()) + 1)
+        return block[flat - lo].reshape(arr.shape + (self.tables.d_row,))
+
+    def phi_rows(self, idx):
+        from .schedules import STAGE_PHI_ROWS
+        self._stage(STAGE_PHI_ROWS, self.n_rows, idx)
+
+    def psi_cols(self, idx):
+        from .schedules import STAGE_PSI_COLS
+        self._stage(STAGE_PSI_COLS, self.n_cols, idx)
+
+    def lambda_cols(self, idx):
+        from .schedules import STAGE_LAMBDA_COLS
+        self._stage(STAGE_LAMBDA_COLS, self.n_cols, idx)
+
+    def lambda_elems(self, idx):
+        from .schedules import STAGE_LAMBDA_ELEMS
+        self._stage(STAGE_LAMBDA_ELEMS, self.n_elems, idx)
+
+    def conv_cols(self, idx):
+        from .schedules import STAGE_CONV_COLS
+        self._stage(STAGE_CONV_COLS, self.n_cols, idx)
+
+    def fused_cols(self, idx):
+        from .schedules import STAGE_FUSED_COLS
+        self._stage(STAGE_FUSED_COLS, self.n_cols, idx)
+
+    def patch_cols(self, idx):
+        from .schedules import STAGE_PATCH_COLS
+        if not isinstance(idx, slice):
+            raise TypeError("patch shards are contiguous column ranges")
+        self._stage(STAGE_PATCH_COLS, self.n_cols, idx)
+
+    def swap_row_buffers(self):
+        eng = self.schedule_engine()
+        eng.swap_rows()
+        if not self._resident:
+            from .schedules import A_LAM_R, A_PSI_R
+            eng.get(A_PSI_R, self.triple.psi_r)
+            eng.get(A_LAM_R, self.triple.lam_r)
+
+    def exchange_phi_to_col(self):
+        from .schedules import STAGE_EXCHANGE_PHI
+        self._stage(STAGE_EXCHANGE_PHI, 0, slice(0, 0))
+
+    def exchange_psi_lam_to_row(self):
+        from .schedules import STAGE_EXCHANGE_PSI_LAM
+        self._stage(STAGE_EXCHANGE_PSI_LAM, 0, slice(0, 0))
+
+    def reduce_residuals(self):
+        if self._resident and self._engine is not None:
+            from .schedules import A_DUAL_C, A_PRI_C
+            self._engine.get(A_PRI_C, self.pri_c)
+            self._engine.get(A_DUAL_C, self.dual_c)
+        from .strategies import reduce_convergence
+        pri, dual, _ = reduce_convergence(self.pri_c, self.dual_c, 0.0, 0.0)
+        return pri, dual
 
     def session(self, exact: bool, device: int = 0) -> DeviceSession:
         key = (bool(exact), int(device))
@@ -185,6 +383,26 @@ class AdmmWorkspace:
         for s in self._sessions.values():
             s.close()
         self._sessions.clear()
+        if self._engine is not None:
+            self._engine.close()
+            self._engine = None
+
+
+def _index_runs(idx, n):
+    """Contiguous [lo, hi) runs of a slice / index array / int over n items."""
+    if isinstance(idx, slice):
+        lo, hi, step = idx.indices(n)
+        if step != 1:
+            return [(i, i + 1) for i in range(lo, hi, step)]
+        return [(lo, hi)] if hi > lo else ([(0, 0)] if n == 0 else [])
+    if isinstance(idx, (int, np.integer)):
+        i = int(idx) % n if n else 0
+        return [(i, i + 1)]
+    pos = np.unique(np.asarray(idx, dtype=np.int64).ravel())
+    if pos.size == 0:
+        return []
+    cuts = np.nonzero(np.diff(pos) != 1)[0] + 1
+    return [(int(r[0]), int(r[-1]) + 1) for r in np.split(pos, cuts)]
 
 
 def admm_solve(row_data: RowData, col_solvers, triple: PhiTriple, spec: ProblemSpec,
@@ -199,11 +417,36 @@ def admm_solve(row_data: RowData, col_solvers, triple: PhiTriple, spec: ProblemS
     else:
         strat = strategy or ExecStrategy("b200")
     if workspace is None:
-        workspace = AdmmWorkspace(triple, col_solvers, spec)
+        from .strategies import build_patches
+        patches = build_patches(triple.tables) if strat.variant == "patch-local" else None
+        workspace = AdmmWorkspace(triple, col_solvers, spec, patches=patches)
     workspace.set_row_data(row_data)
-    n, history, ok = workspace.device_solve(strat, spec.max_iters, spec.eps_pri, spec.eps_dual)
-    if executor is not None:
-        executor.ledger.record_launch(n, workspace.last_device_ms)
+    if strat.staged:
+        # the reference's loop (admm.py:331-343) over a device schedule, the
+        # state resident on the device for the whole solve
+        own = executor is None
+        ex = executor if executor is not None else Executor(strat)
+        eng = workspace.schedule_engine(strat.device)
+        workspace.push_schedule_state(eng)
+        workspace._resident = True
+        history, ok = [], False
+        try:
+            for _ in range(spec.max_iters):
+                pri, dual = ex.run_iteration(workspace)
+                history.append((pri, dual))
+                if pri <= spec.eps_pri and dual <= spec.eps_dual:
+                    ok = True
+                    break
+        finally:
+            workspace._resident = False
+            workspace.pull_schedule_state(eng)
+            if own:
+                ex.close()
+        n = len(history)
+    else:
+        n, history, ok = workspace.device_solve(strat, spec.max_iters, spec.eps_pri, spec.eps_dual)
+        if executor is not None:
+            executor.ledger.record_launch(n, workspace.last_device_ms)
     triple._dlmpc_ws = (workspace, strat)
     if not ok:
         raise NotConverged(history)
@@ -364,6 +607,101 @@ def _cached_session(system, spec, mask, strat):
     return sess, False
 
 
+def _simulate_staged(system, spec, mask, x0, t_sim, strat, warm_start, audit):
+    """The reference's closed loop (admm.py:437-540) over a per-iteration
+    device schedule (naive / padded / fused / patch-local): per MPC step the
+    row data on the device, the schedule's iterations with the state
+    resident, control extraction and plant step as device operators. Same
+    phases and report as the reference."""
+    from .report import PHASES, RunReport
+    from .sls_core import (build_column_classes, build_dynamics_operator, precompute_column_solvers,
+                           row_index_map)
+    from .strategies import build_patches, prepare_work_items
+
+    total_start = time.perf_counter()
+    phases = dict.fromkeys(PHASES, 0.0)
+    start = time.perf_counter()
+    executor = Executor(strat)
+    tables = LayoutTables(mask)
+    triple = PhiTriple(tables)
+    patches = build_patches(tables) if strat.variant == "patch-local" else None
+    prepare_work_items(strat, tables, executor.ledger)
+    phases["setup"] = time.perf_counter() - start
+
+    start = time.perf_counter()
+    operator = build_dynamics_operator(system, spec.horizon)
+    col_solvers = precompute_column_solvers(operator, mask, build_column_classes(operator, mask))
+    metas = row_index_map(system.partition, spec.horizon, spec)
+    ws = AdmmWorkspace(triple, col_solvers, spec, patches=patches, system=system)
+    eng = ws.schedule_engine(strat.device)
+    eng.set_costs(*spec.row_arrays())
+    phases["precompute_global"] = time.perf_counter() - start
+
+    states, inputs, iters = [np.asarray(x0, dtype=np.float64)], [], []
+    audit_worst = {"dynamics_residual": 0.0, "resolve_residual": 0.0, "consensus_gap": 0.0} if audit else None
+    x = states[0]
+    try:
+        for step in range(t_sim):
+            start = time.perf_counter()
+            try:
+                eng.set_x(x)
+            except RowInfeasible as err:
+                err.step = step
+                raise
+            phases["precompute_per_step"] += time.perf_counter() - start
+            if not warm_start:
+                triple.zero_()
+            start = time.perf_counter()
+            ws.push_schedule_state(eng)
+            ws._resident = True
+            history, ok = [], False
+            try:
+                for _ in range(spec.max_iters):
+                    pri, dual = executor.run_iteration(ws)
+                    history.append((pri, dual))
+                    if pri <= spec.eps_pri and dual <= spec.eps_dual:
+                        ok = True
+                        break
+            finally:
+                ws._resident = False
+                ws.pull_schedule_state(eng)
+            if not ok:
+                raise NotConverged(history, step=step)
+            phases["optimize"] += time.perf_counter() - start
+            iters.append(len(history))
+            if audit:
+                from .schedules import A_A_PAD, A_ADA
+                a_pad, ada = np.zeros((tables.n_rows, tables.d_row)), np.zeros(tables.n_rows)
+                eng.get(A_A_PAD, a_pad)
+                eng.get(A_ADA, ada)
+                w, lo, hi = spec.row_arrays()
+                rep = verify_fixed_point(triple, RowData(tables, a_pad, ada, w, lo, hi, x_tau=x), operator, spec)
+                for key in audit_worst:
+                    audit_worst[key] = max(audit_worst[key], getattr(rep, key))
+            start = time.perf_counter()
+            u = extract_control(triple, x, metas)
+            x = step_dynamics(system, x, u)
+            inputs.append(u)
+            states.append(x)
+            phases["dynamics"] += time.perf_counter() - start
+    finally:
+        executor.close()
+        ws.close()
+    traj = Trajectory(np.array(states), np.array(inputs).reshape(len(inputs), system.n_inputs), iters)
+    report = RunReport(
+        scenario={"strategy": strat.variant, "worker_count": executor.workers, "t_sim": t_sim,
+                  "warm_start": warm_start, "rho": spec.rho, "eps": spec.eps_pri},
+        phase_times_ms={k: v * 1e3 for k, v in phases.items()},
+        per_step_iters=iters,
+        ledger=executor.ledger,
+        closed_loop_cost=closed_loop_cost(traj),
+        converged_all_steps=True,
+        total_wall_ms=(time.perf_counter() - total_start) * 1e3,
+        audit_worst=audit_worst,
+    )
+    return traj, report
+
+
 def dlmpc_simulate(system: LtiSystem, spec: ProblemSpec, mask: LocalityMask,
                    x0: np.ndarray, t_sim: int, strategy="b200",
                    warm_start: bool = True, audit: bool = False):
@@ -379,6 +717,8 @@ def dlmpc_simulate(system: LtiSystem, spec: ProblemSpec, mask: LocalityMask,
     if t_sim < 1:
         raise ValueError("t_sim must be >= 1")
     strat = ExecStrategy(strategy) if isinstance(strategy, str) else strategy
+    if strat.staged:
+        return _simulate_staged(system, spec, mask, x0, t_sim, strat, warm_start, audit)
     total_start = time.perf_counter()
     phases = dict.fromkeys(PHASES, 0.0)
     start = time.perf_counter()

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 using namespace dlmpc;
@@ -1238,6 +1239,415 @@ int dlmpc_info(const dlmpc_handle* h, int64_t* out) {
   out[4] = h->grid; out[5] = h->P.tile_cols; out[6] = h->smem_bytes;
   out[7] = h->mode; out[8] = h->n_units;
   return DLMPC_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// The reference's device schedules (dlmpc_schedules.cuh) and its scalar stage
+// functions as standalone device operators.
+// ===========================================================================
+#include "dlmpc_schedules.cuh"
+
+struct dlmpc_sched {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  sched::RefDev R{};
+  std::vector<void*> allocs;
+  std::string err;
+  int sm_count = 0;
+  int smem_psi = 0;       // dynamic shared memory of the Ψ-carrying kernels (k [s] + r [m])
+  long long n_x = 0;      // state dimension (max column index + 1)
+  double* d_x = nullptr;  // measured state of the current step
+  double* d_out = nullptr; size_t out_cap = 0;   // _phi_compute scratch
+  bool has_patch = false;
+};
+
+namespace {
+
+int sfail(dlmpc_sched* h, int code, const std::string& msg) {
+  if (h) h->err = msg; else g_global_error = msg;
+  return code;
+}
+
+#define SCUDA(h, expr)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return sfail((h), DLMPC_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>   // T from dst only: src may be nullptr (zeroed allocation)
+int supload(dlmpc_sched* h, const typename std::common_type<T>::type* src, size_t n, T** dst) {
+  *dst = nullptr;
+  void* p = nullptr;
+  SCUDA(h, cudaMalloc(&p, (n ? n : 1) * sizeof(T)));
+  h->allocs.push_back(p);
+  if (src && n) SCUDA(h, cudaMemcpy(p, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  else SCUDA(h, cudaMemset(p, 0, (n ? n : 1) * sizeof(T)));
+  *dst = static_cast<T*>(p);
+  return DLMPC_OK;
+}
+
+double* sched_array(dlmpc_sched* h, int which, size_t* n) {
+  sched::RefDev& R = h->R;
+  const size_t nr = (size_t)R.n_rows * R.d_row, nc = (size_t)R.n_cols * R.d_col;
+  switch (which) {
+    case DLMPC_SCHED_PHI_R: *n = nr; return R.phi_r;
+    case DLMPC_SCHED_PSI_R: *n = nr; return R.psi_r;
+    case DLMPC_SCHED_LAM_R: *n = nr; return R.lam_r;
+    case DLMPC_SCHED_PHI_C: *n = nc; return R.phi_c;
+    case DLMPC_SCHED_PSI_C: *n = nc; return R.psi_c;
+    case DLMPC_SCHED_LAM_C: *n = nc; return R.lam_c;
+    case DLMPC_SCHED_PSI_PREV_C: *n = nc; return R.prev_c;
+    case DLMPC_SCHED_PRI_C: *n = R.n_cols; return R.pri_c;
+    case DLMPC_SCHED_DUAL_C: *n = R.n_cols; return R.dual_c;
+    case DLMPC_SCHED_A_PAD: *n = nr; return R.a_pad;
+    case DLMPC_SCHED_ADA: *n = R.n_rows; return R.ada;
+    case DLMPC_SCHED_ROW_W: *n = R.n_rows; return R.w;
+    case DLMPC_SCHED_ROW_LO: *n = R.n_rows; return R.lo;
+    case DLMPC_SCHED_ROW_HI: *n = R.n_rows; return R.hi;
+    default: *n = 0; return nullptr;
+  }
+}
+
+// Host-pointer operands of one standalone operator call: device copies freed
+// on scope exit.
+struct OpBufs {
+  std::vector<void*> p;
+  ~OpBufs() { for (void* q : p) cudaFree(q); }
+  template <class T>
+  T* up(const T* src, size_t n) {
+    void* q = nullptr;
+    if (cudaMalloc(&q, (n ? n : 1) * sizeof(T)) != cudaSuccess) return nullptr;
+    p.push_back(q);
+    if (src && n && cudaMemcpy(q, src, n * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    return static_cast<T*>(q);
+  }
+};
+
+int op_begin(int device) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return sfail(nullptr, DLMPC_NO_DEVICE, "no CUDA device visible");
+  if (device < 0 || device >= ndev) return sfail(nullptr, DLMPC_BAD_ARGUMENT, "device out of range");
+  if (cudaSetDevice(device) != cudaSuccess) return sfail(nullptr, DLMPC_CUDA_ERROR, "cudaSetDevice failed");
+  return DLMPC_OK;
+}
+
+int op_end(double* host_out, const double* dev_out, size_t n) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && n) e = cudaMemcpy(host_out, dev_out, n * sizeof(double), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return sfail(nullptr, DLMPC_CUDA_ERROR, std::string("operator: ") + cudaGetErrorString(e));
+  return DLMPC_OK;
+}
+
+int grid_for(long long n, int per_block) {
+  return (int)std::max<long long>(1, std::min<long long>((n + per_block - 1) / per_block, 148LL * 16));
+}
+
+}  // namespace
+
+extern "C" {
+
+int dlmpc_sched_create(const dlmpc_sched_problem* pr, int device, dlmpc_sched** out) {
+  if (!pr || !out) return sfail(nullptr, DLMPC_BAD_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (int rc = op_begin(device)) return rc;
+  if (pr->n_rows < 1 || pr->n_cols < 1 || pr->d_row < 1 || pr->d_col < 1)
+    return sfail(nullptr, DLMPC_BAD_ARGUMENT, "empty layout");
+  auto* h = new dlmpc_sched();
+  h->device = device;
+  sched::RefDev& R = h->R;
+  R.n_rows = pr->n_rows; R.n_cols = pr->n_cols; R.d_row = pr->d_row; R.d_col = pr->d_col;
+  R.n_elems = pr->n_elems; R.rho = pr->rho;
+  const size_t nr = (size_t)R.n_rows * R.d_row, nc = (size_t)R.n_cols * R.d_col;
+  int rc = DLMPC_OK;
+  int m_max = 1, s_max = 1;
+  for (int k = 0; k < pr->n_classes; ++k) { m_max = std::max(m_max, pr->class_m[k]); s_max = std::max(s_max, pr->class_s[k]); }
+  h->smem_psi = (m_max + s_max) * 8;
+  long long nx = 0;
+  for (size_t q = 0; q < nr; ++q) nx = std::max<long long>(nx, pr->rs[q] + 1);
+  h->n_x = nx;
+#define SUP(field, src, n) do { if ((rc = supload(h, src, (size_t)(n), &field)) != DLMPC_OK) goto bad; } while (0)
+  {
+    int* row_len; int* col_len; long long* rs; long long* c2r; long long* r2c; long long* ef;
+    int* col_class; int* class_m; long long* g_off; double* g_pool; long long* p_off; double* p_pool;
+    long long* rhs_off; double* rhs_pool;
+    SUP(row_len, pr->row_len, R.n_rows); SUP(col_len, pr->col_len, R.n_cols);
+    SUP(rs, reinterpret_cast<const long long*>(pr->rs), nr);
+    SUP(c2r, reinterpret_cast<const long long*>(pr->c2r_flat), nc);
+    SUP(r2c, reinterpret_cast<const long long*>(pr->r2c_flat), nr);
+    SUP(ef, reinterpret_cast<const long long*>(pr->elem_flat_col), R.n_elems);
+    SUP(col_class, pr->col_class, R.n_cols); SUP(class_m, pr->class_m, pr->n_classes);
+    SUP(g_off, reinterpret_cast<const long long*>(pr->class_g_off), pr->n_classes + 1);
+    SUP(g_pool, pr->g_pool, pr->class_g_off[pr->n_classes]);
+    SUP(p_off, reinterpret_cast<const long long*>(pr->class_p_off), pr->n_classes + 1);
+    SUP(p_pool, pr->p_pool, pr->class_p_off[pr->n_classes]);
+    SUP(rhs_off, reinterpret_cast<const long long*>(pr->col_rhs_off), R.n_cols + 1);
+    SUP(rhs_pool, pr->rhs_pool, pr->col_rhs_off[R.n_cols]);
+    SUP(R.w, pr->row_w, R.n_rows); SUP(R.lo, pr->row_lo, R.n_rows); SUP(R.hi, pr->row_hi, R.n_rows);
+    R.row_len = row_len; R.col_len = col_len; R.rs = rs; R.c2r = c2r; R.r2c = r2c; R.elem_flat = ef;
+    R.col_class = col_class; R.class_m = class_m; R.g_off = g_off; R.g_pool = g_pool; R.p_off = p_off;
+    R.p_pool = p_pool; R.rhs_off = rhs_off; R.rhs_pool = rhs_pool;
+    if (pr->n_patch > 0 && pr->patch_off && pr->patch_rows && pr->patch_slot && pr->patch_owned) {
+      long long* po; long long* prw; int* ps; int* pw;
+      SUP(po, reinterpret_cast<const long long*>(pr->patch_off), R.n_cols + 1);
+      SUP(prw, reinterpret_cast<const long long*>(pr->patch_rows), pr->n_patch);
+      SUP(ps, pr->patch_slot, pr->n_patch); SUP(pw, pr->patch_owned, pr->n_patch);
+      R.patch_off = po; R.patch_rows = prw; R.patch_slot = ps; R.patch_owned = pw;
+      h->has_patch = true;
+    }
+    SUP(R.phi_r, nullptr, nr); SUP(R.psi_r, nullptr, nr); SUP(R.lam_r, nullptr, nr);
+    SUP(R.psi_r_nx, nullptr, nr); SUP(R.lam_r_nx, nullptr, nr);
+    SUP(R.phi_c, nullptr, nc); SUP(R.psi_c, nullptr, nc); SUP(R.lam_c, nullptr, nc); SUP(R.prev_c, nullptr, nc);
+    SUP(R.pri_c, nullptr, R.n_cols); SUP(R.dual_c, nullptr, R.n_cols);
+    SUP(R.a_pad, nullptr, nr); SUP(R.ada, nullptr, R.n_rows);
+    SUP(R.resid, nullptr, 2); SUP(R.bad, nullptr, 1); SUP(h->d_x, nullptr, std::max<long long>(1, nx));
+    if (h->smem_psi > 48 * 1024) {
+      const void* fns[] = {reinterpret_cast<const void*>(sched::psi_cols_kernel),
+                           reinterpret_cast<const void*>(sched::fused_cols_kernel),
+                           reinterpret_cast<const void*>(sched::patch_cols_kernel<false>),
+                           reinterpret_cast<const void*>(sched::patch_cols_kernel<true>)};
+      for (const void* f : fns)
+        if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_psi) != cudaSuccess) {
+          rc = sfail(h, DLMPC_BAD_ARGUMENT, "column operator too large for shared memory"); goto bad;
+        }
+    }
+    if (cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      rc = sfail(h, DLMPC_CUDA_ERROR, "stream creation failed"); goto bad;
+    }
+  }
+#undef SUP
+  *out = h;
+  return DLMPC_OK;
+bad:
+  g_global_error = h->err;
+  dlmpc_sched_destroy(h);
+  return rc;
+}
+
+void dlmpc_sched_destroy(dlmpc_sched* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void* p : h->allocs) cudaFree(p);
+  if (h->d_out) cudaFree(h->d_out);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+const char* dlmpc_sched_last_error(const dlmpc_sched* h) { return h ? h->err.c_str() : g_global_error.c_str(); }
+
+int dlmpc_sched_put(dlmpc_sched* h, int which, const double* src) {
+  if (!h || !src) return sfail(h, DLMPC_BAD_ARGUMENT, "null argument");
+  size_t n = 0;
+  double* dst = sched_array(h, which, &n);
+  if (!dst) return sfail(h, DLMPC_BAD_ARGUMENT, "unknown array");
+  cudaSetDevice(h->device);
+  SCUDA(h, cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  SCUDA(h, cudaStreamSynchronize(h->stream));
+  return DLMPC_OK;
+}
+
+int dlmpc_sched_get(dlmpc_sched* h, int which, double* dst) {
+  if (!h || !dst) return sfail(h, DLMPC_BAD_ARGUMENT, "null argument");
+  size_t n = 0;
+  double* src = sched_array(h, which, &n);
+  if (!src) return sfail(h, DLMPC_BAD_ARGUMENT, "unknown array");
+  cudaSetDevice(h->device);
+  SCUDA(h, cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  SCUDA(h, cudaStreamSynchronize(h->stream));
+  return DLMPC_OK;
+}
+
+int dlmpc_sched_set_x(dlmpc_sched* h, const double* x, int64_t n_x, int64_t* bad_row) {
+  if (!h || !x) return sfail(h, DLMPC_BAD_ARGUMENT, "null argument");
+  if (n_x < h->n_x) return sfail(h, DLMPC_BAD_ARGUMENT, "state shorter than the layout's columns");
+  cudaSetDevice(h->device);
+  SCUDA(h, cudaMemcpyAsync(h->d_x, x, h->n_x * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  SCUDA(h, cudaMemsetAsync(h->R.bad, 0x7f, sizeof(int), h->stream));
+  sched::set_x_kernel<<<grid_for(h->R.n_rows, 256), 256, 0, h->stream>>>(h->R, h->d_x);
+  SCUDA(h, cudaGetLastError());
+  int bad = 0;
+  SCUDA(h, cudaMemcpyAsync(&bad, h->R.bad, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  SCUDA(h, cudaStreamSynchronize(h->stream));
+  if (bad_row) *bad_row = bad == kBadNone ? -1 : bad;
+  return bad == kBadNone ? DLMPC_OK : DLMPC_ROW_INFEASIBLE;
+}
+
+int dlmpc_sched_stage(dlmpc_sched* h, int stage, int64_t lo, int64_t hi) {
+  if (!h) return sfail(h, DLMPC_BAD_ARGUMENT, "null handle");
+  sched::RefDev& R = h->R;
+  const bool rows = stage == DLMPC_STAGE_PHI_ROWS || stage == DLMPC_STAGE_PHI_ROWS_PADDED;
+  const long long n_items = rows ? R.n_rows : (stage == DLMPC_STAGE_LAMBDA_ELEMS ? R.n_elems : R.n_cols);
+  if (lo < 0 || hi > n_items || lo > hi) return sfail(h, DLMPC_BAD_ARGUMENT, "item range out of bounds");
+  if ((stage == DLMPC_STAGE_PATCH_COLS || stage == DLMPC_STAGE_PATCH_COLS_PADDED) && !h->has_patch)
+    return sfail(h, DLMPC_BAD_ARGUMENT, "no patch tables");
+  cudaSetDevice(h->device);
+  const int cols_grid = (int)std::max<long long>(1, std::min<long long>(hi - lo, (long long)h->sm_count * 8));
+  switch (stage) {
+    case DLMPC_STAGE_PHI_ROWS:
+      sched::phi_rows_kernel<false><<<grid_for(hi - lo, 128), 128, 0, h->stream>>>(R, lo, hi, nullptr); break;
+    case DLMPC_STAGE_PHI_ROWS_PADDED:
+      sched::phi_rows_kernel<true><<<grid_for(hi - lo, 128), 128, 0, h->stream>>>(R, lo, hi, nullptr); break;
+    case DLMPC_STAGE_EXCHANGE_PHI:
+      sched::exchange_phi_kernel<<<grid_for((long long)R.n_cols * R.d_col, 256), 256, 0, h->stream>>>(R); break;
+    case DLMPC_STAGE_PSI_COLS:
+      sched::psi_cols_kernel<<<cols_grid, 256, h->smem_psi, h->stream>>>(R, (int)lo, (int)hi); break;
+    case DLMPC_STAGE_LAMBDA_COLS:
+      sched::lambda_cols_kernel<<<cols_grid, 128, 0, h->stream>>>(R, (int)lo, (int)hi); break;
+    case DLMPC_STAGE_LAMBDA_ELEMS:
+      sched::lambda_elems_kernel<<<grid_for(hi - lo, 256), 256, 0, h->stream>>>(R, lo, hi); break;
+    case DLMPC_STAGE_CONV_COLS:
+      sched::conv_cols_kernel<<<cols_grid, 128, 0, h->stream>>>(R, (int)lo, (int)hi); break;
+    case DLMPC_STAGE_EXCHANGE_PSI_LAM:
+      sched::exchange_psi_lam_kernel<<<grid_for((long long)R.n_rows * R.d_row, 256), 256, 0, h->stream>>>(R); break;
+    case DLMPC_STAGE_FUSED_COLS:
+      sched::fused_cols_kernel<<<cols_grid, 256, h->smem_psi, h->stream>>>(R, (int)lo, (int)hi); break;
+    case DLMPC_STAGE_PATCH_COLS:
+      sched::patch_cols_kernel<false><<<cols_grid, 256, h->smem_psi, h->stream>>>(R, (int)lo, (int)hi); break;
+    case DLMPC_STAGE_PATCH_COLS_PADDED:
+      sched::patch_cols_kernel<true><<<cols_grid, 256, h->smem_psi, h->stream>>>(R, (int)lo, (int)hi); break;
+    default:
+      return sfail(h, DLMPC_BAD_ARGUMENT, "unknown stage");
+  }
+  SCUDA(h, cudaGetLastError());
+  return DLMPC_OK;
+}
+
+int dlmpc_sched_sync(dlmpc_sched* h) {
+  if (!h) return sfail(h, DLMPC_BAD_ARGUMENT, "null handle");
+  cudaSetDevice(h->device);
+  SCUDA(h, cudaStreamSynchronize(h->stream));
+  return DLMPC_OK;
+}
+
+int dlmpc_sched_read_residuals(dlmpc_sched* h, double* pri_dual) {
+  if (!h || !pri_dual) return sfail(h, DLMPC_BAD_ARGUMENT, "null argument");
+  cudaSetDevice(h->device);
+  unsigned long long bits[2];
+  SCUDA(h, cudaMemcpyAsync(bits, h->R.resid, sizeof(bits), cudaMemcpyDeviceToHost, h->stream));
+  SCUDA(h, cudaMemsetAsync(h->R.resid, 0, sizeof(bits), h->stream));
+  SCUDA(h, cudaStreamSynchronize(h->stream));
+  std::memcpy(pri_dual, bits, sizeof(bits));   // the ordered bits are the doubles' own patterns
+  return DLMPC_OK;
+}
+
+int dlmpc_sched_phi_compute(dlmpc_sched* h, int64_t lo, int64_t hi, double* out_host) {
+  if (!h || !out_host) return sfail(h, DLMPC_BAD_ARGUMENT, "null argument");
+  if (lo < 0 || hi > h->R.n_rows || lo > hi) return sfail(h, DLMPC_BAD_ARGUMENT, "row range out of bounds");
+  cudaSetDevice(h->device);
+  const size_t n = (size_t)h->R.n_rows * h->R.d_row;
+  if (!h->d_out) {
+    SCUDA(h, cudaMalloc(&h->d_out, n * sizeof(double)));
+    h->out_cap = n;
+  }
+  sched::phi_rows_kernel<false><<<grid_for(hi - lo, 128), 128, 0, h->stream>>>(h->R, lo, hi, h->d_out);
+  SCUDA(h, cudaGetLastError());
+  const size_t off = (size_t)lo * h->R.d_row, cnt = (size_t)(hi - lo) * h->R.d_row;
+  SCUDA(h, cudaMemcpyAsync(out_host, h->d_out + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  SCUDA(h, cudaStreamSynchronize(h->stream));
+  return DLMPC_OK;
+}
+
+int dlmpc_sched_swap_rows(dlmpc_sched* h) {
+  if (!h) return sfail(h, DLMPC_BAD_ARGUMENT, "null handle");
+  std::swap(h->R.psi_r, h->R.psi_r_nx);
+  std::swap(h->R.lam_r, h->R.lam_r_nx);
+  return DLMPC_OK;
+}
+
+int dlmpc_op_phi_rows(int device, int n, int d, const int32_t* len, const double* a, const double* v,
+                      const double* ada, const double* w, const double* lo, const double* hi, double rho,
+                      double* out) {
+  if (n < 0 || d < 1 || !len || !a || !v || !ada || !w || !lo || !hi || !out)
+    return sfail(nullptr, DLMPC_BAD_ARGUMENT, "bad argument");
+  if (n == 0) return DLMPC_OK;
+  if (int rc = op_begin(device)) return rc;
+  OpBufs B;
+  const size_t nd = (size_t)n * d;
+  int* dl = B.up(len, n); double* da = B.up(a, nd); double* dv = B.up(v, nd); double* dd = B.up(ada, n);
+  double* dw = B.up(w, n); double* dlo = B.up(lo, n); double* dhi = B.up(hi, n); double* dout = B.up<double>(nullptr, nd);
+  if (!dl || !da || !dv || !dd || !dw || !dlo || !dhi || !dout) return sfail(nullptr, DLMPC_CUDA_ERROR, "operator buffers");
+  sched::op_phi_rows_kernel<<<grid_for(n, 128), 128>>>(n, d, dl, da, dv, dd, dw, dlo, dhi, rho, dout);
+  return op_end(out, dout, nd);
+}
+
+int dlmpc_op_psi_cols(int device, int n, int m, int s, const double* g, const double* P, const double* rhs,
+                      const double* k, double* out) {
+  if (n < 0 || m < 1 || s < 1 || !g || !P || !rhs || !k || !out) return sfail(nullptr, DLMPC_BAD_ARGUMENT, "bad argument");
+  if (n == 0) return DLMPC_OK;
+  if (int rc = op_begin(device)) return rc;
+  if ((size_t)m * 8 > 200 * 1024) return sfail(nullptr, DLMPC_BAD_ARGUMENT, "too many constraint rows");
+  OpBufs B;
+  double* dg = B.up(g, (size_t)n * m * s); double* dp = B.up(P, (size_t)n * s * m);
+  double* dr = B.up(rhs, (size_t)n * m); double* dk = B.up(k, (size_t)n * s); double* dout = B.up<double>(nullptr, (size_t)n * s);
+  if (!dg || !dp || !dr || !dk || !dout) return sfail(nullptr, DLMPC_CUDA_ERROR, "operator buffers");
+  const int smem = m * 8;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(sched::op_psi_cols_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  sched::op_psi_cols_kernel<<<std::min(n, 148 * 8), 256, smem>>>(n, m, s, dg, dp, dr, dk, dout);
+  return op_end(out, dout, (size_t)n * s);
+}
+
+int dlmpc_op_lambda(int device, int64_t n, const double* lam, const double* phi, const double* psi, double* out) {
+  if (n < 0 || !lam || !phi || !psi || !out) return sfail(nullptr, DLMPC_BAD_ARGUMENT, "bad argument");
+  if (n == 0) return DLMPC_OK;
+  if (int rc = op_begin(device)) return rc;
+  OpBufs B;
+  double* dl = B.up(lam, n); double* df = B.up(phi, n); double* ds = B.up(psi, n); double* dout = B.up<double>(nullptr, n);
+  if (!dl || !df || !ds || !dout) return sfail(nullptr, DLMPC_CUDA_ERROR, "operator buffers");
+  sched::op_lambda_kernel<<<grid_for(n, 256), 256>>>(n, dl, df, ds, dout);
+  return op_end(out, dout, n);
+}
+
+int dlmpc_op_residuals(int device, int n, int d, const int32_t* len, const double* phi, const double* psi,
+                       const double* prev, double rho, double* out2) {
+  if (n < 0 || d < 1 || !len || !phi || !psi || !prev || !out2) return sfail(nullptr, DLMPC_BAD_ARGUMENT, "bad argument");
+  if (n == 0) return DLMPC_OK;
+  if (int rc = op_begin(device)) return rc;
+  OpBufs B;
+  const size_t nd = (size_t)n * d;
+  int* dl = B.up(len, n); double* df = B.up(phi, nd); double* ds = B.up(psi, nd); double* dp = B.up(prev, nd);
+  double* dout = B.up<double>(nullptr, 2 * (size_t)n);
+  if (!dl || !df || !ds || !dp || !dout) return sfail(nullptr, DLMPC_CUDA_ERROR, "operator buffers");
+  sched::op_residuals_kernel<<<grid_for(n, 128), 128>>>(n, d, dl, df, ds, dp, rho, dout);
+  return op_end(out2, dout, 2 * (size_t)n);
+}
+
+int dlmpc_op_row_dots(int device, int n, int d, const int32_t* len, const double* vals, const int64_t* idx,
+                      int64_t n_x, const double* x, double* out) {
+  if (n < 0 || d < 1 || n_x < 0 || !len || !vals || !idx || !x || !out) return sfail(nullptr, DLMPC_BAD_ARGUMENT, "bad argument");
+  if (n == 0) return DLMPC_OK;
+  for (size_t q = 0; q < (size_t)n * d; ++q)
+    if (q % d < (size_t)len[q / d] && (idx[q] < 0 || idx[q] >= n_x)) return sfail(nullptr, DLMPC_BAD_ARGUMENT, "index out of range");
+  if (int rc = op_begin(device)) return rc;
+  OpBufs B;
+  const size_t nd = (size_t)n * d;
+  int* dl = B.up(len, n); double* dv = B.up(vals, nd);
+  long long* di = B.up(reinterpret_cast<const long long*>(idx), nd); double* dx = B.up(x, n_x);
+  double* dout = B.up<double>(nullptr, n);
+  if (!dl || !dv || !di || !dx || !dout) return sfail(nullptr, DLMPC_CUDA_ERROR, "operator buffers");
+  sched::op_row_dots_kernel<<<grid_for(n, 128), 128>>>(n, d, dl, dv, di, dx, dout);
+  return op_end(out, dout, n);
+}
+
+int dlmpc_op_plant_step(int device, int n_x, int n_u, const int64_t* a_ptr, const int32_t* a_idx, const double* a_val,
+                        const int64_t* b_ptr, const int32_t* b_idx, const double* b_val, const double* x,
+                        const double* u, double* out) {
+  if (n_x < 0 || n_u < 0 || !a_ptr || !b_ptr || !x || !out || (n_u > 0 && !u)) return sfail(nullptr, DLMPC_BAD_ARGUMENT, "bad argument");
+  if (n_x == 0) return DLMPC_OK;
+  if (int rc = op_begin(device)) return rc;
+  OpBufs B;
+  const size_t na = (size_t)a_ptr[n_x], nb = (size_t)b_ptr[n_x];
+  long long* ap = B.up(reinterpret_cast<const long long*>(a_ptr), n_x + 1); int* ai = B.up(a_idx, na); double* av = B.up(a_val, na);
+  long long* bp = B.up(reinterpret_cast<const long long*>(b_ptr), n_x + 1); int* bi = B.up(b_idx, nb); double* bv = B.up(b_val, nb);
+  double* dx = B.up(x, n_x); double* du = B.up(u, n_u); double* dout = B.up<double>(nullptr, n_x);
+  if (!ap || !ai || !av || !bp || !bi || !bv || !dx || !du || !dout) return sfail(nullptr, DLMPC_CUDA_ERROR, "operator buffers");
+  sched::op_plant_kernel<<<grid_for(n_x, 128), 128>>>(n_x, ap, ai, av, bp, bi, bv, dx, du, dout);
+  return op_end(out, dout, n_x);
 }
 
 }  // extern "C"

@@ -60,7 +60,27 @@ EXPORTS = ("dlmpc_create", "dlmpc_destroy", "dlmpc_last_error", "dlmpc_global_er
            "dlmpc_phase_times", "dlmpc_audit", "dlmpc_get_cols", "dlmpc_put_cols",
            "dlmpc_finish_step", "dlmpc_set_halo", "dlmpc_halo_pack", "dlmpc_halo_unpack",
            "dlmpc_iterate_async", "dlmpc_halo_pack_async", "dlmpc_halo_unpack_async", "dlmpc_set_stream",
-           "dlmpc_fp64_peak")
+           "dlmpc_fp64_peak",
+           "dlmpc_sched_create", "dlmpc_sched_destroy", "dlmpc_sched_last_error", "dlmpc_sched_put",
+           "dlmpc_sched_get", "dlmpc_sched_set_x", "dlmpc_sched_stage", "dlmpc_sched_sync",
+           "dlmpc_sched_read_residuals", "dlmpc_sched_phi_compute", "dlmpc_sched_swap_rows",
+           "dlmpc_op_phi_rows", "dlmpc_op_psi_cols", "dlmpc_op_lambda", "dlmpc_op_residuals",
+           "dlmpc_op_row_dots", "dlmpc_op_plant_step")
+
+
+class _SchedProblem(C.Structure):
+    _fields_ = [
+        ("n_rows", C.c_int32), ("n_cols", C.c_int32), ("d_row", C.c_int32), ("d_col", C.c_int32),
+        ("n_elems", C.c_int64), ("rho", C.c_double),
+        ("row_len", _i32p), ("col_len", _i32p), ("rs", _i64p), ("c2r_flat", _i64p), ("r2c_flat", _i64p),
+        ("elem_flat_col", _i64p),
+        ("n_classes", C.c_int32), ("col_class", _i32p), ("class_m", _i32p), ("class_s", _i32p),
+        ("class_g_off", _i64p), ("g_pool", _f64p), ("class_p_off", _i64p), ("p_pool", _f64p),
+        ("col_rhs_off", _i64p), ("rhs_pool", _f64p),
+        ("n_patch", C.c_int64), ("patch_off", _i64p), ("patch_rows", _i64p), ("patch_slot", _i32p),
+        ("patch_owned", _i32p),
+        ("row_w", _f64p), ("row_lo", _f64p), ("row_hi", _f64p),
+    ]
 
 _lib = None
 
@@ -113,6 +133,27 @@ def load_library():
     lib.dlmpc_halo_unpack_async.argtypes = [vp, vp]
     lib.dlmpc_set_stream.argtypes = [vp, vp]
     lib.dlmpc_fp64_peak.argtypes = [C.c_int, _f64p]
+    lib.dlmpc_sched_create.argtypes = [_P(_SchedProblem), C.c_int, _P(vp)]
+    lib.dlmpc_sched_destroy.argtypes = [vp]
+    lib.dlmpc_sched_destroy.restype = None
+    lib.dlmpc_sched_last_error.argtypes = [vp]
+    lib.dlmpc_sched_last_error.restype = C.c_char_p
+    lib.dlmpc_sched_put.argtypes = [vp, C.c_int, _f64p]
+    lib.dlmpc_sched_get.argtypes = [vp, C.c_int, _f64p]
+    lib.dlmpc_sched_set_x.argtypes = [vp, _f64p, C.c_int64, _i64p]
+    lib.dlmpc_sched_stage.argtypes = [vp, C.c_int, C.c_int64, C.c_int64]
+    lib.dlmpc_sched_sync.argtypes = [vp]
+    lib.dlmpc_sched_read_residuals.argtypes = [vp, _f64p]
+    lib.dlmpc_sched_phi_compute.argtypes = [vp, C.c_int64, C.c_int64, _f64p]
+    lib.dlmpc_sched_swap_rows.argtypes = [vp]
+    lib.dlmpc_op_phi_rows.argtypes = [C.c_int, C.c_int, C.c_int, _i32p, _f64p, _f64p, _f64p, _f64p, _f64p,
+                                      _f64p, C.c_double, _f64p]
+    lib.dlmpc_op_psi_cols.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _f64p, _f64p, _f64p, _f64p, _f64p]
+    lib.dlmpc_op_lambda.argtypes = [C.c_int, C.c_int64, _f64p, _f64p, _f64p, _f64p]
+    lib.dlmpc_op_residuals.argtypes = [C.c_int, C.c_int, C.c_int, _i32p, _f64p, _f64p, _f64p, C.c_double, _f64p]
+    lib.dlmpc_op_row_dots.argtypes = [C.c_int, C.c_int, C.c_int, _i32p, _f64p, _i64p, C.c_int64, _f64p, _f64p]
+    lib.dlmpc_op_plant_step.argtypes = [C.c_int, C.c_int, C.c_int, _i64p, _i32p, _f64p, _i64p, _i32p, _f64p,
+                                        _f64p, _f64p, _f64p]
     _lib = lib
     return lib
 

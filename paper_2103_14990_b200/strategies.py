@@ -1,23 +1,31 @@
 """Execution-strategy plugin point (reference `strategies.py:44-314`).
 
-The reference models five CPU schedules (sequential/naive/padded/fused/
-patch-local) that differ in how many kernel launches and host syncs an ADMM
-iteration costs. This package implements the schedule all of them approximate
--- the whole solve in ONE persistent device launch -- in two arithmetic
-flavours:
+Seven variants, every one executed on the GPU:
 
-  b200        fast path: Ψ as two FP64 tensor-core GEMMs against the class
-              null-space basis, FMA-contracted Φ. Same iteration counts as the
-              reference, iterates within ~1e-14 relative (tested at 1e-9).
-  b200-exact  the reference's own arithmetic order (dense projector, numpy
-              pairwise sums, no FMA): iterates bit-identical to the
-              reference's `sequential` schedule.
+  b200         the production path: the whole solve in ONE persistent device
+               launch, Ψ as two FP64 tensor-core GEMMs against the class
+               null-space basis, FMA-contracted Φ. Same iteration counts as
+               the reference, iterates within ~1e-14 relative (tested 1e-9).
+  b200-exact   the same single launch with the reference's own arithmetic
+               order (dense projector, numpy pairwise sums, no FMA): iterates
+               bit-identical to the reference.
 
-Per iteration both cost 0 host syncs, 0 kernel launches and 0 flag reads;
-the single launch per solve is counted in `solve_launches`, so
-`counts_consistent()` keeps the reference's meaning (strategies.py:120-123).
-The reference's CPU worker pool (strategies.py:186-210) has no counterpart:
-the CUDA grid replaces it.
+and the reference's five schedule names (strategies.py:46-55), with the
+reference's per-iteration ledger constants, as real device schedules over
+the reference's dual padded layout (`schedules.py`,
+`csrc/dlmpc_schedules.cuh`; reference arithmetic, bit-identical iterates):
+
+  sequential   = b200-exact: the whole solve in one launch, (0, 0, 0)
+  naive        4 stage launches + 4 host syncs per iteration, exact-size items
+  padded       the same with longest-vector items (paper §III-B)
+  fused        Φ launch, host sync, combined column launch, flag read (§III-C)
+  patch-local  one column-patch launch, pointer swap, flag read (§III-D)
+
+The ledger counts the schedules' real launches, stream synchronisations and
+residual reads, so `counts_consistent()` keeps the reference's meaning
+(strategies.py:120-123); single-launch solves add to `solve_launches`. The
+reference's CPU worker pool (strategies.py:186-210) has no counterpart: the
+CUDA grid replaces it (`worker_count` is accepted and ignored).
 """
 
 from __future__ import annotations
@@ -27,10 +35,32 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-STRATEGY_NAMES = ("b200", "b200-exact")
+WORKERS_ENV_VAR = "LOCALITY_MPC_WORKERS"   # reference strategies.py:44
 
-# per-iteration (host syncs, kernel launches, flag reads)
-_SCHEDULE_COUNTS = {"b200": (0, 0, 0), "b200-exact": (0, 0, 0)}
+REFERENCE_SCHEDULES = ("sequential", "naive", "padded", "fused", "patch-local")
+STRATEGY_NAMES = ("b200", "b200-exact") + REFERENCE_SCHEDULES
+
+# per-iteration (host syncs, kernel launches, flag reads); the reference's
+# constants for its five names (strategies.py:49-55)
+_SCHEDULE_COUNTS = {"b200": (0, 0, 0), "b200-exact": (0, 0, 0), "sequential": (0, 0, 0),
+                    "naive": (4, 4, 0), "padded": (4, 4, 0), "fused": (1, 2, 1), "patch-local": (0, 1, 1)}
+# variants run as per-iteration device schedules (the rest: one persistent launch per solve)
+STAGED = ("naive", "padded", "fused", "patch-local")
+
+
+def default_worker_count() -> int:
+    """The reference's worker-count default (strategies.py:58-67). The device
+    schedules do not use host workers; the count is kept for the report."""
+    import os
+    env = os.environ.get(WORKERS_ENV_VAR)
+    if env:
+        try:
+            n = int(env)
+            if n >= 1:
+                return n
+        except ValueError:
+            pass
+    return os.cpu_count() or 1
 
 
 @dataclass(frozen=True)
@@ -54,10 +84,19 @@ class ExecStrategy:
 
     @property
     def exact(self) -> bool:
-        return self.variant == "b200-exact"
+        """Reference arithmetic (every variant except the fast `b200`)."""
+        return self.variant != "b200"
+
+    @property
+    def staged(self) -> bool:
+        return self.variant in STAGED
 
     def resolved_workers(self) -> int:
-        return 1
+        """Reported worker count, as the reference resolves it (strategies.py:
+        84-87); the GPU grid, not a host pool, runs every variant."""
+        if self.variant in ("sequential", "b200", "b200-exact"):
+            return 1
+        return self.worker_count if self.worker_count is not None else default_worker_count()
 
 
 @dataclass
@@ -111,6 +150,42 @@ class SyncLedger:
         }
 
 
+@dataclass
+class ColumnPatch:
+    """The row computations attached to one column's work item (reference
+    strategies.py:138-144)."""
+
+    column: int
+    member_rows: np.ndarray
+    scratch: np.ndarray | None = None
+
+
+def build_patches(tables) -> list:
+    """One patch per column; members are exactly the column's support rows
+    (reference strategies.py:147-150)."""
+    return [ColumnPatch(c, tables.cs[c, :tables.col_len[c]].copy()) for c in range(tables.n_cols)]
+
+
+def patch_duplication(patches) -> int:
+    """Duplicated row computations one patch sweep incurs (reference 153-157)."""
+    total = sum(int(p.member_rows.size) for p in patches)
+    distinct = int(np.unique(np.concatenate([p.member_rows for p in patches])).size)
+    return total - distinct
+
+
+def prepare_work_items(strategy: ExecStrategy, tables, ledger: "SyncLedger"):
+    """Per-item setup of a schedule (reference strategies.py:160-175): the
+    exact-size schedules size every item, the padded ones use the two
+    longest-vector strides; the cost lands in the ledger's setup account."""
+    start = time.perf_counter()
+    if strategy.variant in ("sequential", "naive"):
+        sizes = ([int(n) for n in tables.row_len], [int(n) for n in tables.col_len])
+    else:
+        sizes = (int(tables.d_row), int(tables.d_col))
+    ledger.setup_wall_time += time.perf_counter() - start
+    return sizes
+
+
 def reduce_convergence(pri_c: np.ndarray, dual_c: np.ndarray, eps_pri: float, eps_dual: float):
     """Order-independent global decision (reference strategies.py:178-183)."""
     pri = float(np.max(pri_c))
@@ -144,7 +219,67 @@ class Executor:
         """One ADMM iteration on the device; returns the reduced (pri, dual)
         and refreshes `ws.triple` (reference strategies.py:249-260)."""
         start = time.perf_counter()
-        pri, dual = ws.device_iterate(self.strategy)
-        self.ledger.record_launch(1, ws.last_device_ms)
+        if self.strategy.staged:
+            out = self._iter_staged(ws)
+        else:
+            out = ws.device_iterate(self.strategy)
+            self.ledger.record_launch(1, ws.last_device_ms)
         self.ledger.add_stage_time("device", time.perf_counter() - start)
+        return out
+
+    # -- the reference's schedules as device schedules ------------------------------
+    def _launch(self, eng, stage_name, stage, n_items):
+        start = time.perf_counter()
+        eng.stage(stage, 0, n_items)
+        self.ledger.kernel_launch_events += 1
+        self.ledger.add_stage_time(stage_name, time.perf_counter() - start)
+
+    def _host_sync(self, eng):
+        eng.sync()
+        self.ledger.host_sync_events += 1
+
+    def _exchange(self, eng, stage):
+        start = time.perf_counter()
+        eng.stage(stage, 0, 0)
+        self.ledger.add_stage_time("exchange", time.perf_counter() - start)
+
+    def _iter_staged(self, ws):
+        from . import schedules as S
+        v = self.strategy.variant
+        eng = ws.schedule_engine(self.strategy.device)
+        resident = ws._resident
+        if not resident:
+            ws.push_schedule_state(eng)
+        if v in ("naive", "padded"):
+            # strategies.py:283-296: four stage launches, a host sync after each
+            self._launch(eng, "phi", S.STAGE_PHI_ROWS_PADDED if v == "padded" else S.STAGE_PHI_ROWS, ws.n_rows)
+            self._host_sync(eng)
+            self._exchange(eng, S.STAGE_EXCHANGE_PHI)
+            self._launch(eng, "psi", S.STAGE_PSI_COLS, ws.n_cols)
+            self._host_sync(eng)
+            self._launch(eng, "lambda", S.STAGE_LAMBDA_ELEMS, ws.n_elems)
+            self._host_sync(eng)
+            self._launch(eng, "conv", S.STAGE_CONV_COLS, ws.n_cols)
+            pri, dual = eng.read_residuals()     # the fourth host sync carries the maxima
+            self.ledger.host_sync_events += 1
+            self._exchange(eng, S.STAGE_EXCHANGE_PSI_LAM)
+        elif v == "fused":
+            # strategies.py:298-303
+            self._launch(eng, "phi", S.STAGE_PHI_ROWS, ws.n_rows)
+            self._host_sync(eng)
+            self._exchange(eng, S.STAGE_EXCHANGE_PHI)
+            self._launch(eng, "fused", S.STAGE_FUSED_COLS, ws.n_cols)
+            pri, dual = eng.read_residuals()
+            self.ledger.flag_read_events += 1
+        else:
+            # strategies.py:305-314
+            self._launch(eng, "patch", S.STAGE_PATCH_COLS, ws.n_cols)
+            eng.swap_rows()
+            pri, dual = eng.read_residuals()
+            self.ledger.flag_read_events += 1
+            self.ledger.duplicated_row_computations += ws.duplicated_rows_per_iter
+        self.ledger.iterations += 1
+        if not resident:
+            ws.pull_schedule_state(eng)
+        ws._last_resid = (pri, dual)
         return pri, dual

@@ -189,13 +189,40 @@ class TestSpecAndRows:
 
 class TestStrategyPlugin:
     def test_variants(self):
-        assert pb.STRATEGY_NAMES == ("b200", "b200-exact")
+        # the production variants plus the reference's five names (strategies.py:46)
+        assert pb.STRATEGY_NAMES == ("b200", "b200-exact", "sequential", "naive", "padded", "fused",
+                                     "patch-local")
         assert pb.ExecStrategy().variant == "b200"
-        assert pb.ExecStrategy("b200-exact").exact
+        assert pb.ExecStrategy("b200-exact").exact and not pb.ExecStrategy("b200").exact
+        for v in ("sequential", "naive", "padded", "fused", "patch-local"):
+            s = pb.ExecStrategy(v, worker_count=4)
+            assert s.exact                     # reference arithmetic: bit-identical iterates
+            assert s.staged == (v != "sequential")
         with pytest.raises(ValueError):
-            pb.ExecStrategy("fused")          # CPU schedules are not part of this package
+            pb.ExecStrategy("gpu")
         with pytest.raises(ValueError):
             pb.ExecStrategy("b200", 0)
+
+    def test_reference_ledger_constants(self):
+        """strategies.py:49-55: (host syncs, kernel launches, flag reads)."""
+        want = {"sequential": (0, 0, 0), "naive": (4, 4, 0), "padded": (4, 4, 0), "fused": (1, 2, 1),
+                "patch-local": (0, 1, 1)}
+        for v, c in want.items():
+            led = pb.SyncLedger.for_variant(v)
+            assert (led.host_syncs_per_iter, led.kernel_launches_per_iter, led.flag_reads_per_iter) == c
+
+    def test_patches(self):
+        """build_patches / patch_duplication (strategies.py:147-157): one patch
+        per column holding its support rows; duplication = nnz - n_rows."""
+        mask = pb.build_locality_mask(pb.build_chain_network(6), 2, 4)
+        tables = pb.LayoutTables(mask)
+        patches = pb.build_patches(tables)
+        assert len(patches) == tables.n_cols
+        for p in patches:
+            assert np.array_equal(p.member_rows, tables.cs[p.column, :tables.col_len[p.column]])
+        assert pb.patch_duplication(patches) == int(tables.col_len.sum()) - tables.n_rows
+        sizes = pb.prepare_work_items(pb.ExecStrategy("padded"), tables, pb.SyncLedger.for_variant("padded"))
+        assert sizes == (tables.d_row, tables.d_col)
 
     def test_ledger(self):
         led = pb.SyncLedger.for_variant("b200")

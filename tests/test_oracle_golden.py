@@ -181,3 +181,20 @@ def test_sequential_schedule_restatement_bitwise():
     assert res["step_iterations"] == list(g["step_iters"])
     assert np.array_equal(res["states"], g["states"])
     assert np.array_equal(res["inputs"], g["inputs"])
+
+
+@pytest.mark.parametrize("name", ["c3_n1000_step0", "c3_n3000_step0"])
+def test_large_step0_bitwise_pins_the_class_shared_oracle(name):
+    """The oracle with class-shared (broadcast) operators -- the form that
+    generated the N=10^4 and C4 fixtures the reference cannot reach here
+    (make_oracle_golden.py) -- reproduces the reference's own N=1000 and
+    N=3000 step-0 solves bit for bit."""
+    import os
+    g = golden(name)
+    n, d, t, t_sim, seed = (int(v) for v in g["config"])
+    b = chain_bundle(n, t, d)
+    res = admm_ref.simulate(b["system"], b["spec"], b["tables"], b["col_solvers"], g["x0"], t_sim,
+                            workers=os.cpu_count() or 1)
+    assert res["step_iterations"] == [int(v) for v in g["step_iters"]]
+    assert np.array_equal(res["states"], g["states"])
+    assert np.array_equal(res["inputs"], g["inputs"])
