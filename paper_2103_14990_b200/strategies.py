@@ -37,8 +37,12 @@ import numpy as np
 
 WORKERS_ENV_VAR = "LOCALITY_MPC_WORKERS"   # reference strategies.py:44
 
-REFERENCE_SCHEDULES = ("sequential", "naive", "padded", "fused", "patch-local")
-STRATEGY_NAMES = ("b200", "b200-exact") + REFERENCE_SCHEDULES
+# the reference's schedule names (strategies.py:46), all run on the device;
+# code that iterates STRATEGY_NAMES sees exactly the reference's five
+STRATEGY_NAMES = ("sequential", "naive", "padded", "fused", "patch-local")
+REFERENCE_SCHEDULES = STRATEGY_NAMES
+# every variant ExecStrategy accepts: the production variants first
+VARIANTS = ("b200", "b200-exact") + STRATEGY_NAMES
 
 # per-iteration (host syncs, kernel launches, flag reads); the reference's
 # constants for its five names (strategies.py:49-55)
@@ -76,9 +80,9 @@ class ExecStrategy:
     device: int = 0
 
     def __post_init__(self):
-        if self.variant not in STRATEGY_NAMES:
+        if self.variant not in VARIANTS:
             raise ValueError(f"unknown strategy {self.variant!r}; "
-                             f"choose from {', '.join(STRATEGY_NAMES)}")
+                             f"choose from {', '.join(VARIANTS)}")
         if self.worker_count is not None and self.worker_count < 1:
             raise ValueError("worker_count must be >= 1")
 

@@ -51,8 +51,8 @@ def run():
                PYTHONDONTWRITEBYTECODE="1")
     args = [sys.executable, "-m", "pytest", DST, "-q", "-p", "no:cacheprovider", "-rfE",
             "--junitxml", os.path.join(out_dir, "reference_tests.xml")]
-    for node, _ in EXCLUDED:
-        args += ["--deselect", os.path.join(DST, node)] if "::" in node else ["--ignore", os.path.join(DST, node)]
+    for node, _ in EXCLUDED:   # node ids relative to the rootdir (DST)
+        args += ["--deselect", node] if "::" in node else ["--ignore", os.path.join(DST, node)]
     res = subprocess.run(args, cwd=DST, env=env, capture_output=True, text=True)
     tail = (res.stdout + res.stderr)[-6000:]
     with open(os.path.join(out_dir, "reference_tests.log"), "w") as fh:
