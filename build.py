@@ -18,6 +18,9 @@ SOURCES = [os.path.join(SRC_DIR, "dlmpc.cu")]
 DEPS = SOURCES + [os.path.join(SRC_DIR, "dlmpc_device.cuh"), os.path.join(SRC_DIR, "dlmpc_schedules.cuh"),
         os.path.join(ROOT, "include", "dlmpc.h")]
 OUT = os.path.join(PKG, "libdlmpc.so")
+# bounds-checked variant (-DDLMPC_CHECKED): the pool has no compute-sanitizer,
+# so the tests run the kernels once more with every risky access checked
+OUT_CHECKED = os.path.join(PKG, "libdlmpc_checked.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 
@@ -27,17 +30,18 @@ def nvcc():
     return cand if os.path.exists(cand) else "nvcc"
 
 
-def needs_build():
-    if not os.path.exists(OUT):
+def needs_build(out=OUT):
+    if not os.path.exists(out):
         return True
-    t = os.path.getmtime(OUT)
+    t = os.path.getmtime(out)
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
-        return OUT
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", OUT] + SOURCES
+def build(force=False, verbose=False, checked=False):
+    out = OUT_CHECKED if checked else OUT
+    if not force and not needs_build(out):
+        return out
+    cmd = [nvcc()] + NVCC_FLAGS + (["-DDLMPC_CHECKED"] if checked else []) + ["-o", out] + SOURCES
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
@@ -46,8 +50,8 @@ def build(force=False, verbose=False):
         for line in (res.stdout + res.stderr).splitlines():
             if "registers" in line or "spill" in line or "error" in line:
                 print(line)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

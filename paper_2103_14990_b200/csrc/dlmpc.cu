@@ -162,11 +162,29 @@ int finish_timing(dlmpc_handle* h) {
   return DLMPC_OK;
 }
 
+// Checked build: a recorded out-of-range access (dlmpc_device.cuh DCHK) fails
+// the call loudly; the production build has no checks.
+int check_dbg(dlmpc_handle* h) {
+#ifdef DLMPC_CHECKED
+  int dbg[4] = {0, 0, 0, 0};
+  CUDA_OR_FAIL(h, cudaMemcpy(dbg, h->P.dbg, sizeof(dbg), cudaMemcpyDeviceToHost));
+  if (dbg[0] != 0) {
+    long long idx = 0;
+    std::memcpy(&idx, dbg + 2, sizeof(idx));
+    return fail(h, DLMPC_CUDA_ERROR, "checked build: out-of-range access, check " + std::to_string(dbg[0]) +
+                                         " at index " + std::to_string(idx));
+  }
+#else
+  (void)h;
+#endif
+  return DLMPC_OK;
+}
+
 int read_ctl(dlmpc_handle* h, int* ctl) {
   CUDA_OR_FAIL(h, cudaMemcpyAsync(ctl, h->P.ctl, sizeof(int) * 8, cudaMemcpyDeviceToHost, h->stream));
   CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
   h->cur_b = ctl[4]; h->b_valid = 1;
-  return DLMPC_OK;
+  return check_dbg(h);
 }
 
 // The current buffer without a round trip when the host knows it (after
@@ -402,6 +420,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
             tot += (long long)(z - a + 1) * (pr->row_start[i + 1] - pr->row_start[i]);
           }
           part_total = tot;
+          P.part_cap = std::max<long long>(1, tot);
           if (ok) {
             h->mode = kStream;
             // host-built control tables (see DevProblem)
@@ -656,6 +675,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       }
     }
   }
+  P.smem_doubles = h->smem_bytes / 8;
   KernelFn fn = pick_kernel(h->mode, P.tile_cols, P.rb_gemv);
   CUDA_OR_FAIL(h, cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
@@ -739,6 +759,7 @@ int dlmpc_create(const dlmpc_problem* pr, int device, dlmpc_handle** out) {
     if ((rc = alloc(h, (size_t)pr->n_sub + 2, &P.ada)) != DLMPC_OK) goto bad;
     if ((rc = alloc(h, (size_t)(pr->n_inputs ? pr->n_inputs : 1), &P.u)) != DLMPC_OK) goto bad;
     if ((rc = alloc(h, 8, &P.ctl)) != DLMPC_OK) goto bad;
+    if ((rc = alloc(h, 4, &P.dbg)) != DLMPC_OK) goto bad;
     if ((rc = alloc(h, ncell, &h->d_scratch)) != DLMPC_OK) goto bad;
     if ((rc = alloc(h, 16 * 1024, &P.phase_ns)) != DLMPC_OK) goto bad;
     if (cudaMemset(P.ctl + 2, 0x7f, sizeof(int) * 2) != cudaSuccess) { rc = fail(h, DLMPC_CUDA_ERROR, "memset"); goto bad; }
@@ -1140,7 +1161,7 @@ void* dlmpc_stream(dlmpc_handle* h) { return h ? static_cast<void*>(h->stream) :
 int dlmpc_synchronize(dlmpc_handle* h) {
   if (!h) return DLMPC_BAD_ARGUMENT;
   CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
-  return DLMPC_OK;
+  return check_dbg(h);
 }
 
 int dlmpc_audit(dlmpc_handle* h, const double* phi_host, double* out3) {

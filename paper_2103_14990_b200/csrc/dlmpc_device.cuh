@@ -140,6 +140,11 @@ struct DevProblem {
   int rb_gemv;                 // patch mode, TC 8: register-blocked GEMV pair for chunks of <= 2 columns
   int stash_cols;              // columns per ψ,λ staging buffer (TC, or 2 with rb_gemv)
   int g1_mrow;                 // GEMM 1 by whole m-rows where it pays (DLMPC_G1_MROW=0 disables: A/B tests)
+  // checked build (-DDLMPC_CHECKED, libdlmpc_checked.so): the first out-of-range
+  // access is recorded here (code, then the offending index) and skipped
+  int* dbg;                    // [4]: code, -, index (long long)
+  long long part_cap;          // stream mode: doubles per Φ-partials buffer
+  long long smem_doubles;      // dynamic shared memory of the plan
 };
 
 struct RunArgs {
@@ -159,6 +164,27 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+// Bounds checks of the checked build (there is no compute-sanitizer on the
+// GPU pool): DCHK(P, cond, code, idx) records the first failing (code, idx)
+// in P.dbg and returns false so the caller skips the access; the host turns a
+// recorded violation into DLMPC_CUDA_ERROR. In the production build it is
+// the constant `true` and compiles away.
+#ifdef DLMPC_CHECKED
+__device__ __noinline__ bool dchk_fail(const DevProblem& P, int code, long long idx) {
+  if (atomicCAS(P.dbg, 0, code) == 0) reinterpret_cast<long long*>(P.dbg)[1] = idx;
+  return false;
+}
+#define DCHK(P, cond, code, idx) ((cond) ? true : dchk_fail((P), (code), static_cast<long long>(idx)))
+#else
+#define DCHK(P, cond, code, idx) true
+#endif
+// the owned support cell `pos` of the column layout (epilogue stores)
+#define DCHK_CELL(P, pos, code)                                                                      \
+  DCHK(P, (pos) >= static_cast<long long>((P).own_col_lo) * (P).s_pad &&                              \
+              (pos) < static_cast<long long>((P).own_col_hi) * (P).s_pad &&                           \
+              ((pos) % (P).s_pad) < (P).col_len[(pos) / (P).s_pad], code, pos)
+#define DCHK_ROW(P, r, code) DCHK(P, (r) >= 0 && (r) < (P).n_rows, code, r)
 
 __device__ __forceinline__ void cp_async16(double* smem_dst, const double* gmem_src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
@@ -424,7 +450,8 @@ __device__ __forceinline__ void phi_rows_of(const DevProblem& P, int i, const do
           const long long bk = __shfl_sync(0xffffffffu, base_k, (u0 + u) & 31);
           xv[u] = __shfl_sync(0xffffffffu, x_k, (u0 + u) & 31);
           pv[u] = 0.0; lv[u] = 0.0;
-          if (row_ok && u0 + u < kn) {
+          if (row_ok && u0 + u < kn &&
+              DCHK(P, bk + l >= 0 && bk + l < static_cast<long long>(P.n_cols) * P.s_pad, 9, bk + l)) {
             pv[u] = ld_cg(psi + bk + l);
             lv[u] = ld_cg(lam + bk + l);
           }
@@ -949,8 +976,10 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
             const double phi = make_phi<false>(__dsub_rn(ps[u], lm[u]), sr[u], xc);
             const double pn = qv[u] + kt[t * ldk + p];
             const double d = __dsub_rn(phi, pn);
-            psi_n[pos0 + p] = pn;
-            lam_n[pos0 + p] = __dadd_rn(lm[u], d);
+            if (DCHK_CELL(P, pos0 + p, 1)) {
+              psi_n[pos0 + p] = pn;
+              lam_n[pos0 + p] = __dadd_rn(lm[u], d);
+            }
             pri_m = rmax(pri_m, fabs(d));
             dual_m = rmax(dual_m, fabs(__dsub_rn(pn, ps[u])));
           }
@@ -1055,8 +1084,10 @@ __device__ void rb_chunk_al(const DevProblem& P, int k, int nt, double* psi_n, d
     const double phi = make_phi<false>(__dsub_rn(e_ps, e_lm), e_sr, e_x);
     const double pn = e_q + o;
     const double d = __dsub_rn(phi, pn);
-    psi_n[e_pos + ep] = pn;
-    lam_n[e_pos + ep] = __dadd_rn(e_lm, d);
+    if (DCHK_CELL(P, e_pos + ep, 2)) {
+      psi_n[e_pos + ep] = pn;
+      lam_n[e_pos + ep] = __dadd_rn(e_lm, d);
+    }
     pri_m = rmax(pri_m, fabs(d));
     dual_m = rmax(dual_m, fabs(__dsub_rn(pn, e_ps)));
   };
@@ -1225,8 +1256,10 @@ __device__ __forceinline__ void phi_rows_cached(const DevProblem& P, int q, int 
         pv[u] = lv[u] = 0.0;
         if (k0 + u < D) {
           const long long b = bk[k0 + u] + l;
-          pv[u] = ld_cg(psi + b);
-          lv[u] = ld_cg(lam + b);
+          if (DCHK(P, b >= 0 && b < static_cast<long long>(P.n_cols) * P.s_pad, 10, b)) {
+            pv[u] = ld_cg(psi + b);
+            lv[u] = ld_cg(lam + b);
+          }
         }
       }
 #pragma unroll
@@ -1341,7 +1374,9 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
         cp_async_wait<0>();
         return true;
       }
-      for (int r = threadIdx.x; r < o_n; r += kThreads) P.s_row[prow0 + o_off + r] = s_patch[o_off + r];
+      for (int r = threadIdx.x; r < o_n; r += kThreads)
+        if (DCHK_ROW(P, prow0 + o_off + r, 5) && DCHK(P, o_off + r < P.patch_cap, 6, o_off + r))
+          P.s_row[prow0 + o_off + r] = s_patch[o_off + r];
     }
     PT_LAP(P, 7)
     // chunk pipeline: ψ,λ of chunk i+1 stream into the other staging buffer
@@ -1415,6 +1450,13 @@ __device__ __forceinline__ void stash_cols_bulk(const DevProblem& P, int c0, int
                                                 double* st, unsigned long long* bar, int issuer = 0) {
   if (threadIdx.x == issuer) {
     const unsigned bytes = static_cast<unsigned>(P.s_pad) * 8u;
+#ifdef DLMPC_CHECKED
+    extern __shared__ double dyn_smem_chk[];
+    if (!DCHK(P, c0 >= 0 && c0 + nt <= P.n_cols, 11, c0) ||
+        !DCHK(P, (st - dyn_smem_chk) + static_cast<long long>(nt - 1) * P.ldk + P.s_pad <= P.smem_doubles, 12,
+              st - dyn_smem_chk))
+      nt = 0;
+#endif
     fence_proxy_async();
     mbar_expect_tx(bar, bytes * nt);
     if (P.ldk == P.s_pad)   // consecutive columns are one contiguous range
@@ -1433,6 +1475,13 @@ __device__ __forceinline__ void stash_lam_bulk(const DevProblem& P, int c0, int 
   if ((threadIdx.x >> 5) == kWarps - 1) {
     const int lane = threadIdx.x & 31;
     const unsigned bytes = static_cast<unsigned>(P.s_pad) * 8u;
+#ifdef DLMPC_CHECKED
+    extern __shared__ double dyn_smem_chk[];
+    if (!DCHK(P, c0 >= 0 && c0 + nt <= P.n_cols, 13, c0) ||
+        !DCHK(P, (st - dyn_smem_chk) + static_cast<long long>(nt - 1) * ldl + P.s_pad <= P.smem_doubles, 14,
+              st - dyn_smem_chk))
+      nt = 0;
+#endif
     if (lane == 0) mbar_expect_tx(bar, bytes * nt);
     __syncwarp();
     if (lane < nt) {
@@ -1456,6 +1505,9 @@ struct StreamEpi {
   unsigned long long* lam_bar; unsigned lam_phase;   // if set: λ lands before the first store
   bool paired;   // column pairs (2q, 2q+1) share support rows (host flag per chunk)
   double qv[kMG2][NTN][2];
+#ifdef DLMPC_CHECKED
+  const DevProblem* Pc = nullptr;   // bounds checks of the epilogue stores
+#endif
 #ifdef DLMPC_PHASE_TIMING
   unsigned long long t_kloop = 0, t_lam = 0;   // profiling build: end of the k loop, λ landed (thread 0)
   __device__ __forceinline__ void before_store() {
@@ -1495,8 +1547,10 @@ struct StreamEpi {
         s_pair = sv;
         const double ps = fma(-sv, m_x[t], kv);
         const long long pos = m_pos[t] + p;
-        psi_n[pos] = pn;
-        lam_n[pos] = ln;
+        if (DCHK_CELL((*Pc), pos, 3)) {
+          psi_n[pos] = pn;
+          lam_n[pos] = ln;
+        }
         pri_m = rmax(pri_m, fabs(__dsub_rn(ln, lm)));
         dual_m = rmax(dual_m, fabs(__dsub_rn(pn, ps)));
         const double v = __dsub_rn(pn, ln);
@@ -1681,7 +1735,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
           const double y = fmin(fmax(rho * c[u] * w[u], lo[u]), hi[u]);
           const double sv = (y - c[u]) * ada[u];
           s_patch[r0 + u * kThreads] = sv;
-          if (own[u]) P.s_row[grow[u]] = sv;
+          if (own[u] && DCHK_ROW(P, grow[u], 7)) P.s_row[grow[u]] = sv;
         }
       }
     }
@@ -1798,6 +1852,9 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
           PT_LAP(P, 12)
           StreamEpi<TC> epi{P.psi[b ^ 1], P.lam[b ^ 1], P.q_pool, m_pos, m_s, m_q, m_x,
                             s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, bars + 2, (ph >> 2) & 1u, ce[6] != 0};
+#ifdef DLMPC_CHECKED
+          epi.Pc = &P;
+#endif
           gemm2<TC, StreamEpi<TC>, kCons>(S8, n08, ldn, nop, yb, P.ldy, epi);
           pri_m = epi.pri_m; dual_m = epi.dual_m;
 #ifdef DLMPC_PHASE_TIMING
@@ -1850,6 +1907,9 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       PT_LAP(P, 2)
       StreamEpi<TC> epi{P.psi[b ^ 1], P.lam[b ^ 1], P.q_pool, m_pos, m_s, m_q, m_x,
                         s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, nullptr, 0u, ce[6] != 0};
+#ifdef DLMPC_CHECKED
+      epi.Pc = &P;
+#endif
       gemm2<TC>(S8, n08, ldn, nop, yb, P.ldy, epi);
       pri_m = epi.pri_m; dual_m = epi.dual_m;
       __syncthreads();
@@ -1877,7 +1937,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       const int q = rowq[r];
       const double* e = ptab + 6 * q;
       const int* ei = reinterpret_cast<const int*>(e);
-      part_out[reinterpret_cast<const long long*>(e)[2] + static_cast<long long>(ei[3]) * ei[1] + (r - ei[0])] =
+      const long long pidx = reinterpret_cast<const long long*>(e)[2] + static_cast<long long>(ei[3]) * ei[1] + (r - ei[0]);
+      if (DCHK(P, pidx >= 0 && pidx < P.part_cap, 8, pidx)) part_out[pidx] =
           c_patch[r];
     }
     __syncthreads();
@@ -1934,8 +1995,10 @@ __device__ void column_stage_exact(const DevProblem& P, int b, const double* x, 
       const size_t pos = static_cast<size_t>(c) * sp + p;
       const double pn = pnew[p];
       const double d = __dsub_rn(phi_s[p], pn);
-      psi_n[pos] = pn;
-      lam_n[pos] = __dadd_rn(lam_s[p], d);
+      if (DCHK_CELL(P, static_cast<long long>(pos), 4)) {
+        psi_n[pos] = pn;
+        lam_n[pos] = __dadd_rn(lam_s[p], d);
+      }
       pri_m = rmax(pri_m, fabs(d));
       dual_m = rmax(dual_m, fabs(__dsub_rn(pn, psi_s[p])));
     }
