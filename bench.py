@@ -198,7 +198,7 @@ def algorithmic_work(sess):
 
 
 def ncu_traffic():
-    path = os.path.join(ROOT, "profiles", "ncu_c2_summary.json")
+    path = os.path.join(ROOT, "profiles", "ncu_c2_summary_r02.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
@@ -331,7 +331,7 @@ def sweep(pb, hbm_peak, fp64_peak, cpu_seconds=6.0):
                  "hbm_gbs": bytes_it / s_it / 1e9, "hbm_frac": bytes_it / s_it / 1e9 / hbm_peak,
                  "flops_per_iteration": flops_it, "bytes_per_iteration": bytes_it,
                  "parity": sweep_parity(n, traj, sess, spec)}
-        summ = os.path.join(ROOT, "profiles", f"ncu_stream_n1e{len(str(n)) - 1}_summary.json")
+        summ = os.path.join(ROOT, "profiles", f"ncu_stream_n1e{len(str(n)) - 1}_summary_r02.json")
         if os.path.exists(summ):   # ncu evidence for this size (one capture, committed)
             try:
                 with open(summ) as fh:

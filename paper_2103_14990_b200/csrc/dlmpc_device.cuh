@@ -171,11 +171,17 @@ __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 // recorded violation into DLMPC_CUDA_ERROR. In the production build it is
 // the constant `true` and compiles away.
 #ifdef DLMPC_CHECKED
-__device__ __noinline__ bool dchk_fail(const DevProblem& P, int code, long long idx) {
-  if (atomicCAS(P.dbg, 0, code) == 0) reinterpret_cast<long long*>(P.dbg)[1] = idx;
+__device__ __noinline__ bool dchk_fail(int* dbg, int code, long long idx) {
+  if (atomicCAS(dbg, 0, code) == 0) reinterpret_cast<long long*>(dbg)[1] = idx;
   return false;
 }
-#define DCHK(P, cond, code, idx) ((cond) ? true : dchk_fail((P), (code), static_cast<long long>(idx)))
+#ifndef DLMPC_CHECKED_NODCHK
+#define DCHK(P, cond, code, idx) ((cond) ? true : dchk_fail((P).dbg, (code), static_cast<long long>(idx)))
+#else
+#define DCHK(P, cond, code, idx) true
+#endif
+// the fields DCHK_CELL reads, for code that holds no DevProblem (StreamEpi)
+struct CellChk { int* dbg; int own_col_lo, own_col_hi, s_pad; const int* col_len; };
 #else
 #define DCHK(P, cond, code, idx) true
 #endif
@@ -1506,7 +1512,7 @@ struct StreamEpi {
   bool paired;   // column pairs (2q, 2q+1) share support rows (host flag per chunk)
   double qv[kMG2][NTN][2];
 #ifdef DLMPC_CHECKED
-  const DevProblem* Pc = nullptr;   // bounds checks of the epilogue stores
+  CellChk chk;   // bounds checks of the epilogue stores
 #endif
 #ifdef DLMPC_PHASE_TIMING
   unsigned long long t_kloop = 0, t_lam = 0;   // profiling build: end of the k loop, λ landed (thread 0)
@@ -1547,7 +1553,7 @@ struct StreamEpi {
         s_pair = sv;
         const double ps = fma(-sv, m_x[t], kv);
         const long long pos = m_pos[t] + p;
-        if (DCHK_CELL((*Pc), pos, 3)) {
+        if (DCHK_CELL(chk, pos, 3)) {
           psi_n[pos] = pn;
           lam_n[pos] = ln;
         }
@@ -1853,7 +1859,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
           StreamEpi<TC> epi{P.psi[b ^ 1], P.lam[b ^ 1], P.q_pool, m_pos, m_s, m_q, m_x,
                             s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, bars + 2, (ph >> 2) & 1u, ce[6] != 0};
 #ifdef DLMPC_CHECKED
-          epi.Pc = &P;
+          epi.chk = CellChk{P.dbg, P.own_col_lo, P.own_col_hi, P.s_pad, P.col_len};
 #endif
           gemm2<TC, StreamEpi<TC>, kCons>(S8, n08, ldn, nop, yb, P.ldy, epi);
           pri_m = epi.pri_m; dual_m = epi.dual_m;
@@ -1908,7 +1914,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       StreamEpi<TC> epi{P.psi[b ^ 1], P.lam[b ^ 1], P.q_pool, m_pos, m_s, m_q, m_x,
                         s_patch, kt, lam_st, ldk, ldl, S, nt, pri_m, dual_m, nullptr, 0u, ce[6] != 0};
 #ifdef DLMPC_CHECKED
-      epi.Pc = &P;
+      epi.chk = CellChk{P.dbg, P.own_col_lo, P.own_col_hi, P.s_pad, P.col_len};
 #endif
       gemm2<TC>(S8, n08, ldn, nop, yb, P.ldy, epi);
       pri_m = epi.pri_m; dual_m = epi.dual_m;
