@@ -147,6 +147,8 @@ int launch(dlmpc_handle* h, const RunArgs& R) {
   DevProblem P = h->P;
   RunArgs Rc = R;
   void* args[] = {&P, &Rc};
+  if (h->P.pair_flag)   // K-split pair counters restart with every launch
+    CUDA_OR_FAIL(h, cudaMemsetAsync(h->P.pair_flag, 0, sizeof(unsigned) * h->grid, h->stream));
   CUDA_OR_FAIL(h, cudaEventRecord(h->ev0, h->stream));
   CUDA_OR_FAIL(h, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(h->grid), dim3(kThreads),
                                               args, static_cast<size_t>(h->smem_bytes), h->stream));
@@ -245,6 +247,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
     std::vector<int64_t> part_off;
     std::vector<int> st_unit_desc, st_chunk_desc, st_cta_gop;
     std::vector<double> st_ptab;
+    std::vector<int> cta_pair;   // patch mode: per CTA -1, or partner * 2 + half (K-split pairs)
     long long part_total = 0;
     long long prows_max = 0, np_max = 0;
     if (h->mode == kPatch) {
@@ -277,13 +280,76 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           if (best < 0) break;
           ctas[best]++;
         }
+        // K-split pairs (C4 large bases): a run of ONE subsystem
+        // whose class operator cannot be resident in shared memory (its CTA
+        // streams an unshared basis from L2 and is the straggler, e.g. d=6,
+        // T=30: 235 vs 187 us) gets a second CTA; the two split the support
+        // rows of GEMM 1 / GEMM 2 and exchange their partial Y. The CTAs come
+        // from multi-subsystem runs that can give one up without any CTA's
+        // chunk count growing. Not in stream mode (duplicated units would
+        // duplicate the Φ partials).
+        std::vector<char> paired(nr, 0);
+        {
+          const bool stream_likely = (long long)P.n_cols >= 2LL * tc * G ||
+                                     (getenv("DLMPC_FORCE_STREAM") && getenv("DLMPC_FORCE_STREAM")[0] == '1');
+          const char* np = getenv("DLMPC_NO_PAIRS");
+          const bool l2_fed = opr_need * 8 > 3 * limit * 8 / 4;   // the operator region will not hold the basis
+          if (!stream_likely && l2_fed && !(np && np[0] == '1')) {
+            std::vector<int> cand;
+            for (int r = 0; r < nr; ++r)
+              if (run_hi[r] - run_lo[r] == 1 && ctas[r] == 1) cand.push_back(r);
+            auto work = [&](int r) {
+              const int k = sub_class(run_lo[r]);
+              return (long long)pr->class_s[k] * pr->class_n0[k];
+            };
+            std::sort(cand.begin(), cand.end(), [&](int a, int b) { return work(a) > work(b); });
+            int spare = 0;
+            if (!cand.empty()) {
+              for (int r = 0; r < nr; ++r) {
+                const int n = run_hi[r] - run_lo[r];
+                if (n <= 1) continue;
+                const long long spc = (cols[r] + n - 1) / n;
+                auto chunks = [&](int c) { return ((n + c - 1) / c * spc + tc - 1) / tc; };
+                const long long want = chunks(ctas[r]);
+                int c = ctas[r];
+                while (c > 1 && chunks(c - 1) == want) --c;
+                spare += ctas[r] - c;
+                ctas[r] = c;
+              }
+            }
+            for (int r : cand)
+              if (spare > 0) { paired[r] = 1; ctas[r] = 2; --spare; }
+            for (; spare > 0; --spare) {   // the rest back to the most loaded runs
+              int best = -1; double load = -1.0;
+              for (int r = 0; r < nr; ++r) {
+                if (paired[r] || ctas[r] >= run_hi[r] - run_lo[r]) continue;
+                const double l = (double)cols[r] / ctas[r];
+                if (l > load) { load = l; best = r; }
+              }
+              if (best < 0) break;
+              ctas[best]++;
+            }
+          }
+        }
         for (int r = 0; r < nr; ++r) {
           const int n = run_hi[r] - run_lo[r];
+          if (paired[r]) {   // both CTAs run the same unit, halves 0 and 1 of the support rows
+            const int q0 = (int)ranges.size() / 2;
+            for (int half = 0; half < 2; ++half) {
+              ranges.push_back(run_lo[r]);
+              ranges.push_back(run_hi[r]);
+            }
+            if ((int)cta_pair.size() < q0) cta_pair.resize(q0, -1);
+            cta_pair.push_back(2 * (q0 + 1) + 0);
+            cta_pair.push_back(2 * q0 + 1);
+            continue;
+          }
           for (int q = 0; q < ctas[r]; ++q) {
             ranges.push_back(run_lo[r] + (int)((long long)n * q / ctas[r]));
             ranges.push_back(run_lo[r] + (int)((long long)n * (q + 1) / ctas[r]));
           }
         }
+        if (!cta_pair.empty()) cta_pair.resize(G, -1);
       } else {
         const int n_own = o_hi - o_lo;
         for (int q = 0; q < G; ++q) {
@@ -556,7 +622,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       // iteration against the DFMA GEMV + DMMA GEMM pair). That path needs no K tile and stages
       // two columns, which keeps the plan inside the 196 KB carveout (a larger
       // one leaves too little L1 for the kernel's table loads: -25% measured).
-      bool rb = h->mode == kPatch && tc == 8 && !rb_off;
+      bool rb = h->mode == kPatch && tc == 8 && !rb_off && cta_pair.empty();
       const int rb_al = RB_AL_MAX;
       for (int n : ch_n) rb = rb && n <= 2;
       for (int k = 0; k < pr->n_classes && rb; ++k) {
@@ -651,6 +717,17 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           (rc = upload(h, ch_n.data(), ch_n.size(), &P.chunk_n)))
         return rc;
       if (h->mode == kPatch && (rc = alloc(h, 1, &P.gbar))) return rc;
+      if (h->mode == kPatch && !cta_pair.empty()) {
+        if ((rc = upload(h, cta_pair.data(), cta_pair.size(), &P.cta_pair)) ||
+            (rc = alloc(h, (size_t)G, &P.pair_flag)) ||
+            (rc = alloc(h, (size_t)2 * G * P.n08_max * P.tile_cols, &P.ypair)))
+          return rc;
+        if (getenv("DLMPC_DEBUG_PLAN")) {
+          int np = 0;
+          for (int v : cta_pair) np += v >= 0;
+          fprintf(stderr, "plan: %d CTAs in K-split pairs\n", np);
+        }
+      }
       if (h->mode == kStream) {
         if ((rc = upload(h, st_cta_gop.data(), st_cta_gop.size(), &P.cta_gop)) ||
             (rc = upload(h, st_unit_desc.data(), st_unit_desc.size(), &P.unit_desc)) ||

@@ -143,6 +143,11 @@ struct DevProblem {
   // checked build (-DDLMPC_CHECKED, libdlmpc_checked.so): the first out-of-range
   // access is recorded here (code, then the offending index) and skipped
   int* dbg;                    // [4]: code, -, index (long long)
+  // patch mode, K-split pairs: per CTA -1 or partner * 2 + half; the two CTAs
+  // run the same unit on halves of the support rows and swap partial Y
+  const int* cta_pair;
+  unsigned* pair_flag;         // [grid] partial-Y publications (monotonic per launch)
+  double* ypair;               // [grid][2][n08_max * TC] partial Y, double-buffered
   long long part_cap;          // stream mode: doubles per Φ-partials buffer
   long long smem_doubles;      // dynamic shared memory of the plan
 };
@@ -879,10 +884,47 @@ struct StoreO {
 // `irow` non-null, the global generic layout maps support slots to rows.
 // shared: kt [TC][ldk] (K, then O), yb [n08][ldy], yp [split][n08][TC].
 // ---------------------------------------------------------------------------
+// K-split pairs (P.cta_pair, patch mode): this CTA's half of the support
+// rows [p_lo, p_hi) in GEMM 1 (partial Y), GEMM 2 and the epilogue; the two
+// partial Y are swapped through global memory (double-buffered, a release /
+// acquire counter per CTA) and summed in the same order in both CTAs.
+struct KSplit {
+  int partner = -1, half = 0;
+  int* cnt = nullptr;   // this CTA's publications so far in the launch
+};
+
+__device__ __forceinline__ void ksplit_exchange_y(const DevProblem& P, const KSplit& ks, double* yb, int ldy,
+                                                  int n08, int TCc) {
+  const int tid = threadIdx.x;
+  const int slot = *ks.cnt & 1;
+  const size_t per = static_cast<size_t>(P.n08_max) * TCc;
+  double* mine = P.ypair + (static_cast<size_t>(blockIdx.x) * 2 + slot) * per;
+  const double* theirs = P.ypair + (static_cast<size_t>(ks.partner) * 2 + slot) * per;
+  for (int idx = tid; idx < n08 * TCc; idx += kThreads) {
+    const int a = idx / TCc, t = idx - a * TCc;
+    mine[idx] = yb[a * ldy + t];
+  }
+  __syncthreads();
+  *ks.cnt += 1;
+  if (tid == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" :: "l"(P.pair_flag + blockIdx.x) : "memory");
+    while (static_cast<int>(ld_acquire_u32(P.pair_flag + ks.partner) - static_cast<unsigned>(*ks.cnt)) < 0) {}
+  }
+  __syncthreads();
+  for (int idx = tid; idx < n08 * TCc; idx += kThreads) {
+    const int a = idx / TCc, t = idx - a * TCc;
+    const double o = __ldcg(theirs + idx), m = yb[a * ldy + t];
+    yb[a * ldy + t] = ks.half == 0 ? m + o : o + m;   // Y = Y(half 0) + Y(half 1) in both CTAs
+  }
+  __syncthreads();
+}
+
 template <int TC, bool S_GLOBAL, bool OPS>
 __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi, const double* lam,
                            double* psi_n, double* lam_n, const double* s_src, const int* irow_tab,
-                           double* smem, double& pri_m, double& dual_m, const double* st) {
+                           double* smem, double& pri_m, double& dual_m, const double* st,
+                           const KSplit& ks = KSplit()) {
   constexpr int NTN = TC / 8;
   constexpr int WPC = kWarps / TC;   // warps per column in the element loops
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -903,15 +945,18 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
   PT_DECL
   PT_START
   const int t_el = warp / WPC;                  // this warp's column in element loops
-  const int p_el0 = (warp % WPC) * 32 + lane;   // first support slot
   constexpr int PSTEP = 32 * WPC;
+  // support rows of this CTA: all, or its half of a K-split pair (multiple of 8)
+  const int p_lo = ks.partner < 0 || ks.half == 0 ? 0 : ((S8 >> 1) + 7) & ~7;
+  const int p_hi = ks.partner < 0 || ks.half == 1 ? S8 : ((S8 >> 1) + 7) & ~7;
+  const int p_el0 = p_lo + (warp % WPC) * 32 + lane;   // first support slot
   // prologue: K[t][p] = φ + λ (admm.py:183), zero padded to TC x S8
   {
     const int t = t_el;
     const bool col_ok = t < nt;
     const long long pos0 = col_ok ? m_pos[t] : 0, s0 = col_ok ? m_s[t] : 0;
     const double xc = col_ok ? m_x[t] : 0.0;
-    for (int pb = p_el0; pb < S8; pb += 4 * PSTEP) {
+    for (int pb = p_el0; pb < p_hi; pb += 4 * PSTEP) {
       double ps[4], lm[4], sr[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -931,7 +976,7 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int p = pb + u * PSTEP;
-        if (p < S8) {
+        if (p < p_hi) {
           double kv = 0.0;
           if (col_ok && p < S) kv = __dadd_rn(make_phi<false>(__dsub_rn(ps[u], lm[u]), sr[u], xc), lm[u]);
           kt[t * ldk + p] = kv;
@@ -941,14 +986,16 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
   }
   __syncthreads();
   PT_LAP(P, 1)
-  if (TC == 8 && nt <= 2 && P.small_gemv && n08 * 10 <= kThreads)
+  if (TC == 8 && nt <= 2 && P.small_gemv && n08 * 10 <= kThreads && ks.partner < 0)
     gemv1_small<TC>(S, n08, ldn, nop, kt, ldk, yp, yb, ldy, nt);
   else
-    gemm1<TC, NoHook, kWarps, CtaBar, 1>(P, S8, n08, ldn, nop, kt, ldk, yb, ldy, yp);
+    gemm1<TC, NoHook, kWarps, CtaBar, 1>(P, p_hi - p_lo, n08, ldn, nop + static_cast<size_t>(p_lo) * ldn,
+                                         kt + p_lo, ldk, yb, ldy, yp);
+  if (ks.partner >= 0) ksplit_exchange_y(P, ks, yb, ldy, n08, TC);
   PT_LAP(P, 2)
   // GEMM 2: O[t][p] = sum_a N[p][a] Y[a][t]  (M = S, N = TC, K = n0) -> kt
-  StoreO epi{kt, ldk};
-  gemm2<TC>(S8, n08, ldn, nop, yb, ldy, epi);
+  StoreO epi{kt + p_lo, ldk};
+  gemm2<TC>(p_hi - p_lo, n08, ldn, nop + static_cast<size_t>(p_lo) * ldn, yb, ldy, epi);
   __syncthreads();
   PT_LAP(P, 3)
   // epilogue: ψ' = q + O, λ' = λ + (φ - ψ'), residuals (admm.py:186, 207, 216-217)
@@ -957,13 +1004,14 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
     if (t < nt) {
       const long long pos0 = m_pos[t], s0 = m_s[t], q0 = m_q[t];
       const double xc = m_x[t];
-      for (int pb = p_el0; pb < S; pb += 4 * PSTEP) {
+      const int p_end = min(S, p_hi);
+      for (int pb = p_el0; pb < p_end; pb += 4 * PSTEP) {
         double ps[4], lm[4], sr[4], qv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int p = pb + u * PSTEP;
           ps[u] = lm[u] = sr[u] = qv[u] = 0.0;
-          if (p < S) {
+          if (p < p_end) {
             if (st) {
               ps[u] = st[(2 * t) * ldk + p];
               lm[u] = st[(2 * t + 1) * ldk + p];
@@ -978,7 +1026,7 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int p = pb + u * PSTEP;
-          if (p < S) {
+          if (p < p_end) {
             const double phi = make_phi<false>(__dsub_rn(ps[u], lm[u]), sr[u], xc);
             const double pn = qv[u] + kt[t * ldk + p];
             const double d = __dsub_rn(phi, pn);
@@ -1032,11 +1080,11 @@ __device__ __forceinline__ void run_chunk(const DevProblem& P, int k, int nt, co
                                           const double* lam, double* psi_n, double* lam_n,
                                           const double* s_src, const int* irow_tab, double* smem,
                                           int& cur, double& pri_m, double& dual_m,
-                                          const double* st = nullptr) {
+                                          const double* st = nullptr, const KSplit& ks = KSplit()) {
   if (stage_operator(P, k, smem, cur))
-    fast_chunk<TC, S_GLOBAL, true>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st);
+    fast_chunk<TC, S_GLOBAL, true>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st, ks);
   else
-    fast_chunk<TC, S_GLOBAL, false>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st);
+    fast_chunk<TC, S_GLOBAL, false>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st, ks);
 }
 
 // Patch-kernel chunk of <= 2 columns on the register-blocked GEMV pair
@@ -1295,7 +1343,7 @@ __device__ __forceinline__ bool patch_stop_test(const DevProblem& P, const RunAr
 
 template <int TC, bool RB>
 __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int it, double* smem,
-                                int& cur, const RunArgs& R, unsigned bar_target) {
+                                int& cur, const RunArgs& R, unsigned bar_target, int& pair_cnt) {
   double* s_patch = smem + P.off_patch;
   long long* m_pos = reinterpret_cast<long long*>(smem + P.off_meta);
   double* m_x = smem + P.off_meta + 3 * TC;
@@ -1420,8 +1468,15 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
         rb_chunk<TC>(P, k, nt, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, smem, cur, pri_m, dual_m,
                      stash + sb * stash_stride);
       else
+      {
+        KSplit ks;
+        if (P.cta_pair) {
+          const int pv = P.cta_pair[blockIdx.x];
+          if (pv >= 0) { ks.partner = pv >> 1; ks.half = pv & 1; ks.cnt = &pair_cnt; }
+        }
         run_chunk<TC, false>(P, k, nt, psi, lam, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, nullptr, smem, cur,
-                             pri_m, dual_m, P.stash_bufs > 0 ? stash + sb * stash_stride : nullptr);
+                             pri_m, dual_m, P.stash_bufs > 0 ? stash + sb * stash_stride : nullptr, ks);
+      }
       if (P.stash_bufs == 1 && ch + 1 < ch_b)   // single buffer: refill after the chunk is done
         stash_issue(P, P.chunk_col0[ch + 1], P.chunk_n[ch + 1], P.class_s[P.chunk_class[ch + 1]], psi, lam, stash);
     }
@@ -2123,6 +2178,7 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
   // previous launch has ended, and no CTA arrives before the first grid.sync)
   const unsigned bar_base = (PATCH && tid == 0) ? ld_acquire_u32(P.gbar) : 0u;
   unsigned bar_epoch = 0;
+  int pair_cnt = 0;   // K-split pairs: partial-Y publications of this CTA in this launch
   for (int step = 0; step < R.t_sim; ++step) {
     PT_DECL
     PT_START
@@ -2160,7 +2216,7 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
           break;
         }
         bar_epoch += gridDim.x;
-        if (patch_iteration<TC, MODE == kPatchRb>(P, b, x, it, smem, cur, R, bar_base + bar_epoch)) {
+        if (patch_iteration<TC, MODE == kPatchRb>(P, b, x, it, smem, cur, R, bar_base + bar_epoch, pair_cnt)) {
           bar_epoch -= gridDim.x;   // returned before arriving
           conv = true;
           break;
