@@ -293,7 +293,10 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           const bool stream_likely = (long long)P.n_cols >= 2LL * tc * G ||
                                      (getenv("DLMPC_FORCE_STREAM") && getenv("DLMPC_FORCE_STREAM")[0] == '1');
           const char* np = getenv("DLMPC_NO_PAIRS");
-          const bool l2_fed = opr_need * 8 > 3 * limit * 8 / 4;   // the operator region will not hold the basis
+          // bases of >= 1.5 MB (far beyond the operator region): measured on the
+          // C4 cells at N=1000 (tools/c4_pairs_ab.py) d=6,T=30 238.6 -> 196.1
+          // us/iter, d=4,T=30 84.8 -> 82.9; neutral to +1% below that size
+          const bool l2_fed = opr_need * 8 > 1536LL * 1024;
           if (!stream_likely && l2_fed && !(np && np[0] == '1')) {
             std::vector<int> cand;
             for (int r = 0; r < nr; ++r)
