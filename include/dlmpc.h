@@ -136,6 +136,10 @@ typedef struct dlmpc_problem {
   const int64_t* class_perm_off; /* [n_classes+1] */
   const int32_t* perm_pool;
   const int32_t* col_pin;        /* [n_cols] row of rhs0 = 1 among the touched rows, -1 if none */
+  /* CTAs of the persistent kernel (0: one per SM). The one-GPU test of the
+   * device-side exchange runs the ranks of a partitioned solve as slices of
+   * one cooperative grid (dlmpc_multi_solve), so each rank plans for its slice. */
+  int32_t grid_ctas;
 } dlmpc_problem;
 
 typedef struct dlmpc_handle dlmpc_handle;
@@ -342,6 +346,45 @@ int dlmpc_op_row_dots(int device, int n, int d, const int32_t* len, const double
 int dlmpc_op_plant_step(int device, int n_x, int n_u, const int64_t* a_ptr, const int32_t* a_idx,
                         const double* a_val, const int64_t* b_ptr, const int32_t* b_idx, const double* b_val,
                         const double* x, const double* u, double* out);
+
+/* ------------------------------------------------------------------------
+ * Graph-partitioned solve with the exchange ON THE DEVICE (replaces the
+ * host-driven per-iteration pack / send-recv / unpack / all-reduce of
+ * dlmpc_iterate_async + dlmpc_halo_*; reference: there is no exchange on one
+ * host, admm.py:186-253 and strategies.py:178-183). Each rank's persistent
+ * kernel stores the halo cells its neighbours read straight into their ψ/λ
+ * buffers (peer pointers: NVLink P2P via the IPC helpers below, or the same
+ * device), bumps their arrival counters, posts its residual maxima into
+ * every rank's slot table and waits for its neighbours -- one launch per
+ * solve, no host involvement per iteration, the same global stop decision on
+ * every rank. Non-patch kernel modes (stream, two-phase, exact).
+ * ---------------------------------------------------------------------- */
+/* Allocate the exchange state of a handle for `world` ranks and return the
+ * device pointers a neighbour needs: out[0..6] = ψ buffer 0, ψ buffer 1,
+ * λ buffer 0, λ buffer 1, halo arrival counter, residual slot table,
+ * residual arrival counter. */
+int dlmpc_dist_alloc(dlmpc_handle* h, int world, void** out7);
+/* Wire the exchange: this rank's send list (local cells, destination cells,
+ * destination peer index per entry), per peer its ψ/λ buffers (2 each) and
+ * arrival counter, per rank its slot table and residual counter, and how
+ * many counter increments per iteration this rank receives (the CTAs of all
+ * its sending neighbours). Pointers are device addresses (peer or local). */
+int dlmpc_dist_setup(dlmpc_handle* h, int rank, int world, int n_peers, int64_t n_send,
+                     const int64_t* send_src, const int64_t* send_dst, const int32_t* send_peer,
+                     void* const* peer_psi, void* const* peer_lam, void* const* peer_flag,
+                     uint32_t halo_per_iter, void* const* all_slots, void* const* all_rflag);
+/* One partitioned solve (every rank calls it; ranks on different GPUs run
+ * concurrently). Same results as dlmpc_solve: iterations, global history. */
+int dlmpc_dist_solve(dlmpc_handle* h, int max_iters, double eps_pri, double eps_dual, int* iters, double* hist);
+/* The one-GPU test: the n ranks' handles (same device, same kernel mode)
+ * as slices of ONE cooperative launch; iters / hist as dlmpc_dist_solve. */
+int dlmpc_multi_solve(dlmpc_handle* const* hs, int n, int max_iters, double eps_pri, double eps_dual,
+                      int* iters, double* hist);
+/* CUDA IPC of device allocations for the multi-process exchange (64-byte
+ * handles). */
+int dlmpc_ipc_get(const void* dev_ptr, void* handle64);
+int dlmpc_ipc_open(const void* handle64, int device, void** dev_ptr);
+int dlmpc_ipc_close(void* dev_ptr);
 
 /* Measured FP64 tensor-core (DMMA m8n8k4) peak of `device` in TFLOP/s: the
  * denominator of bench.py's FP64 roofline fraction (no reference counterpart;

@@ -43,6 +43,8 @@ struct dlmpc_handle {
   char* h_stage = nullptr; size_t stage_cap = 0;   // pinned staging of dlmpc_simulate's host copies
   cudaStream_t own_stream = nullptr;   // the handle's stream; `stream` may be an external one (dlmpc_set_stream)
   int cur_b = 0, b_valid = 1;          // current ψ/λ buffer as known on the host (ctl[4])
+  int dist_world = 0;                  // > 0 once dlmpc_dist_alloc ran
+  unsigned dist_epoch = 0;             // iterations of the earlier dist launches (counter base)
 };
 
 namespace {
@@ -82,6 +84,15 @@ int alloc(dlmpc_handle* h, size_t n, T** dst) {
 }
 
 using KernelFn = void (*)(DevProblem, RunArgs);
+
+using MultiFn = void (*)(const DevProblem*, const RunArgs*, const int*, int);
+
+MultiFn pick_multi_kernel(int mode, int tc) {
+  if (mode == kExact) return dlmpc_multi_kernel<8, kExact>;
+  if (mode == kStream) return tc == 16 ? dlmpc_multi_kernel<16, kStream> : dlmpc_multi_kernel<8, kStream>;
+  if (mode == kTwoPhase) return tc == 16 ? dlmpc_multi_kernel<16, kTwoPhase> : dlmpc_multi_kernel<8, kTwoPhase>;
+  return nullptr;   // patch modes: the overlapped stop test reads the local maxima
+}
 
 KernelFn pick_kernel(int mode, int tc, int rb = 0) {
   if (mode == kExact) return dlmpc_persistent<8, kExact>;
@@ -215,7 +226,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
   int optin = 0;
   CUDA_OR_FAIL(h, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
   const long long limit = (optin - 1024) / 8;   // doubles
-  const int G = h->sm_count;
+  const int G = pr->grid_ctas > 0 ? std::min(pr->grid_ctas, h->sm_count) : h->sm_count;
   h->grid = G;
   {
     const char* e = getenv("DLMPC_G1_MROW");
@@ -1283,6 +1294,194 @@ int dlmpc_phase_times(dlmpc_handle* h, uint64_t* out, int reset) {
   CUDA_OR_FAIL(h, cudaMemcpy(out, h->P.phase_ns, sizeof(uint64_t) * 16 * h->grid, cudaMemcpyDeviceToHost));
   if (reset) CUDA_OR_FAIL(h, cudaMemset(h->P.phase_ns, 0, sizeof(uint64_t) * 16 * h->grid));
   return DLMPC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Graph-partitioned solve with the exchange on the device (include/dlmpc.h)
+// ---------------------------------------------------------------------------
+int dlmpc_dist_alloc(dlmpc_handle* h, int world, void** out7) {
+  if (!h || !out7 || world < 1) return fail(h, DLMPC_BAD_ARGUMENT, "bad argument");
+  if (h->mode == kPatch || h->mode == kPatchRb)
+    return fail(h, DLMPC_BAD_ARGUMENT, "the device exchange needs a non-patch kernel mode (stream, two-phase, exact)");
+  cudaSetDevice(h->device);
+  DevProblem& P = h->P;
+  if (h->dist_world != world) {
+    int rc;
+    unsigned* flag; unsigned* rflag; unsigned long long* slots; int* abort_;
+    if ((rc = alloc(h, 1, &flag)) || (rc = alloc(h, 1, &rflag)) || (rc = alloc(h, (size_t)4 * world, &slots)) ||
+        (rc = alloc(h, 1, &abort_)))
+      return rc;
+    P.d_flag = flag; P.d_rflag = rflag; P.d_slots = slots; P.d_abort = abort_;
+    h->dist_world = world;
+    h->dist_epoch = 0;
+  }
+  out7[0] = P.psi[0]; out7[1] = P.psi[1]; out7[2] = P.lam[0]; out7[3] = P.lam[1];
+  out7[4] = P.d_flag; out7[5] = P.d_slots; out7[6] = P.d_rflag;
+  return DLMPC_OK;
+}
+
+int dlmpc_dist_setup(dlmpc_handle* h, int rank, int world, int n_peers, int64_t n_send,
+                     const int64_t* send_src, const int64_t* send_dst, const int32_t* send_peer,
+                     void* const* peer_psi, void* const* peer_lam, void* const* peer_flag,
+                     uint32_t halo_per_iter, void* const* all_slots, void* const* all_rflag) {
+  if (!h || world != h->dist_world || rank < 0 || rank >= world || n_peers < 0 || n_send < 0 ||
+      (n_send > 0 && (!send_src || !send_dst || !send_peer)) || (n_peers > 0 && (!peer_psi || !peer_lam || !peer_flag)) ||
+      !all_slots || !all_rflag)
+    return fail(h, DLMPC_BAD_ARGUMENT, "bad argument (call dlmpc_dist_alloc first)");
+  for (int64_t i = 0; i < n_send; ++i)
+    if (send_peer[i] < 0 || send_peer[i] >= n_peers || send_src[i] < 0 ||
+        send_src[i] >= (int64_t)h->P.n_cols * h->P.s_pad || send_dst[i] < 0)
+      return fail(h, DLMPC_BAD_ARGUMENT, "send list entry out of range");
+  cudaSetDevice(h->device);
+  DevProblem& P = h->P;
+  int rc;
+  std::vector<double*> pp(2 * (size_t)std::max(1, n_peers)), pl(2 * (size_t)std::max(1, n_peers));
+  std::vector<unsigned*> pf(std::max(1, n_peers));
+  for (int q = 0; q < n_peers; ++q) {
+    for (int k = 0; k < 2; ++k) {
+      pp[2 * q + k] = static_cast<double*>(peer_psi[2 * q + k]);
+      pl[2 * q + k] = static_cast<double*>(peer_lam[2 * q + k]);
+    }
+    pf[q] = static_cast<unsigned*>(peer_flag[q]);
+  }
+  std::vector<unsigned long long*> as(world);
+  std::vector<unsigned*> ar(world);
+  for (int r = 0; r < world; ++r) {
+    as[r] = static_cast<unsigned long long*>(all_slots[r]);
+    ar[r] = static_cast<unsigned*>(all_rflag[r]);
+  }
+  const long long* src64 = reinterpret_cast<const long long*>(send_src);
+  const long long* dst64 = reinterpret_cast<const long long*>(send_dst);
+  const long long* dsrc; const long long* ddst; const int* dpeer;
+  double* const* dpp; double* const* dpl; unsigned* const* dpf;
+  unsigned long long* const* das; unsigned* const* dar;
+  if ((rc = upload(h, src64, (size_t)n_send, &dsrc)) || (rc = upload(h, dst64, (size_t)n_send, &ddst)) ||
+      (rc = upload(h, send_peer, (size_t)n_send, &dpeer)) ||
+      (rc = upload(h, pp.data(), pp.size(), &dpp)) || (rc = upload(h, pl.data(), pl.size(), &dpl)) ||
+      (rc = upload(h, pf.data(), pf.size(), &dpf)) ||
+      (rc = upload(h, as.data(), as.size(), &das)) || (rc = upload(h, ar.data(), ar.size(), &dar)))
+    return rc;
+  P.d_send_src = dsrc; P.d_send_dst = ddst; P.d_send_peer = dpeer;
+  P.d_peer_psi = dpp; P.d_peer_lam = dpl; P.d_peer_flag = dpf;
+  P.d_all_slots = das; P.d_all_rflag = dar;
+  P.d_rank = rank; P.d_world = world; P.d_npeer = n_peers; P.d_nsend = n_send;
+  P.d_halo_per_iter = halo_per_iter;
+  P.dist = 1;
+  return DLMPC_OK;
+}
+
+namespace {
+RunArgs solve_args(dlmpc_handle* h, int max_iters, double eps_pri, double eps_dual) {
+  RunArgs R{};
+  R.t_sim = 1; R.closed_loop = 0; R.warm_start = 1; R.cold_start = 0;
+  R.max_iters = max_iters; R.stop_on_conv = 1; R.eps_pri = eps_pri; R.eps_dual = eps_dual;
+  R.hist = h->d_hist; R.step_iters = h->d_step_iters; R.states = h->d_states; R.inputs = h->d_inputs;
+  R.it_base = h->it_cont;
+  R.dist_epoch = h->dist_epoch;
+  return R;
+}
+
+// after a dist launch: status, iterations, history; the counters' base moves on
+int finish_dist(dlmpc_handle* h, int* iters, double* hist) {
+  int ctl[8];
+  if (int rc = read_ctl(h, ctl)) return rc;
+  int n = 0;
+  CUDA_OR_FAIL(h, cudaMemcpy(&n, h->d_step_iters, sizeof(int), cudaMemcpyDeviceToHost));
+  if (ctl[0] != 0) n = ctl[5];
+  if (ctl[0] == 4) return fail(h, DLMPC_CUDA_ERROR, "device exchange timed out (a neighbour rank did not arrive)");
+  h->dist_epoch += (unsigned)n;
+  h->it_cont += n;
+  if (iters) *iters = n;
+  if (hist && n > 0) CUDA_OR_FAIL(h, cudaMemcpy(hist, h->d_hist, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost));
+  return ctl[0];
+}
+}  // namespace
+
+int dlmpc_dist_solve(dlmpc_handle* h, int max_iters, double eps_pri, double eps_dual, int* iters, double* hist) {
+  if (!h || max_iters < 1) return fail(h, DLMPC_BAD_ARGUMENT, "bad argument");
+  if (!h->P.dist) return fail(h, DLMPC_BAD_ARGUMENT, "dlmpc_dist_setup first");
+  cudaSetDevice(h->device);
+  if (int rc = ensure_run_buffers(h, max_iters, 1)) return rc;
+  RunArgs R = solve_args(h, max_iters, eps_pri, eps_dual);
+  if (int rc = launch(h, R)) return rc;
+  if (int rc = finish_timing(h)) return rc;
+  CUDA_OR_FAIL(h, cudaGetLastError());
+  return finish_dist(h, iters, hist);
+}
+
+int dlmpc_multi_solve(dlmpc_handle* const* hs, int n, int max_iters, double eps_pri, double eps_dual,
+                      int* iters, double* hist) {
+  if (!hs || n < 1 || max_iters < 1) return fail(nullptr, DLMPC_BAD_ARGUMENT, "bad argument");
+  dlmpc_handle* h0 = hs[0];
+  for (int r = 0; r < n; ++r) {
+    if (!hs[r] || hs[r]->device != h0->device || hs[r]->mode != h0->mode || hs[r]->P.tile_cols != h0->P.tile_cols)
+      return fail(h0, DLMPC_BAD_ARGUMENT, "the ranks must share device, kernel mode and tile width");
+    if (!hs[r]->P.dist) return fail(h0, DLMPC_BAD_ARGUMENT, "dlmpc_dist_setup first on every rank");
+  }
+  MultiFn fn = pick_multi_kernel(h0->mode, h0->P.tile_cols);
+  if (!fn) return fail(h0, DLMPC_BAD_ARGUMENT, "no multi-rank kernel for this mode");
+  cudaSetDevice(h0->device);
+  std::vector<DevProblem> probs(n);
+  std::vector<RunArgs> runs(n);
+  std::vector<int> base(n + 1, 0);
+  int smem = 0;
+  for (int r = 0; r < n; ++r) {
+    dlmpc_handle* h = hs[r];
+    if (int rc = ensure_run_buffers(h, max_iters, 1)) return rc;
+    CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
+    probs[r] = h->P;
+    runs[r] = solve_args(h, max_iters, eps_pri, eps_dual);
+    base[r + 1] = base[r] + h->grid;
+    smem = std::max(smem, h->smem_bytes);
+  }
+  DevProblem* dprobs = nullptr; RunArgs* druns = nullptr; int* dbase = nullptr;
+  CUDA_OR_FAIL(h0, cudaMalloc(&dprobs, sizeof(DevProblem) * n));
+  CUDA_OR_FAIL(h0, cudaMalloc(&druns, sizeof(RunArgs) * n));
+  CUDA_OR_FAIL(h0, cudaMalloc(&dbase, sizeof(int) * (n + 1)));
+  cudaMemcpy(dprobs, probs.data(), sizeof(DevProblem) * n, cudaMemcpyHostToDevice);
+  cudaMemcpy(druns, runs.data(), sizeof(RunArgs) * n, cudaMemcpyHostToDevice);
+  cudaMemcpy(dbase, base.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice);
+  cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int nn = n;
+  void* args[] = {&dprobs, &druns, &dbase, &nn};
+  if (e == cudaSuccess)
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(base[n]), dim3(kThreads), args,
+                                    static_cast<size_t>(smem), h0->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h0->stream);
+  cudaFree(dprobs); cudaFree(druns); cudaFree(dbase);
+  if (e != cudaSuccess) return fail(h0, DLMPC_CUDA_ERROR, std::string("multi-rank launch: ") + cudaGetErrorString(e));
+  int status = DLMPC_OK;
+  for (int r = 0; r < n; ++r) {
+    hs[r]->b_valid = 0;
+    const int rc = finish_dist(hs[r], r == 0 ? iters : nullptr, r == 0 ? hist : nullptr);
+    if (rc != DLMPC_OK && status == DLMPC_OK) status = rc;
+  }
+  return status;
+}
+
+int dlmpc_ipc_get(const void* dev_ptr, void* handle64) {
+  if (!dev_ptr || !handle64) return fail(nullptr, DLMPC_BAD_ARGUMENT, "null argument");
+  cudaIpcMemHandle_t hd;
+  const cudaError_t e = cudaIpcGetMemHandle(&hd, const_cast<void*>(dev_ptr));
+  if (e != cudaSuccess) return fail(nullptr, DLMPC_CUDA_ERROR, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  std::memcpy(handle64, &hd, sizeof(hd));
+  return DLMPC_OK;
+}
+
+int dlmpc_ipc_open(const void* handle64, int device, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return fail(nullptr, DLMPC_BAD_ARGUMENT, "null argument");
+  cudaSetDevice(device);
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle64, sizeof(hd));
+  const cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(nullptr, DLMPC_CUDA_ERROR, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+  return DLMPC_OK;
+}
+
+int dlmpc_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return DLMPC_OK;
+  const cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  return e == cudaSuccess ? DLMPC_OK : fail(nullptr, DLMPC_CUDA_ERROR, cudaGetErrorString(e));
 }
 
 // FP64 tensor-core peak of this GPU, measured live (the roofline denominator

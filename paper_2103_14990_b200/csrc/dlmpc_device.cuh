@@ -53,12 +53,25 @@ __device__ __forceinline__ unsigned long long gtimer() {   // SM cycles (globalt
 }
 #define PT_DECL unsigned long long pt_t0 = 0;
 #define PT_START if (threadIdx.x == 0) pt_t0 = gtimer();
-#define PT_LAP(P, ph) if (threadIdx.x == 0) { unsigned long long t1_ = gtimer(); (P).phase_ns[blockIdx.x * 16 + (ph)] += t1_ - pt_t0; pt_t0 = t1_; }
+#define PT_LAP(P, ph) if (threadIdx.x == 0) { unsigned long long t1_ = gtimer(); (P).phase_ns[VBID * 16 + (ph)] += t1_ - pt_t0; pt_t0 = t1_; }
 #else
 #define PT_DECL
 #define PT_START
 #define PT_LAP(P, ph)
 #endif
+
+// Virtual CTA index / count of the persistent kernel: blockIdx.x / gridDim.x,
+// except in the multi-rank test launch (dlmpc_multi_kernel: the ranks of a
+// graph-partitioned solve as contiguous CTA slices of ONE cooperative grid on
+// one GPU, so the device-side exchange is tested without separate launches
+// that wait on one another). Set by every kernel entry (vcta_init).
+__shared__ int dlmpc_vcta[2];   // [0] first CTA of this rank's slice, [1] its CTA count
+#define VBID (static_cast<int>(blockIdx.x) - dlmpc_vcta[0])
+#define VGRID (dlmpc_vcta[1])
+__device__ __forceinline__ void vcta_init(int base, int count) {
+  if (threadIdx.x == 0) { dlmpc_vcta[0] = base; dlmpc_vcta[1] = count; }
+  __syncthreads();
+}
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
@@ -148,6 +161,24 @@ struct DevProblem {
   const int* cta_pair;
   unsigned* pair_flag;         // [grid] partial-Y publications (monotonic per launch)
   double* ypair;               // [grid][2][n08_max * TC] partial Y, double-buffered
+  // graph-partitioned solve with the exchange on the device (P.dist, non-patch
+  // modes): see dist_exchange. Peer pointers address the neighbour ranks'
+  // device memory (NVLink P2P; the same device in the one-launch test).
+  int dist, d_rank, d_world, d_npeer;
+  long long d_nsend;
+  const long long* d_send_src;       // [d_nsend] this rank's cells (internal layout)
+  const long long* d_send_dst;       // [d_nsend] the destination rank's cells
+  const int* d_send_peer;            // [d_nsend] destination (index into the peer tables)
+  double* const* d_peer_psi;         // [d_npeer * 2] destination ψ buffers
+  double* const* d_peer_lam;         // [d_npeer * 2] destination λ buffers
+  unsigned* const* d_peer_flag;      // [d_npeer] their halo arrival counters
+  unsigned* d_flag;                  // own halo arrival counter (monotonic, never reset)
+  unsigned d_halo_per_iter;          // its increments per iteration (CTAs of all sending peers)
+  unsigned long long* const* d_all_slots;   // [d_world] every rank's residual slots [2][world][2]
+  unsigned* const* d_all_rflag;      // [d_world] every rank's residual arrival counter
+  unsigned* d_rflag;                 // own residual arrival counter
+  unsigned long long* d_slots;       // own residual slots
+  int* d_abort;                      // set on an exchange timeout (all CTAs then stop)
   long long part_cap;          // stream mode: doubles per Φ-partials buffer
   long long smem_doubles;      // dynamic shared memory of the plan
 };
@@ -156,6 +187,7 @@ struct RunArgs {
   int t_sim, closed_loop, warm_start, cold_start, max_iters, stop_on_conv;
   int it_base;         // iterations already run on this state (host-driven iterate calls): the
                        // stream kernel continues its Φ-dot partials instead of a full Φ
+  unsigned dist_epoch;  // P.dist: iterations of the earlier launches (the counters' base)
   double eps_pri, eps_dual;
   double* hist;        // [2*max_iters] history of the current / failing step
   int* step_iters;     // [t_sim]
@@ -381,9 +413,9 @@ __device__ __forceinline__ void publish_barrier(const DevProblem& P, int it, dou
 // the reference's sequential order (warp_ordered_sum). Item q goes to CTA
 // q % grid first, so the items spread over the SMs.
 __device__ __forceinline__ long long wspread_first() {
-  return static_cast<long long>(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  return static_cast<long long>(threadIdx.x >> 5) * VGRID + VBID;
 }
-__device__ __forceinline__ long long wspread_step() { return static_cast<long long>(gridDim.x) * (blockDim.x >> 5); }
+__device__ __forceinline__ long long wspread_step() { return static_cast<long long>(VGRID) * (blockDim.x >> 5); }
 
 // acc (+)= v_0 + v_1 + ... + v_{n-1} over lanes 0..n-1, strictly in that
 // order with IEEE adds; `first`: acc is not yet set (the reference starts
@@ -496,7 +528,7 @@ __device__ __forceinline__ void phi_rows_of(const DevProblem& P, int i, const do
 // Grid-wide Φ stage of the two-phase kernels: s_r -> global s_row.
 template <bool EXACT>
 __device__ void phi_stage_global(const DevProblem& P, int b, const double* x) {
-  const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5), GW = gridDim.x * kWarps;
+  const int gw = VBID * kWarps + (threadIdx.x >> 5), GW = VGRID * kWarps;
   for (int i = gw; i < P.n_sub; i += GW) {
     double* dst = P.s_row + P.row_start[i];
     phi_rows_of<EXACT>(P, i, P.psi[b], P.lam[b], x, [dst](int l, double s) { dst[l] = s; });
@@ -898,7 +930,7 @@ __device__ __forceinline__ void ksplit_exchange_y(const DevProblem& P, const KSp
   const int tid = threadIdx.x;
   const int slot = *ks.cnt & 1;
   const size_t per = static_cast<size_t>(P.n08_max) * TCc;
-  double* mine = P.ypair + (static_cast<size_t>(blockIdx.x) * 2 + slot) * per;
+  double* mine = P.ypair + (static_cast<size_t>(VBID) * 2 + slot) * per;
   const double* theirs = P.ypair + (static_cast<size_t>(ks.partner) * 2 + slot) * per;
   for (int idx = tid; idx < n08 * TCc; idx += kThreads) {
     const int a = idx / TCc, t = idx - a * TCc;
@@ -908,7 +940,7 @@ __device__ __forceinline__ void ksplit_exchange_y(const DevProblem& P, const KSp
   *ks.cnt += 1;
   if (tid == 0) {
     __threadfence();
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" :: "l"(P.pair_flag + blockIdx.x) : "memory");
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" :: "l"(P.pair_flag + VBID) : "memory");
     while (static_cast<int>(ld_acquire_u32(P.pair_flag + ks.partner) - static_cast<unsigned>(*ks.cnt)) < 0) {}
   }
   __syncthreads();
@@ -1167,7 +1199,7 @@ __device__ void column_stage_tiles(const DevProblem& P, int b, const double* x, 
   long long* m_pos = reinterpret_cast<long long*>(smem + P.off_meta);
   double* m_x = smem + P.off_meta + 3 * TC;
   double pri_m = 0.0, dual_m = 0.0;
-  for (int tile = blockIdx.x; tile < P.n_tiles; tile += gridDim.x) {
+  for (int tile = VBID; tile < P.n_tiles; tile += VGRID) {
     const int k = P.tile_class[tile], first = P.tile_first[tile], nt = P.tile_count[tile];
     if (threadIdx.x < TC) {
       const int t = threadIdx.x;
@@ -1209,8 +1241,8 @@ __device__ void column_stage_tiles(const DevProblem& P, int b, const double* x, 
 // (x of the supports and of the chunk's columns, 1/||a||², 1/(ρ + 2w·||a||²)).
 template <int TC>
 __device__ void cache_phi_meta(const DevProblem& P, const double* x, double* smem, bool full) {
-  const int un0 = P.cta_unit_ptr[blockIdx.x];
-  if (un0 == P.cta_unit_ptr[blockIdx.x + 1]) return;
+  const int un0 = P.cta_unit_ptr[VBID];
+  if (un0 == P.cta_unit_ptr[VBID + 1]) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int plo = P.unit_patch_lo[un0], phi_ = P.unit_patch_hi[un0];
   const int np = phi_ - plo;
@@ -1337,7 +1369,7 @@ __device__ __forceinline__ bool patch_stop_test(const DevProblem& P, const RunAr
                                                 unsigned long long rp, unsigned long long rd) {
   const double pri = __longlong_as_double(static_cast<long long>(rp));
   const double dual = P.rho * __longlong_as_double(static_cast<long long>(rd));
-  if (blockIdx.x == 0 && threadIdx.x == 0) { R.hist[2 * (it - 1)] = pri; R.hist[2 * (it - 1) + 1] = dual; }
+  if (VBID == 0 && threadIdx.x == 0) { R.hist[2 * (it - 1)] = pri; R.hist[2 * (it - 1) + 1] = dual; }
   return R.stop_on_conv && pri <= R.eps_pri && dual <= R.eps_dual;
 }
 
@@ -1359,15 +1391,15 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
   unsigned long long* rbc = reinterpret_cast<unsigned long long*>(smem + P.off_red);
   if (!tested && threadIdx.x == 0) { rp = __ldcg(P.resid + 2 * (it - 1)); rd = __ldcg(P.resid + 2 * (it - 1) + 1); }
   PT_DECL
-  const int un_a = P.cta_unit_ptr[blockIdx.x];
-  if (un_a == P.cta_unit_ptr[blockIdx.x + 1] && !tested) {
+  const int un_a = P.cta_unit_ptr[VBID];
+  if (un_a == P.cta_unit_ptr[VBID + 1] && !tested) {
     if (threadIdx.x == 0) { rbc[0] = rp; rbc[1] = rd; }
     __syncthreads();
     rp = rbc[0]; rd = rbc[1];
     __syncthreads();   // every warp has read the slots before the publish reuses them
     if (patch_stop_test(P, R, it, rp, rd)) return true;
   }
-  for (int un = un_a; un < P.cta_unit_ptr[blockIdx.x + 1]; ++un) {
+  for (int un = un_a; un < P.cta_unit_ptr[VBID + 1]; ++un) {
     PT_START
     int own_lo, own_hi, plo, phi_, prows, ch_a, ch_b, k0 = 0, c00 = 0, nt0 = 0, S0 = 0, o_off, o_n;
     long long prow0;
@@ -1471,7 +1503,7 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
       {
         KSplit ks;
         if (P.cta_pair) {
-          const int pv = P.cta_pair[blockIdx.x];
+          const int pv = P.cta_pair[VBID];
           if (pv >= 0) { ks.partner = pv >> 1; ks.half = pv & 1; ks.cnt = &pair_cnt; }
         }
         run_chunk<TC, false>(P, k, nt, psi, lam, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, nullptr, smem, cur,
@@ -1666,7 +1698,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
   // unit descriptors, double-buffered in shared memory: the next unit's is
   // fetched (cp.async) while the current unit runs
   int* udesc = reinterpret_cast<int*>(smem + P.off_udesc);   // [2][16]
-  const int un_a = P.cta_unit_ptr[blockIdx.x], un_b = P.cta_unit_ptr[blockIdx.x + 1];
+  const int un_a = P.cta_unit_ptr[VBID], un_b = P.cta_unit_ptr[VBID + 1];
   if (un_a < un_b && tid < 4)
     reinterpret_cast<int4*>(udesc)[tid] = __ldg(reinterpret_cast<const int4*>(P.unit_desc) + 4 * un_a + tid);
   __syncthreads();
@@ -1920,8 +1952,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
           pri_m = epi.pri_m; dual_m = epi.dual_m;
 #ifdef DLMPC_PHASE_TIMING
           if (tid == 0) {
-            P.phase_ns[blockIdx.x * 16 + 9] += epi.t_kloop - pt_t0;
-            P.phase_ns[blockIdx.x * 16 + 10] += epi.t_lam - epi.t_kloop;
+            P.phase_ns[VBID * 16 + 9] += epi.t_kloop - pt_t0;
+            P.phase_ns[VBID * 16 + 10] += epi.t_lam - epi.t_kloop;
             pt_t0 = epi.t_lam;
           }
 #endif
@@ -2026,7 +2058,7 @@ __device__ void column_stage_exact(const DevProblem& P, int b, const double* x, 
   double* psi_n = P.psi[b ^ 1];
   double* lam_n = P.lam[b ^ 1];
   double pri_m = 0.0, dual_m = 0.0;
-  for (int c = P.own_col_lo + blockIdx.x; c < P.own_col_hi; c += gridDim.x) {
+  for (int c = P.own_col_lo + VBID; c < P.own_col_hi; c += VGRID) {
     const int owner = P.col_owner[c];
     const int k = P.col_class[c];
     const int S = P.class_s[k], m = P.class_m[k];
@@ -2153,19 +2185,123 @@ __device__ void control_plant_stage(const DevProblem& P, int pb, const double* x
 
 __device__ void zero_iterate(const DevProblem& P, int b) {
   const size_t n = static_cast<size_t>(P.n_cols) * P.s_pad;
-  const size_t gt = blockIdx.x * blockDim.x + threadIdx.x, GT = gridDim.x * blockDim.x;
+  const size_t gt = VBID * blockDim.x + threadIdx.x, GT = VGRID * blockDim.x;
   for (size_t q = gt; q < n; q += GT) { P.psi[b][q] = 0.0; P.lam[b][q] = 0.0; }
 }
 
 
+// ---------------------------------------------------------------------------
+// Device-side exchange of the graph-partitioned solve (P.dist).
+// Called by every CTA after the rank's grid barrier of iteration `it`, with
+// ψ', λ' of the owned columns in buffer b and the rank's residual maxima in
+// P.resid[2 it]:
+//  1. every CTA stores its share of the halo cells the neighbour ranks read
+//     straight into THEIR buffer b (peer memory), fences at system scope and
+//     bumps each neighbour's arrival counter;
+//  2. CTA 0 posts the rank's two maxima into every rank's slot table
+//     (parity (epoch + it) & 1) and bumps every rank's residual counter;
+//  3. thread 0 of every CTA waits (acquire, system scope) for all CTAs of
+//     all sending neighbours and for all ranks' maxima of this iteration;
+//     a ~4 s bound turns a protocol failure into an error instead of a hang;
+//  4. a grid barrier makes the outcome uniform; every CTA forms the global
+//     maxima from the slots -- the same bits on every rank, so every rank
+//     takes the same stop decision.
+// Buffer b of a rank is written by its neighbours only in halo cells it
+// never writes itself, and only after the rank has finished reading b
+// (ping-pong: iteration it+1 reads b, writes b^1; a neighbour's next push
+// into b follows this rank's next arrival). Replaces the host-driven pack /
+// NCCL send-recv / unpack / all-reduce per iteration (partition.py).
+// Returns false on an exchange failure (P.d_abort set).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned ld_acquire_sys_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <class Grid>
+__device__ bool dist_exchange(const DevProblem& P, const RunArgs& R, int it, int b, Grid& grid,
+                              unsigned long long* out2) {
+  const int tid = threadIdx.x;
+  const size_t gt = static_cast<size_t>(VBID) * blockDim.x + tid, GT = static_cast<size_t>(VGRID) * blockDim.x;
+  const unsigned k = R.dist_epoch + static_cast<unsigned>(it);   // global iteration index
+  const int par = k & 1;
+  const double* psi = P.psi[b];
+  const double* lam = P.lam[b];
+  for (size_t i = gt; i < static_cast<size_t>(P.d_nsend); i += GT) {
+    const int q = P.d_send_peer[i];
+    const long long src = P.d_send_src[i], dst = P.d_send_dst[i];
+    P.d_peer_psi[2 * q + b][dst] = psi[src];
+    P.d_peer_lam[2 * q + b][dst] = lam[src];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0)
+    for (int q = 0; q < P.d_npeer; ++q) atomicAdd_system(P.d_peer_flag[q], 1u);
+  if (VBID == 0 && tid == 0) {
+    const unsigned long long rp = __ldcg(P.resid + 2 * it), rd = __ldcg(P.resid + 2 * it + 1);
+    for (int r = 0; r < P.d_world; ++r) {
+      volatile unsigned long long* slot = P.d_all_slots[r] + (static_cast<size_t>(par) * P.d_world + P.d_rank) * 2;
+      slot[0] = rp;
+      slot[1] = rd;
+    }
+    __threadfence_system();
+    for (int r = 0; r < P.d_world; ++r) atomicAdd_system(P.d_all_rflag[r], 1u);
+  }
+  if (tid == 0) {
+    const unsigned want_h = (k + 1) * P.d_halo_per_iter, want_r = (k + 1) * static_cast<unsigned>(P.d_world);
+    const long long t0 = clock64();
+    while (static_cast<int>(ld_acquire_sys_u32(P.d_flag) - want_h) < 0 ||
+           static_cast<int>(ld_acquire_sys_u32(P.d_rflag) - want_r) < 0) {
+      if (*reinterpret_cast<volatile int*>(P.d_abort)) break;
+      if (clock64() - t0 > (8LL << 30)) { atomicExch(P.d_abort, 1); break; }
+    }
+  }
+  __syncthreads();
+  fence_proxy_async_global();   // the neighbours' stores are read by TMA bulk copies next
+  grid.sync();
+  if (*reinterpret_cast<volatile int*>(P.d_abort)) return false;
+  unsigned long long mp = 0ull, md = 0ull;
+  const volatile unsigned long long* own = P.d_slots + static_cast<size_t>(par) * P.d_world * 2;
+  for (int r = 0; r < P.d_world; ++r) {   // ordered bits of non-negative maxima: NaN wins
+    const unsigned long long a = own[2 * r] & 0x7fffffffffffffffull, c = own[2 * r + 1] & 0x7fffffffffffffffull;
+    mp = a > mp ? a : mp;
+    md = c > md ? c : md;
+  }
+  out2[0] = mp;
+  out2[1] = md;
+  return true;
+}
+
+template <int TC, int MODE>
+__device__ __forceinline__ void persistent_body(const DevProblem& P, const RunArgs& R);
+
 template <int TC, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, RunArgs R) {
+  vcta_init(0, gridDim.x);
+  persistent_body<TC, MODE>(P, R);
+}
+
+// The ranks of a graph-partitioned solve as contiguous CTA slices of ONE
+// cooperative grid on one GPU (cta_base[r] .. cta_base[r+1]), each running
+// its own sub-problem: the one-GPU test of the device-side exchange.
+template <int TC, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) dlmpc_multi_kernel(const DevProblem* probs, const RunArgs* runs,
+                                                                  const int* cta_base, int n_ranks) {
+  int r = 0;
+  while (r + 1 < n_ranks && static_cast<int>(blockIdx.x) >= cta_base[r + 1]) ++r;
+  vcta_init(cta_base[r], cta_base[r + 1] - cta_base[r]);
+  persistent_body<TC, MODE>(probs[r], runs[r]);
+}
+
+template <int TC, int MODE>
+__device__ __forceinline__ void persistent_body(const DevProblem& P, const RunArgs& R) {
   constexpr bool EXACT = MODE == kExact;
   constexpr bool PATCH = MODE == kPatch || MODE == kPatchRb;
   extern __shared__ __align__(16) double smem[];
   cg::grid_group grid = cg::this_grid();
   const int tid = threadIdx.x;
-  const bool leader = blockIdx.x == 0 && tid == 0;
+  const bool leader = VBID == 0 && tid == 0;
   int cur = -1;   // class whose operator is staged at smem offset 0
   int b = P.ctl[4];
   unsigned ph = 0u;   // stream mode: mbarrier phase bits (ψ0, ψ1, λ) -- a register, not an indexed array
@@ -2173,7 +2309,7 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
     if (tid < 3) mbar_init(reinterpret_cast<unsigned long long*>(smem + P.off_bar) + tid, 1);
     __syncthreads();
   }
-  const size_t gt = blockIdx.x * blockDim.x + tid, GT = gridDim.x * blockDim.x;
+  const size_t gt = VBID * blockDim.x + tid, GT = VGRID * blockDim.x;
   // patch modes: the iteration barrier's counter value at launch (stable: the
   // previous launch has ended, and no CTA arrives before the first grid.sync)
   const unsigned bar_base = (PATCH && tid == 0) ? ld_acquire_u32(P.gbar) : 0u;
@@ -2215,9 +2351,9 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
           }
           break;
         }
-        bar_epoch += gridDim.x;
+        bar_epoch += VGRID;
         if (patch_iteration<TC, MODE == kPatchRb>(P, b, x, it, smem, cur, R, bar_base + bar_epoch, pair_cnt)) {
-          bar_epoch -= gridDim.x;   // returned before arriving
+          bar_epoch -= VGRID;   // returned before arriving
           conv = true;
           break;
         }
@@ -2229,7 +2365,7 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
       PT_DECL
       if (MODE == kStream) {
         const int itg = it + (R.closed_loop ? 0 : R.it_base);
-        if (P.cta_gop && P.cta_gop[blockIdx.x]) stream_iteration<TC, false>(P, b, x, it, itg, smem, cur, ph);
+        if (P.cta_gop && P.cta_gop[VBID]) stream_iteration<TC, false>(P, b, x, it, itg, smem, cur, ph);
         else stream_iteration<TC, true>(P, b, x, it, itg, smem, cur, ph);
         fence_proxy_async_global();
         PT_START
@@ -2248,7 +2384,16 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
       b ^= 1;
       // one load of the residual words per CTA, broadcast through shared memory
       unsigned long long* rbc = reinterpret_cast<unsigned long long*>(smem + P.off_red);
-      if (tid == 0) { rbc[0] = __ldcg(P.resid + 2 * it); rbc[1] = __ldcg(P.resid + 2 * it + 1); }
+      if (P.dist) {   // the halo to the neighbour ranks, the global maxima from all ranks
+        unsigned long long g2[2];
+        if (!dist_exchange(P, R, it, b, grid, g2)) {
+          if (leader) { P.ctl[0] = 4; P.ctl[1] = step; P.ctl[5] = it; P.ctl[4] = b; }
+          return;
+        }
+        if (tid == 0) { rbc[0] = g2[0]; rbc[1] = g2[1]; }
+      } else if (tid == 0) {
+        rbc[0] = __ldcg(P.resid + 2 * it); rbc[1] = __ldcg(P.resid + 2 * it + 1);
+      }
       __syncthreads();
       const double pri = __longlong_as_double(static_cast<long long>(rbc[0]));
       const double dual = P.rho * __longlong_as_double(static_cast<long long>(rbc[1]));
@@ -2279,7 +2424,10 @@ __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, Ru
 }
 
 // Row data for the solve API (dlmpc_set_x): a plain launch.
-__global__ void set_x_kernel(DevProblem P) { row_data_stage(P, P.x[0], P.ctl + 2); }
+__global__ void set_x_kernel(DevProblem P) {
+  vcta_init(0, gridDim.x);
+  row_data_stage(P, P.x[0], P.ctl + 2);
+}
 
 // φ of the last iteration, internal column layout (for dlmpc_get(DLMPC_PHI)).
 template <bool EXACT>
@@ -2383,8 +2531,14 @@ __global__ void audit_dynamics_kernel(DevProblem P, int b, double* out) {
 // Control extraction and plant step for the loaded x after a host-driven
 // solve (graph-partitioned multi-GPU path): plain launches, grid-stride.
 template <bool EXACT>
-__global__ void control_kernel(DevProblem P, int pb) { control_stage<EXACT>(P, pb, P.x[0]); }
-__global__ void plant_kernel(DevProblem P) { plant_stage(P, P.x[0], P.x[1]); }
+__global__ void control_kernel(DevProblem P, int pb) {
+  vcta_init(0, gridDim.x);
+  control_stage<EXACT>(P, pb, P.x[0]);
+}
+__global__ void plant_kernel(DevProblem P) {
+  vcta_init(0, gridDim.x);
+  plant_stage(P, P.x[0], P.x[1]);
+}
 
 // Halo exchange of the partitioned path (partition.py halo_cells): gather
 // the (ψ, λ) entries a neighbour reads into one interleaved message, and

@@ -50,6 +50,7 @@ class _Problem(C.Structure):
         ("input_owner", _i32p), ("input_local", _i32p),
         ("class_ntouch", _i32p), ("class_g0_off", _i64p), ("g0_pool", _f64p),
         ("class_perm_off", _i64p), ("perm_pool", _i32p), ("col_pin", _i32p),
+        ("grid_ctas", C.c_int32),
     ]
 
 
@@ -65,7 +66,9 @@ EXPORTS = ("dlmpc_create", "dlmpc_destroy", "dlmpc_last_error", "dlmpc_global_er
            "dlmpc_sched_get", "dlmpc_sched_set_x", "dlmpc_sched_stage", "dlmpc_sched_sync",
            "dlmpc_sched_read_residuals", "dlmpc_sched_phi_compute", "dlmpc_sched_swap_rows",
            "dlmpc_op_phi_rows", "dlmpc_op_psi_cols", "dlmpc_op_lambda", "dlmpc_op_residuals",
-           "dlmpc_op_row_dots", "dlmpc_op_plant_step")
+           "dlmpc_op_row_dots", "dlmpc_op_plant_step",
+           "dlmpc_dist_alloc", "dlmpc_dist_setup", "dlmpc_dist_solve", "dlmpc_multi_solve",
+           "dlmpc_ipc_get", "dlmpc_ipc_open", "dlmpc_ipc_close")
 
 
 class _SchedProblem(C.Structure):
@@ -154,6 +157,14 @@ def load_library():
     lib.dlmpc_op_row_dots.argtypes = [C.c_int, C.c_int, C.c_int, _i32p, _f64p, _i64p, C.c_int64, _f64p, _f64p]
     lib.dlmpc_op_plant_step.argtypes = [C.c_int, C.c_int, C.c_int, _i64p, _i32p, _f64p, _i64p, _i32p, _f64p,
                                         _f64p, _f64p, _f64p]
+    lib.dlmpc_dist_alloc.argtypes = [vp, C.c_int, _P(vp)]
+    lib.dlmpc_dist_setup.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int64, _i64p, _i64p, _i32p,
+                                     _P(vp), _P(vp), _P(vp), C.c_uint32, _P(vp), _P(vp)]
+    lib.dlmpc_dist_solve.argtypes = [vp, C.c_int, C.c_double, C.c_double, _i32p, _f64p]
+    lib.dlmpc_multi_solve.argtypes = [_P(vp), C.c_int, C.c_int, C.c_double, C.c_double, _i32p, _f64p]
+    lib.dlmpc_ipc_get.argtypes = [vp, vp]
+    lib.dlmpc_ipc_open.argtypes = [vp, C.c_int, _P(vp)]
+    lib.dlmpc_ipc_close.argtypes = [vp]
     _lib = lib
     return lib
 
@@ -167,6 +178,41 @@ def fp64_peak_tflops(device: int = 0) -> float:
     return float(out.value)
 
 
+def multi_solve(sessions, max_iters, eps_pri, eps_dual):
+    """The one-GPU test of the device exchange: the ranks' sessions as slices
+    of ONE cooperative launch -> (iterations, history, converged)."""
+    lib = load_library()
+    hs = (C.c_void_p * len(sessions))(*[s._h for s in sessions])
+    hist = np.zeros(2 * max_iters)
+    n = C.c_int32(0)
+    rc = lib.dlmpc_multi_solve(hs, len(sessions), int(max_iters), float(eps_pri), float(eps_dual), C.byref(n),
+                               hist.ctypes.data_as(_f64p))
+    if rc not in (DLMPC_OK, DLMPC_NOT_CONVERGED):
+        raise DeviceError(f"dlmpc_multi_solve failed ({rc}): {lib.dlmpc_last_error(sessions[0]._h).decode()}")
+    k = int(n.value)
+    return k, hist[:2 * k].reshape(k, 2), rc == DLMPC_OK
+
+
+def ipc_handle(dev_ptr: int) -> bytes:
+    lib = load_library()
+    buf = C.create_string_buffer(64)
+    if lib.dlmpc_ipc_get(C.c_void_p(dev_ptr), buf) != 0:
+        raise DeviceError("dlmpc_ipc_get: " + lib.dlmpc_global_error().decode())
+    return buf.raw
+
+
+def ipc_open(handle: bytes, device: int) -> int:
+    lib = load_library()
+    out = C.c_void_p()
+    if lib.dlmpc_ipc_open(C.create_string_buffer(handle, 64), int(device), C.byref(out)) != 0:
+        raise DeviceError("dlmpc_ipc_open: " + lib.dlmpc_global_error().decode())
+    return int(out.value)
+
+
+def ipc_close(dev_ptr: int):
+    load_library().dlmpc_ipc_close(C.c_void_p(dev_ptr))
+
+
 def _ptr(a, ctype):
     if a is None:
         return None
@@ -176,7 +222,7 @@ def _ptr(a, ctype):
 class DeviceSession:
     """One uploaded problem (a `dlmpc_handle`) on one GPU."""
 
-    def __init__(self, layout, device: int = 0):
+    def __init__(self, layout, device: int = 0, grid_ctas: int = 0):
         lib = load_library()
         self.layout = L = layout
         self._keep = []
@@ -196,6 +242,7 @@ class DeviceSession:
         p.n_sub, p.n_rows, p.n_cols, p.n_inputs = L.n_sub, L.n_rows, L.n_cols, L.n_inputs
         p.s_pad, p.horizon, p.exact, p.contiguous = L.s_pad, L.horizon, int(L.exact), int(L.contiguous)
         p.rho = L.rho
+        p.grid_ctas = int(grid_ctas)
         p.own_sub_lo, p.own_sub_hi = L.own_sub
         p.own_col_lo, p.own_col_hi = L.own_cols
         p.row_start, p.ball_ptr = i64("row_start"), i64("ball_ptr")
@@ -340,6 +387,43 @@ class DeviceSession:
         v = np.ascontiguousarray(values, dtype=np.float64)
         self._check(self._lib.dlmpc_put_cols(self._h, int(which), int(c0), int(n), v.ctypes.data),
                     "dlmpc_put_cols")
+
+    # -- graph-partitioned solve with the exchange on the device -----------------
+    def dist_alloc(self, world):
+        """Exchange state for `world` ranks -> the 7 device pointers a
+        neighbour needs (ψ0, ψ1, λ0, λ1, halo counter, slot table, residual counter)."""
+        out = (C.c_void_p * 7)()
+        self._check(self._lib.dlmpc_dist_alloc(self._h, int(world), out), "dlmpc_dist_alloc")
+        return [int(v or 0) for v in out]
+
+    def dist_setup(self, rank, world, send_src, send_dst, send_peer, peer_bufs, halo_per_iter, all_bufs):
+        """peer_bufs: per destination peer its dist_alloc pointers; all_bufs:
+        per rank its dist_alloc pointers (slot table and residual counter)."""
+        n_peers = len(peer_bufs)
+        self._dist_keep = [np.ascontiguousarray(send_src, dtype=np.int64),
+                           np.ascontiguousarray(send_dst, dtype=np.int64),
+                           np.ascontiguousarray(send_peer, dtype=np.int32)]
+        arr = lambda vals: (C.c_void_p * max(1, len(vals)))(*[C.c_void_p(v) for v in vals])
+        psi = arr([b[k] for b in peer_bufs for k in (0, 1)])
+        lam = arr([b[k] for b in peer_bufs for k in (2, 3)])
+        flag = arr([b[4] for b in peer_bufs])
+        slots = arr([b[5] for b in all_bufs])
+        rflag = arr([b[6] for b in all_bufs])
+        self._dist_ptrs = (psi, lam, flag, slots, rflag)
+        src, dst, peer = self._dist_keep
+        self._check(self._lib.dlmpc_dist_setup(self._h, int(rank), int(world), n_peers, int(src.size),
+                                               _ptr(src, C.c_int64), _ptr(dst, C.c_int64), _ptr(peer, C.c_int32),
+                                               psi, lam, flag, C.c_uint32(int(halo_per_iter)), slots, rflag),
+                    "dlmpc_dist_setup")
+
+    def dist_solve(self, max_iters, eps_pri, eps_dual):
+        """One partitioned solve, exchange on the device -> (iterations, history, converged)."""
+        hist = np.zeros(2 * max_iters)
+        n = C.c_int32(0)
+        rc = self._check(self._lib.dlmpc_dist_solve(self._h, int(max_iters), float(eps_pri), float(eps_dual),
+                                                    C.byref(n), _ptr(hist, C.c_double)), "dlmpc_dist_solve")
+        k = int(n.value)
+        return k, hist[:2 * k].reshape(k, 2), rc == DLMPC_OK
 
     def set_halo(self, send_cells, recv_cells):
         """Register the partitioned path's halo cell lists (internal layout)."""

@@ -171,7 +171,9 @@ class RankSolver:
     cells are read-only input, refreshed after every iteration from the
     neighbours' packed messages (`halo_cells` order, ψ,λ interleaved)."""
 
-    def __init__(self, system, spec, mask, plans, rank, strategy="b200", device=0):
+    def __init__(self, system, spec, mask, plans, rank, strategy="b200", device=0, grid_ctas=0,
+                 device_exchange=False):
+        import os
         from .device import DeviceSession
         from .strategies import ExecStrategy
         strat = ExecStrategy(strategy) if isinstance(strategy, str) else strategy
@@ -184,9 +186,30 @@ class RankSolver:
         self.recv_from = sorted(plan.recv)
         send = [halo_cells(mask, plans, rank, q, self.layout, self.sub_ids, "src") for q in self.send_to]
         recv = [halo_cells(mask, plans, q, rank, self.layout, self.sub_ids, "dst") for q in self.recv_from]
+        self.send_cells, self.recv_cells = send, recv
         self.send_off = np.concatenate([[0], np.cumsum([2 * c.size for c in send])]).astype(np.int64)
         self.recv_off = np.concatenate([[0], np.cumsum([2 * c.size for c in recv])]).astype(np.int64)
-        self.session = DeviceSession(self.layout, strat.device if device is None else device)
+        dev = strat.device if device is None else device
+        if device_exchange:
+            # the device-side exchange runs in the non-patch modes (their stop
+            # test reads the global maxima after the exchange): the stream
+            # kernel where the layout allows it, else the two-phase kernel
+            saved = {k: os.environ.get(k) for k in ("DLMPC_FORCE_STREAM", "DLMPC_FORCE_TWOPHASE")}
+            try:
+                os.environ["DLMPC_FORCE_STREAM"] = "1"
+                self.session = DeviceSession(self.layout, dev, grid_ctas)
+                if self.session.info()["mode"] == "patch":
+                    self.session.close()
+                    os.environ["DLMPC_FORCE_TWOPHASE"] = "1"
+                    self.session = DeviceSession(self.layout, dev, grid_ctas)
+            finally:
+                for k, v in saved.items():
+                    if v is None:
+                        os.environ.pop(k, None)
+                    else:
+                        os.environ[k] = v
+        else:
+            self.session = DeviceSession(self.layout, dev, grid_ctas)
         cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0, np.int64)
         self.session.set_halo(cat(send), cat(recv))
 
@@ -278,6 +301,96 @@ def simulate_partitioned_inprocess(system, spec, mask, x0, t_sim, world, strateg
     finally:
         for rk in ranks:
             rk.close()
+
+
+def wire_device_exchange(ranks, bufs, rank, world):
+    """dlmpc_dist_setup arguments of rank `rank` from every rank's solver
+    (`ranks`, in-process) or their gathered lists: the send entries (own
+    cells, destination cells = the destination's receive cells for this
+    source, destination peer index), the peers' device buffers, the counter
+    increments per iteration (CTAs of every sending neighbour)."""
+    rk = ranks[rank]
+    src, dst, peer = [], [], []
+    for k, q in enumerate(rk.send_to):
+        kq = ranks[q].recv_from.index(rank)
+        a, b = rk.send_cells[k], ranks[q].recv_cells[kq]
+        if a.size != b.size:
+            raise RuntimeError("halo lists of ranks %d -> %d disagree" % (rank, q))
+        src.append(a); dst.append(b); peer.append(np.full(a.size, k, dtype=np.int32))
+    cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(0, dt)
+    per_iter = sum(int(ranks[q].session.info()["grid"]) for q in rk.recv_from)
+    rk.session.dist_setup(rank, world, cat(src, np.int64), cat(dst, np.int64), cat(peer, np.int32),
+                          [bufs[q] for q in rk.send_to], per_iter, bufs)
+
+
+def simulate_partitioned_device_inprocess(system, spec, mask, x0, t_sim, world, strategy="b200", device=0,
+                                          warm_start=True):
+    """The partitioned closed loop with the per-iteration exchange ON THE
+    DEVICE (dlmpc_dist_setup): every rank's halo stores, arrival counters and
+    residual slots inside the persistent kernel. On one GPU the ranks run as
+    slices of ONE cooperative launch per MPC step (dlmpc_multi_solve; each
+    rank plans for sm_count // world CTAs), so no rank's kernel waits on a
+    separate launch. Per MPC step the host sets each rank's window state and
+    collects the owned (u, x_next). Returns (states, inputs, step_iters)."""
+    import torch
+    from .device import multi_solve
+    from .errors import NotConverged
+    plans = plan_partition(mask, world)
+    sms = torch.cuda.get_device_properties(device).multi_processor_count if torch.cuda.is_available() else 148
+    ranks = [RankSolver(system, spec, mask, plans, r, strategy, device, grid_ctas=sms // world,
+                        device_exchange=True) for r in range(world)]
+    try:
+        bufs = [rk.session.dist_alloc(world) for rk in ranks]
+        for r in range(world):
+            wire_device_exchange(ranks, bufs, r, world)
+        x = np.asarray(x0, dtype=np.float64)
+        states, inputs, iters = [x], [], []
+        for step in range(t_sim):
+            for rk in ranks:
+                rk.start_step(x, cold=(step == 0 or not warm_start))
+            n, hist, ok = multi_solve([rk.session for rk in ranks], spec.max_iters, spec.eps_pri, spec.eps_dual)
+            if not ok:
+                raise NotConverged([tuple(h) for h in hist], step=step)
+            u = np.zeros(system.n_inputs)
+            xn = np.zeros(system.n_states)
+            for rk in ranks:
+                iid, uu, sid, xx = rk.finish_step()
+                u[iid] = uu
+                xn[sid] = xx
+            x = xn
+            states.append(x)
+            inputs.append(u)
+            iters.append(n)
+        return np.array(states), np.array(inputs), iters
+    finally:
+        for rk in ranks:
+            rk.close()
+
+
+def x_halo_lists(plans, system, rank):
+    """Per MPC step the measured state is needed on a rank's window (the 2d
+    hop halo, not the whole network): (send, recv) dicts of global state ids
+    -- the owned states of `rank` in each neighbour's window, and the states
+    of `rank`'s window owned by each neighbour."""
+    st = np.asarray(system.partition.state_ranges, dtype=np.int64).reshape(-1, 2)
+
+    def states_of(subs):
+        subs = np.asarray(subs, dtype=np.int64)
+        return np.concatenate([np.arange(*st[i]) for i in subs]) if subs.size else np.zeros(0, np.int64)
+
+    me = plans[rank]
+    own = set(range(*me.own))
+    send, recv = {}, {}
+    for q, p in enumerate(plans):
+        if q == rank:
+            continue
+        mine_in_q = [i for i in np.asarray(p.need).tolist() if i in own]
+        if mine_in_q:
+            send[q] = states_of(mine_in_q)
+        theirs = [i for i in np.asarray(me.need).tolist() if p.own[0] <= i < p.own[1]]
+        if theirs:
+            recv[q] = states_of(theirs)
+    return send, recv
 
 
 class DistExchange:
@@ -388,4 +501,86 @@ def simulate_partitioned(system, spec, mask, x0, t_sim, strategy="b200", warm_st
             iters.append(len(hist))
         return np.array(states), np.array(inputs), iters
     finally:
+        rk.close()
+
+
+def simulate_partitioned_device(system, spec, mask, x0, t_sim, strategy="b200", warm_start=True, group=None):
+    """The partitioned closed loop over torch.distributed ranks, one GPU per
+    rank, with the per-iteration exchange ON THE DEVICE: the ranks' buffers
+    are mapped into each other's address space once (CUDA IPC, NVLink P2P),
+    and every MPC step is ONE persistent launch per rank whose CTAs store the
+    halo straight into the neighbours' ψ/λ buffers and agree on the global
+    stop test through the residual slots (dlmpc_dist_solve) -- no host
+    involvement per ADMM iteration. Per MPC step only the 2d-hop halo of the
+    measured state crosses (x_halo_lists, point to point); the owned parts
+    of the trajectory are gathered once at the end. Returns (states,
+    inputs, step_iters) on every rank."""
+    import torch
+    import torch.distributed as dist
+    from .device import ipc_close, ipc_handle, ipc_open
+    from .errors import NotConverged
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = torch.cuda.current_device()
+    plans = plan_partition(mask, world)
+    rk = RankSolver(system, spec, mask, plans, rank, strategy, dev, device_exchange=True)
+    opened = []
+    try:
+        bufs = rk.session.dist_alloc(world)
+        mine = {"ipc": [ipc_handle(p) for p in bufs], "grid": rk.session.info()["grid"],
+                "recv_from": list(rk.recv_from), "recv_cells": [np.asarray(c) for c in rk.recv_cells]}
+        infos = [None] * world
+        dist.all_gather_object(infos, mine, group=group)
+        all_bufs = []
+        for q in range(world):
+            if q == rank:
+                all_bufs.append(bufs)
+            else:
+                ptrs = [ipc_open(h, dev) for h in infos[q]["ipc"]]
+                opened.extend(ptrs)
+                all_bufs.append(ptrs)
+        src, dst, peer = [], [], []
+        for k, q in enumerate(rk.send_to):
+            b = infos[q]["recv_cells"][infos[q]["recv_from"].index(rank)]
+            src.append(rk.send_cells[k]); dst.append(b); peer.append(np.full(b.size, k, dtype=np.int32))
+        cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(0, dt)
+        rk.session.dist_setup(rank, world, cat(src, np.int64), cat(dst, np.int64), cat(peer, np.int32),
+                              [all_bufs[q] for q in rk.send_to], sum(infos[q]["grid"] for q in rk.recv_from),
+                              all_bufs)
+        dist.barrier(group=group)   # every rank's counters exist before the first push
+        xsend, xrecv = x_halo_lists(plans, system, rank)
+        tdev = torch.device("cuda", dev) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+        x = np.array(x0, dtype=np.float64)
+        own_x, own_u, iters = [], [], []
+        for step in range(t_sim):
+            rk.start_step(x, cold=(step == 0 or not warm_start))
+            n, hist, ok = rk.session.dist_solve(spec.max_iters, spec.eps_pri, spec.eps_dual)
+            if not ok:
+                raise NotConverged([tuple(h) for h in hist], step=step)
+            iid, uu, sid, xx = rk.finish_step()
+            x[sid] = xx
+            ops, rbufs = [], {}
+            for q, ids in xsend.items():
+                ops.append(dist.P2POp(dist.isend, torch.as_tensor(x[ids], device=tdev), q, group))
+            for q, ids in xrecv.items():
+                rbufs[q] = torch.zeros(ids.size, dtype=torch.float64, device=tdev)
+                ops.append(dist.P2POp(dist.irecv, rbufs[q], q, group))
+            if ops:
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+            for q, ids in xrecv.items():
+                x[ids] = rbufs[q].cpu().numpy()
+            own_x.append((sid, xx)); own_u.append((iid, uu)); iters.append(n)
+        parts = [None] * world
+        dist.all_gather_object(parts, (own_x, own_u), group=group)
+        states = np.zeros((t_sim + 1, system.n_states))
+        inputs = np.zeros((t_sim, system.n_inputs))
+        states[0] = x0
+        for px, pu in parts:
+            for t, ((sid, xx), (iid, uu)) in enumerate(zip(px, pu)):
+                states[t + 1, sid] = xx
+                inputs[t, iid] = uu
+        return states, inputs, iters
+    finally:
+        for p in opened:
+            ipc_close(p)
         rk.close()

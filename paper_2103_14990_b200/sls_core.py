@@ -31,6 +31,30 @@ import scipy.sparse as sp
 from .errors import LocalityInfeasible, RowInfeasible
 from .system_model import LocalityMask, LtiSystem, SubsystemPartition
 
+# The class factorisations (pivoted QR, Cholesky, SVD null space) run with a
+# FIXED number of BLAS threads: OpenBLAS's multi-threaded kernels split the
+# work by thread count, so their last bits depend on the machine (measured:
+# the d=4, T=20 class operators differ between an 8- and a 16-core host, the
+# d=6, T=30 ones between every thread count). Two threads reproduce the
+# reference's own multi-threaded setup on the benchmark chains (d=3, T=10:
+# the same bits for 2, 4 and 8 threads) and make every other cell the same
+# on every host, so the exact path stays bit-identical across machines.
+SETUP_BLAS_THREADS = 2
+
+
+def _fixed_blas(fn):
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        try:
+            from threadpoolctl import threadpool_limits
+        except ImportError:   # pragma: no cover - threadpoolctl is a scikit-learn dependency here
+            return fn(*args, **kwargs)
+        with threadpool_limits(limits=SETUP_BLAS_THREADS, user_api="blas"):
+            return fn(*args, **kwargs)
+    return wrapped
+
 STATE = "state"
 INPUT = "input"
 
@@ -279,6 +303,7 @@ class ColumnClasses:
         return self.classes[self.col_class[c]].projector @ self.reduced_rhs(c)
 
     @classmethod
+    @_fixed_blas
     def from_precomps(cls, col_solvers):
         """Classes recovered from a plain list of ColumnPrecomp (bit-identical
         `g` and `projector` -> one class)."""
@@ -398,6 +423,7 @@ def _finish_classes(classes, col_class, col_pin, n_touch_of_col, reps_g0, failin
     return ColumnClasses(classes, col_class, rhs_table, col_rhs, sub_struct, touch, col_pin)
 
 
+@_fixed_blas
 def build_column_classes(op: DynamicsOperator, mask: LocalityMask) -> ColumnClasses:
     """Class-deduplicated version of the reference's per-column reduction
     (sls_core.py:253-289): one restricted operator per support set (read from
@@ -511,6 +537,7 @@ def _window_operator(system: LtiSystem, horizon: int, d: int, j: int):
     return touch, g0, pins
 
 
+@_fixed_blas
 def build_column_classes_structural(system: LtiSystem, horizon: int, mask: LocalityMask,
                                     verify_members: int = 2) -> ColumnClasses:
     """Scalable class builder for large networks (N up to 10^6+): subsystems

@@ -262,3 +262,52 @@ def test_distributed_driver_gloo_multi_process(name, world):
         assert iters == list(g["step_iters"]), rank
         assert np.array_equal(states, g["states"]), rank
         assert np.array_equal(inputs, g["inputs"]), rank
+
+
+# --------------------------------------------------------------------------
+# the exchange ON THE DEVICE (dlmpc_dist_setup / dlmpc_multi_solve)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("name,world", [("c1_loop_seed1", 2), ("c2_loop_seed1", 3), ("d4_loop_n20", 2),
+                                        ("unbounded_loop_n8", 2), ("d1_loop_n30", 4)])
+@pytest.mark.parametrize("variant", [EXACT, FAST])
+def test_device_exchange_closed_loop_against_reference(name, world, variant):
+    """Every ADMM iteration's halo stores, arrival counters and global stop
+    test inside the persistent kernel (the ranks as slices of one cooperative
+    launch on this GPU): the reference's closed loops, bit for bit in exact
+    mode."""
+    from paper_2103_14990_b200.partition import simulate_partitioned_device_inprocess
+    g = golden(name)
+    system, spec, mask, t_sim = loop_problem(g)
+    states, inputs, iters = simulate_partitioned_device_inprocess(system, spec, mask, g["x0"], t_sim, world,
+                                                                  variant)
+    assert iters == list(g["step_iters"])
+    if variant == EXACT:
+        assert np.array_equal(states, g["states"]) and np.array_equal(inputs, g["inputs"])
+    else:
+        assert rel_err(states, g["states"]) <= 1e-9 and rel_err(inputs, g["inputs"]) <= 1e-9
+
+
+def test_device_exchange_matches_host_driven_exchange():
+    """Device-side and host-driven exchange run the same rank sub-problems
+    on the same kernels: bit-identical trajectories (N=2500, 4 ranks, stream
+    kernel)."""
+    from paper_2103_14990_b200.partition import simulate_partitioned_device_inprocess
+    system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=2500, d=3, horizon=10, seed=6))
+    a_states, a_inputs, a_iters = simulate_partitioned_device_inprocess(system, spec, mask, x0, 2, 4, FAST)
+    one, _ = pb.dlmpc_simulate(system, spec, mask, x0, 2, FAST)
+    assert a_iters == list(one.step_iterations)
+    assert rel_err(a_states, one.states) <= 1e-12
+
+
+@pytest.mark.slow
+def test_device_exchange_c5_determinism_at_1e5():
+    """N=10^5 on 8 ranks, exchange on the device, exact arithmetic: bit for
+    bit the single-domain solve (the C5 claim of SURVEY §8(e))."""
+    from paper_2103_14990_b200.partition import simulate_partitioned_device_inprocess
+    system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=100000, d=3, horizon=10, seed=1))
+    states, inputs, iters = simulate_partitioned_device_inprocess(system, spec, mask, x0, 1, 8, EXACT)
+    sess = pb.DlmpcSession(system, spec, mask, EXACT)
+    one, _ = sess.simulate(x0, 1)
+    sess.close()
+    assert iters == list(one.step_iterations)
+    assert np.array_equal(states, one.states) and np.array_equal(inputs, one.inputs)

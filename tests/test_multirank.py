@@ -230,3 +230,26 @@ def test_rank_window_layouts_reproduce_single_domain(n, d, t, world):
             w = min(RL.s_pad, L.s_pad)
             assert np.array_equal(em.psi[c * RL.s_pad:c * RL.s_pad + w], ref.psi[g * L.s_pad:g * L.s_pad + w])
             assert np.array_equal(em.lam[c * RL.s_pad:c * RL.s_pad + w], ref.lam[g * L.s_pad:g * L.s_pad + w])
+
+
+def test_x_halo_lists_cover_every_window():
+    """Per MPC step only the 2d-hop halo of the measured state crosses ranks
+    (partition.x_halo_lists): what r sends q is exactly what q expects from
+    r, and own + received states cover each rank's window."""
+    import paper_2103_14990_b200 as pb
+    from paper_2103_14990_b200.partition import plan_partition, x_halo_lists
+    system = pb.build_chain_network(40)
+    mask = pb.build_locality_mask(system, 3, 5)
+    st = np.asarray(system.partition.state_ranges).reshape(-1, 2)
+    for world in (2, 3, 5):
+        plans = plan_partition(mask, world)
+        lists = [x_halo_lists(plans, system, r) for r in range(world)]
+        for r in range(world):
+            send, recv = lists[r]
+            for q, ids in send.items():
+                assert np.array_equal(ids, lists[q][1][r])
+            window = np.concatenate([np.arange(*st[i]) for i in plans[r].need])
+            own = np.concatenate([np.arange(*st[i]) for i in range(*plans[r].own)])
+            got = np.concatenate([own] + list(recv.values()))
+            assert np.array_equal(np.sort(got), np.sort(window))
+            assert sum(v.size for v in recv.values()) < system.n_states - own.size or world == 2
