@@ -369,18 +369,20 @@ C5_N = 1000000
 
 def partitioned_c5(pb, dist, local, solves=2):
     """SURVEY §8(e) C5 on all ranks: the chain N=10^6, d=3, T=10 step-0 solve,
-    graph-partitioned across the world (each rank: own subsystem range + 2d
-    halo; per iteration an all-reduce(max) of the residuals and one NCCL
-    message per neighbour). Strong scaling (total work fixed). Beside it, in
+    graph-partitioned across the world with the exchange ON THE DEVICE
+    (partition.DeviceExchangeRank: each rank's persistent kernel stores the
+    halo into its neighbours' buffers over NVLink and agrees on the global
+    stop test through residual slots -- one launch per solve, no host step
+    per ADMM iteration). Strong scaling (total work fixed). Beside it, in
     the same run, every rank solves the WHOLE problem alone on its own GPU
     (the world-1 baseline; max over ranks), so the efficiency is
-    t_1 / (world * t_world) from one run. Timed with CUDA events on each
-    rank's library stream around whole solves, max over ranks."""
+    t_1 / (world * t_world) from one run. Device time of each rank's launch
+    (CUDA events on its stream), max over ranks."""
     import torch
-    from paper_2103_14990_b200.partition import DistExchange, RankSolver, halo_bytes_per_iteration, plan_partition
+    from paper_2103_14990_b200.partition import DeviceExchangeRank, halo_bytes_per_iteration, plan_partition
     rank, world = dist.get_rank(), dist.get_world_size()
     t0 = time.perf_counter()
-    rk, err = None, None
+    ex, err = None, None
     try:
         system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=C5_N, d=D, horizon=T, t_sim=1, seed=1))
         # same-run single-GPU baseline of the same problem
@@ -390,45 +392,38 @@ def partitioned_c5(pb, dist, local, solves=2):
         one_its = int(tr.step_iterations[0])
         one.close()
         del one
-        plans = plan_partition(mask, world)
-        rk = RankSolver(system, spec, mask, plans, rank, "b200", local)
     except Exception as exc:
         err = repr(exc)[:300]
         one_ms, one_its = 0.0, 0
-    setup_s = time.perf_counter() - t0
-    # no rank enters the per-iteration collectives unless every rank is set up
     ok = torch.tensor([0.0 if err else 1.0], dtype=torch.float64, device=f"cuda:{local}")
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     if ok.item() < 1.0:
-        if rk is not None:
-            rk.close()
         return {"error": err or "setup failed on another rank"}
     try:
-        ex = DistExchange(rk)
-        ext = torch.cuda.ExternalStream(rk.session.stream, device=f"cuda:{local}")
-        ex.solve_step(x0, True, spec)                       # warm-up solve
-        dist.barrier()
-        torch.cuda.synchronize()
+        plans = plan_partition(mask, world)
+        ex = DeviceExchangeRank(system, spec, mask, "b200", plans=plans)
+        setup_s = time.perf_counter() - t0
+        n, _, conv = ex.solve(x0, True)                       # warm-up solve
         ms, its = 0.0, 0
         for _ in range(solves):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(ext)
-            hist = ex.solve_step(x0, True, spec)
-            e1.record(ext)
-            torch.cuda.synchronize()
-            ms += e0.elapsed_time(e1)
-            its += len(hist)
-        # every rank runs the same (global) iterations: max over ranks for all
-        t = torch.tensor([its, ms, setup_s, one_ms, one_its], dtype=torch.float64, device=f"cuda:{local}")
+            dist.barrier()
+            n, _, conv = ex.solve(x0, True)
+            ms += ex.rk.session.last_timing()[0]
+            its += n
+        t = torch.tensor([its, ms, setup_s, one_ms, one_its, 0.0 if conv else 1.0], dtype=torch.float64,
+                         device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        its_m, ms_m, setup_m, one_ms_m, one_its_m = (float(v) for v in t.cpu())
-        hb = max(halo_bytes_per_iteration(plans, mask, rk.layout.s_pad))
+        its_m, ms_m, setup_m, one_ms_m, one_its_m, bad = (float(v) for v in t.cpu())
+        hb = max(halo_bytes_per_iteration(plans, mask, ex.rk.layout.s_pad))
         ms_it = ms_m / its_m
         one_ms_it = one_ms_m / max(1.0, one_its_m)
         return {"workload": "chain N=1e6 d=3 T=10 step-0 solve (C5), graph-partitioned, cold start",
                 "n_gpus": world, "scaling": "strong",
+                "exchange": "on the device: halo stores into peer buffers over NVLink (CUDA IPC), arrival "
+                            "counters and residual slots inside the persistent kernel, one launch per solve",
                 "value": C5_N * its_m / (ms_m * 1e-3), "unit": UNIT,
                 "ms_per_iteration": ms_it, "iterations_per_solve": its_m / solves,
+                "converged": bad == 0.0,
                 "single_gpu_same_run": {"ms_per_iteration": one_ms_it, "iterations": one_its_m,
                                         "value": C5_N / (one_ms_it * 1e-3),
                                         "timing": "whole problem on each rank's own GPU, best of "
@@ -436,11 +431,12 @@ def partitioned_c5(pb, dist, local, solves=2):
                 "speedup_vs_single_gpu": one_ms_it / ms_it,
                 "parallel_efficiency": one_ms_it / ms_it / world,
                 "iterations_equal_single_gpu": abs(its_m / solves - one_its_m) < 0.5,
-                "solves_timed": solves, "per_rank_kernel": rk.session.info()["mode"],
+                "solves_timed": solves, "per_rank_kernel": ex.rk.session.info()["mode"],
                 "halo_bytes_per_iteration_max_rank": hb, "setup_s_max_rank": setup_m,
-                "timing": "CUDA events on each rank's stream around whole solves, max over ranks"}
+                "timing": "CUDA events around each rank's persistent launch, max over ranks"}
     finally:
-        rk.close()
+        if ex is not None:
+            ex.close()
 
 
 def run_reference_arm(args):

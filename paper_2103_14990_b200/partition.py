@@ -504,56 +504,83 @@ def simulate_partitioned(system, spec, mask, x0, t_sim, strategy="b200", warm_st
         rk.close()
 
 
-def simulate_partitioned_device(system, spec, mask, x0, t_sim, strategy="b200", warm_start=True, group=None):
-    """The partitioned closed loop over torch.distributed ranks, one GPU per
-    rank, with the per-iteration exchange ON THE DEVICE: the ranks' buffers
-    are mapped into each other's address space once (CUDA IPC, NVLink P2P),
-    and every MPC step is ONE persistent launch per rank whose CTAs store the
-    halo straight into the neighbours' ψ/λ buffers and agree on the global
-    stop test through the residual slots (dlmpc_dist_solve) -- no host
-    involvement per ADMM iteration. Per MPC step only the 2d-hop halo of the
-    measured state crosses (x_halo_lists, point to point); the owned parts
-    of the trajectory are gathered once at the end. Returns (states,
-    inputs, step_iters) on every rank."""
-    import torch
-    import torch.distributed as dist
-    from .device import ipc_close, ipc_handle, ipc_open
-    from .errors import NotConverged
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    dev = torch.cuda.current_device()
-    plans = plan_partition(mask, world)
-    rk = RankSolver(system, spec, mask, plans, rank, strategy, dev, device_exchange=True)
-    opened = []
-    try:
-        bufs = rk.session.dist_alloc(world)
+class DeviceExchangeRank:
+    """One rank of the partitioned solve with the exchange on the device,
+    over torch.distributed (one GPU per rank): the rank's sub-problem on a
+    non-patch kernel, its buffers mapped into every other rank (CUDA IPC,
+    NVLink P2P) and the exchange wired (dlmpc_dist_setup). `solve(x, cold)`
+    is then ONE persistent launch per MPC step with no host involvement per
+    ADMM iteration."""
+
+    def __init__(self, system, spec, mask, strategy="b200", group=None, plans=None):
+        import torch
+        import torch.distributed as dist
+        from .device import ipc_handle, ipc_open
+        self.dist, self.group, self.spec = dist, group, spec
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.dev = torch.cuda.current_device()
+        self.plans = plans if plans is not None else plan_partition(mask, self.world)
+        self.rk = rk = RankSolver(system, spec, mask, self.plans, self.rank, strategy, self.dev,
+                                  device_exchange=True)
+        self._opened = []
+        bufs = rk.session.dist_alloc(self.world)
         mine = {"ipc": [ipc_handle(p) for p in bufs], "grid": rk.session.info()["grid"],
                 "recv_from": list(rk.recv_from), "recv_cells": [np.asarray(c) for c in rk.recv_cells]}
-        infos = [None] * world
+        infos = [None] * self.world
         dist.all_gather_object(infos, mine, group=group)
         all_bufs = []
-        for q in range(world):
-            if q == rank:
+        for q in range(self.world):
+            if q == self.rank:
                 all_bufs.append(bufs)
             else:
-                ptrs = [ipc_open(h, dev) for h in infos[q]["ipc"]]
-                opened.extend(ptrs)
+                ptrs = [ipc_open(h, self.dev) for h in infos[q]["ipc"]]
+                self._opened.extend(ptrs)
                 all_bufs.append(ptrs)
         src, dst, peer = [], [], []
         for k, q in enumerate(rk.send_to):
-            b = infos[q]["recv_cells"][infos[q]["recv_from"].index(rank)]
+            b = infos[q]["recv_cells"][infos[q]["recv_from"].index(self.rank)]
             src.append(rk.send_cells[k]); dst.append(b); peer.append(np.full(b.size, k, dtype=np.int32))
         cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(0, dt)
-        rk.session.dist_setup(rank, world, cat(src, np.int64), cat(dst, np.int64), cat(peer, np.int32),
+        rk.session.dist_setup(self.rank, self.world, cat(src, np.int64), cat(dst, np.int64), cat(peer, np.int32),
                               [all_bufs[q] for q in rk.send_to], sum(infos[q]["grid"] for q in rk.recv_from),
                               all_bufs)
         dist.barrier(group=group)   # every rank's counters exist before the first push
-        xsend, xrecv = x_halo_lists(plans, system, rank)
-        tdev = torch.device("cuda", dev) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+
+    def solve(self, x, cold):
+        """One MPC step's solve -> (iterations, history, converged)."""
+        self.rk.start_step(x, cold)
+        return self.rk.session.dist_solve(self.spec.max_iters, self.spec.eps_pri, self.spec.eps_dual)
+
+    def close(self):
+        from .device import ipc_close
+        for p in self._opened:
+            ipc_close(p)
+        self._opened = []
+        self.rk.close()
+
+
+def simulate_partitioned_device(system, spec, mask, x0, t_sim, strategy="b200", warm_start=True, group=None):
+    """The partitioned closed loop over torch.distributed ranks, one GPU per
+    rank, with the per-iteration exchange ON THE DEVICE (DeviceExchangeRank):
+    every MPC step is ONE persistent launch per rank whose CTAs store the halo
+    straight into the neighbours' ψ/λ buffers and agree on the global stop
+    test through the residual slots -- no host involvement per ADMM
+    iteration. Per MPC step only the 2d-hop halo of the measured state
+    crosses (x_halo_lists, point to point); the owned parts of the trajectory
+    are gathered once at the end. Returns (states, inputs, step_iters) on
+    every rank."""
+    import torch
+    import torch.distributed as dist
+    from .errors import NotConverged
+    ex = DeviceExchangeRank(system, spec, mask, strategy, group)
+    rk, rank, world = ex.rk, ex.rank, ex.world
+    try:
+        xsend, xrecv = x_halo_lists(ex.plans, system, rank)
+        tdev = torch.device("cuda", ex.dev) if dist.get_backend(group) == "nccl" else torch.device("cpu")
         x = np.array(x0, dtype=np.float64)
         own_x, own_u, iters = [], [], []
         for step in range(t_sim):
-            rk.start_step(x, cold=(step == 0 or not warm_start))
-            n, hist, ok = rk.session.dist_solve(spec.max_iters, spec.eps_pri, spec.eps_dual)
+            n, hist, ok = ex.solve(x, cold=(step == 0 or not warm_start))
             if not ok:
                 raise NotConverged([tuple(h) for h in hist], step=step)
             iid, uu, sid, xx = rk.finish_step()
@@ -581,6 +608,4 @@ def simulate_partitioned_device(system, spec, mask, x0, t_sim, strategy="b200", 
                 inputs[t, iid] = uu
         return states, inputs, iters
     finally:
-        for p in opened:
-            ipc_close(p)
-        rk.close()
+        ex.close()

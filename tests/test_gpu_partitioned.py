@@ -311,3 +311,27 @@ def test_device_exchange_c5_determinism_at_1e5():
     sess.close()
     assert iters == list(one.step_iterations)
     assert np.array_equal(states, one.states) and np.array_equal(inputs, one.inputs)
+
+
+@pytest.mark.parametrize("name", ["c1_loop_seed1", "c2_loop_seed1"])
+def test_device_exchange_distributed_driver_world1(name):
+    """The torch.distributed driver of the device exchange
+    (simulate_partitioned_device: IPC wiring, one dist_solve launch per MPC
+    step, 2d-hop x halo, trajectory gather) at world size 1 over NCCL on this
+    box: the reference's closed loop bit for bit."""
+    import torch.distributed as dist
+    from paper_2103_14990_b200.partition import simulate_partitioned_device
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        g = golden(name)
+        system, spec, mask, t_sim = loop_problem(g)
+        states, inputs, iters = simulate_partitioned_device(system, spec, mask, g["x0"], t_sim, EXACT)
+        assert iters == list(g["step_iters"])
+        assert np.array_equal(states, g["states"]) and np.array_equal(inputs, g["inputs"])
+    finally:
+        dist.destroy_process_group()
