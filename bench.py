@@ -644,7 +644,7 @@ def run_device_arm(args):
     if part is not None:
         line["partitioned"] = part
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or (part is not None and dist.is_initialized()):
         dist.destroy_process_group()
 
 
