@@ -737,6 +737,69 @@ __device__ __forceinline__ void gemm2(int S8, int n08, int ldn, const double* no
   }
 }
 
+// GEMM 2 on the m16n8k8 FP64 shape (stream mode, DLMPC_STREAM_G2M16): warp w
+// takes the 16-row tile w (two of gemm2's 8-row tiles) and each k8 step is
+// ONE mma per n-tile instead of eight m8n8k4 -- 4x fewer tensor instructions
+// for the same FLOPs and fragment loads. Fragment layouts verified by
+// tools/microbench/dmma_layout.cu (g = lane>>2, t = lane&3):
+//   A (16 x 8, row): a_i = A[g + 8*(i%2)][t + 4*(i/2)];  B (8 x 8, col): b_i = B[t + 4i][g]
+//   C (16 x 8): c0, c1 = C[g][2t], C[g][2t+1];  c2, c3 = C[g+8][2t], C[g+8][2t+1]
+// Rows past S8 (an odd number of 8-row tiles) read zeros. The epilogue sees
+// the same (m, mt, nn, c0, c1) calls as gemm2's.
+__device__ __forceinline__ void dmma16(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+template <int TC, class Epi, int NW = kWarps>
+__device__ __forceinline__ void gemm2_m16(int S8, int n08, int ldn, const double* nop, const double* yb, int ldy,
+                                          Epi& epi) {
+  constexpr int NTN = TC / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tig = lane & 3;
+  const int mt2 = S8 >> 3, mt16 = (mt2 + 1) >> 1, ks8 = n08 >> 3;
+  for (int w = warp; w < mt16; w += NW) {
+    const int mt0 = 2 * w, mt1 = 2 * w + 1;
+    const bool hi_ok = mt1 < mt2;
+    epi.prefetch(0, mt0);
+    if (hi_ok) epi.prefetch(1, mt1);
+    double acc[NTN][4];
+#pragma unroll
+    for (int nn = 0; nn < NTN; ++nn) { acc[nn][0] = acc[nn][1] = acc[nn][2] = acc[nn][3] = 0.0; }
+    const double* r_lo = nop + static_cast<size_t>(mt0 * 8 + g) * ldn;
+    const double* r_hi = nop + static_cast<size_t>(mt1 * 8 + g) * ldn;
+#pragma unroll 2
+    for (int ks = 0; ks < ks8; ++ks) {
+      const int k0 = ks * 8 + tig;
+      double a[4];
+      a[0] = r_lo[k0];
+      a[2] = r_lo[k0 + 4];
+      a[1] = hi_ok ? r_hi[k0] : 0.0;
+      a[3] = hi_ok ? r_hi[k0 + 4] : 0.0;
+#pragma unroll
+      for (int nn = 0; nn < NTN; ++nn) {
+        double bf[2];
+        bf[0] = yb[k0 * ldy + nn * 8 + g];
+        bf[1] = yb[(k0 + 4) * ldy + nn * 8 + g];
+        dmma16(acc[nn], a, bf);
+      }
+    }
+    epi.before_store();
+#pragma unroll
+    for (int nn = 0; nn < NTN; ++nn) {
+      epi.store(0, mt0, nn, acc[nn][0], acc[nn][1]);
+      if (hi_ok) epi.store(1, mt1, nn, acc[nn][2], acc[nn][3]);
+    }
+  }
+}
+
+// measured (tools/lib_ab.sh, fixed 200 iterations): N=3e3 26.01 -> 25.68,
+// N=1e4 72.50 -> 72.40, N=1e5 642.6 -> 640.8 us/iter
+#ifndef DLMPC_STREAM_G2M16
+#define DLMPC_STREAM_G2M16 1
+#endif
+
 // GEMM 1 for chunks of at most two live columns (C2-sized networks): a DFMA
 // GEMV, Y[a][t] = sum_p N[p][a] K[t][p], split over support slices whose
 // partials are reduced in shared memory (`part`, >= 10*n08 doubles). Lanes
@@ -1948,7 +2011,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
 #ifdef DLMPC_CHECKED
           epi.chk = CellChk{P.dbg, P.own_col_lo, P.own_col_hi, P.s_pad, P.col_len};
 #endif
-          gemm2<TC, StreamEpi<TC>, kCons>(S8, n08, ldn, nop, yb, P.ldy, epi);
+          if (DLMPC_STREAM_G2M16) gemm2_m16<TC, StreamEpi<TC>, kCons>(S8, n08, ldn, nop, yb, P.ldy, epi);
+          else gemm2<TC, StreamEpi<TC>, kCons>(S8, n08, ldn, nop, yb, P.ldy, epi);
           pri_m = epi.pri_m; dual_m = epi.dual_m;
 #ifdef DLMPC_PHASE_TIMING
           if (tid == 0) {
@@ -2003,7 +2067,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
 #ifdef DLMPC_CHECKED
       epi.chk = CellChk{P.dbg, P.own_col_lo, P.own_col_hi, P.s_pad, P.col_len};
 #endif
-      gemm2<TC>(S8, n08, ldn, nop, yb, P.ldy, epi);
+      if (DLMPC_STREAM_G2M16) gemm2_m16<TC>(S8, n08, ldn, nop, yb, P.ldy, epi);
+      else gemm2<TC>(S8, n08, ldn, nop, yb, P.ldy, epi);
       pri_m = epi.pri_m; dual_m = epi.dual_m;
       __syncthreads();
       PT_LAP(P, 3)
