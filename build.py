@@ -14,7 +14,7 @@ import sys
 ROOT = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.join(ROOT, "paper_2103_14990_b200")
 SRC_DIR = os.path.join(PKG, "csrc")
-SOURCES = [os.path.join(SRC_DIR, "dlmpc.cu")]
+SOURCES = [os.path.join(SRC_DIR, "dlmpc.cu"), os.path.join(SRC_DIR, "dlmpc_multi.cu")]
 DEPS = SOURCES + [os.path.join(SRC_DIR, "dlmpc_device.cuh"), os.path.join(SRC_DIR, "dlmpc_schedules.cuh"),
         os.path.join(ROOT, "include", "dlmpc.h")]
 OUT = os.path.join(PKG, "libdlmpc.so")
@@ -38,18 +38,32 @@ def needs_build(out=OUT):
 
 
 def build(force=False, verbose=False, checked=False):
+    """Compile the translation units in parallel (one nvcc per source, -c),
+    then link the shared library."""
+    from concurrent.futures import ThreadPoolExecutor
     out = OUT_CHECKED if checked else OUT
     if not force and not needs_build(out):
         return out
-    cmd = [nvcc()] + NVCC_FLAGS + (["-DDLMPC_CHECKED"] if checked else []) + ["-o", out] + SOURCES
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    if verbose:
-        for line in (res.stdout + res.stderr).splitlines():
-            if "registers" in line or "spill" in line or "error" in line:
-                print(line)
+    flags = [f for f in NVCC_FLAGS if f != "-shared"] + (["-DDLMPC_CHECKED"] if checked else [])
+    obj_dir = os.path.join(ROOT, "build", "checked" if checked else "release")
+    os.makedirs(obj_dir, exist_ok=True)
+    objs = [os.path.join(obj_dir, os.path.basename(src) + ".o") for src in SOURCES]
+
+    def compile_one(src, obj):
+        cmd = [nvcc()] + flags + ["-c", "-o", obj, src]
+        return cmd, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(len(SOURCES)) as pool:
+        results = list(pool.map(lambda so: compile_one(*so), zip(SOURCES, objs)))
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out] + objs
+    for cmd, res in results + [(link, subprocess.run(link, capture_output=True, text=True))]:
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("nvcc failed: " + " ".join(cmd))
+        if verbose:
+            for line in (res.stdout + res.stderr).splitlines():
+                if "registers" in line or "spill" in line or "error" in line:
+                    print(line)
     return out
 
 

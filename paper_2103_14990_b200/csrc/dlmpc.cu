@@ -20,6 +20,11 @@ namespace {
 thread_local std::string g_global_error;
 }  // namespace
 
+namespace dlmpc {   // dlmpc_multi.cu
+cudaError_t launch_multi_kernel(int mode, int tc, const DevProblem* probs, const RunArgs* runs,
+                                const int* cta_base, int n_ranks, int grid, int smem, cudaStream_t stream);
+}
+
 struct dlmpc_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -85,21 +90,25 @@ int alloc(dlmpc_handle* h, size_t n, T** dst) {
 
 using KernelFn = void (*)(DevProblem, RunArgs);
 
-using MultiFn = void (*)(const DevProblem*, const RunArgs*, const int*, int);
-
-MultiFn pick_multi_kernel(int mode, int tc) {
-  if (mode == kExact) return dlmpc_multi_kernel<8, kExact>;
-  if (mode == kStream) return tc == 16 ? dlmpc_multi_kernel<16, kStream> : dlmpc_multi_kernel<8, kStream>;
-  if (mode == kTwoPhase) return tc == 16 ? dlmpc_multi_kernel<16, kTwoPhase> : dlmpc_multi_kernel<8, kTwoPhase>;
-  return nullptr;   // patch modes: the overlapped stop test reads the local maxima
-}
-
 KernelFn pick_kernel(int mode, int tc, int rb = 0) {
   if (mode == kExact) return dlmpc_persistent<8, kExact>;
   if (mode == kPatch && rb) return dlmpc_persistent<8, kPatchRb>;   // TC 8 only
   if (mode == kPatch) return tc == 16 ? dlmpc_persistent<16, kPatch> : dlmpc_persistent<8, kPatch>;
   if (mode == kStream) return tc == 16 ? dlmpc_persistent<16, kStream> : dlmpc_persistent<8, kStream>;
   return tc == 16 ? dlmpc_persistent<16, kTwoPhase> : dlmpc_persistent<8, kTwoPhase>;
+}
+
+// the instantiation with the K-split pairs (patch mode) or the device-side
+// exchange (dlmpc_dist_solve; non-patch modes)
+KernelFn pick_kernel_var(int mode, int tc, int var) {
+  if (var == kVarPairs && mode == kPatch)
+    return tc == 16 ? dlmpc_persistent<16, kPatch, kVarPairs> : dlmpc_persistent<8, kPatch, kVarPairs>;
+  if (var == kVarDist) {
+    if (mode == kExact) return dlmpc_persistent<8, kExact, kVarDist>;
+    if (mode == kStream) return tc == 16 ? dlmpc_persistent<16, kStream, kVarDist> : dlmpc_persistent<8, kStream, kVarDist>;
+    if (mode == kTwoPhase) return tc == 16 ? dlmpc_persistent<16, kTwoPhase, kVarDist> : dlmpc_persistent<8, kTwoPhase, kVarDist>;
+  }
+  return nullptr;
 }
 
 int ld_frag(int n) {   // smallest ld >= n with ld % 16 in {4, 12}: conflict-free FP64 fragments
@@ -148,8 +157,11 @@ int ensure_run_buffers(dlmpc_handle* h, int max_iters, int t_sim) {
   return DLMPC_OK;
 }
 
-int launch(dlmpc_handle* h, const RunArgs& R) {
+int launch(dlmpc_handle* h, const RunArgs& R, int var = 0) {
   KernelFn fn = pick_kernel(h->mode, h->P.tile_cols, h->P.rb_gemv);
+  if (h->P.cta_pair && h->mode == kPatch) var |= kVarPairs;
+  if (var) fn = pick_kernel_var(h->mode, h->P.tile_cols, var);
+  if (!fn) return fail(h, DLMPC_BAD_ARGUMENT, "no kernel variant for this mode");
   // the shared-memory limit is a per-function attribute: sessions of one
   // instantiation with different plans (the ranks of a partitioned solve in
   // one process) each set their own before launching
@@ -767,6 +779,8 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
     }
   }
   P.smem_doubles = h->smem_bytes / 8;
+  P.vbase = 0;          // the whole launch (dlmpc_multi_solve shifts it per rank)
+  P.vgrid = h->grid;
   KernelFn fn = pick_kernel(h->mode, P.tile_cols, P.rb_gemv);
   CUDA_OR_FAIL(h, cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem_bytes));
@@ -1403,7 +1417,7 @@ int dlmpc_dist_solve(dlmpc_handle* h, int max_iters, double eps_pri, double eps_
   cudaSetDevice(h->device);
   if (int rc = ensure_run_buffers(h, max_iters, 1)) return rc;
   RunArgs R = solve_args(h, max_iters, eps_pri, eps_dual);
-  if (int rc = launch(h, R)) return rc;
+  if (int rc = launch(h, R, kVarDist)) return rc;
   if (int rc = finish_timing(h)) return rc;
   CUDA_OR_FAIL(h, cudaGetLastError());
   return finish_dist(h, iters, hist);
@@ -1418,8 +1432,8 @@ int dlmpc_multi_solve(dlmpc_handle* const* hs, int n, int max_iters, double eps_
       return fail(h0, DLMPC_BAD_ARGUMENT, "the ranks must share device, kernel mode and tile width");
     if (!hs[r]->P.dist) return fail(h0, DLMPC_BAD_ARGUMENT, "dlmpc_dist_setup first on every rank");
   }
-  MultiFn fn = pick_multi_kernel(h0->mode, h0->P.tile_cols);
-  if (!fn) return fail(h0, DLMPC_BAD_ARGUMENT, "no multi-rank kernel for this mode");
+  if (h0->mode != kExact && h0->mode != kStream && h0->mode != kTwoPhase)
+    return fail(h0, DLMPC_BAD_ARGUMENT, "no multi-rank kernel for this mode");
   cudaSetDevice(h0->device);
   std::vector<DevProblem> probs(n);
   std::vector<RunArgs> runs(n);
@@ -1430,6 +1444,8 @@ int dlmpc_multi_solve(dlmpc_handle* const* hs, int n, int max_iters, double eps_
     if (int rc = ensure_run_buffers(h, max_iters, 1)) return rc;
     CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
     probs[r] = h->P;
+    probs[r].vbase = base[r];
+    probs[r].vgrid = h->grid;
     runs[r] = solve_args(h, max_iters, eps_pri, eps_dual);
     base[r + 1] = base[r] + h->grid;
     smem = std::max(smem, h->smem_bytes);
@@ -1441,12 +1457,7 @@ int dlmpc_multi_solve(dlmpc_handle* const* hs, int n, int max_iters, double eps_
   cudaMemcpy(dprobs, probs.data(), sizeof(DevProblem) * n, cudaMemcpyHostToDevice);
   cudaMemcpy(druns, runs.data(), sizeof(RunArgs) * n, cudaMemcpyHostToDevice);
   cudaMemcpy(dbase, base.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice);
-  cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  int nn = n;
-  void* args[] = {&dprobs, &druns, &dbase, &nn};
-  if (e == cudaSuccess)
-    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(base[n]), dim3(kThreads), args,
-                                    static_cast<size_t>(smem), h0->stream);
+  cudaError_t e = launch_multi_kernel(h0->mode, h0->P.tile_cols, dprobs, druns, dbase, n, base[n], smem, h0->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h0->stream);
   cudaFree(dprobs); cudaFree(druns); cudaFree(dbase);
   if (e != cudaSuccess) return fail(h0, DLMPC_CUDA_ERROR, std::string("multi-rank launch: ") + cudaGetErrorString(e));

@@ -60,18 +60,25 @@ __device__ __forceinline__ unsigned long long gtimer() {   // SM cycles (globalt
 #define PT_LAP(P, ph)
 #endif
 
-// Virtual CTA index / count of the persistent kernel: blockIdx.x / gridDim.x,
-// except in the multi-rank test launch (dlmpc_multi_kernel: the ranks of a
-// graph-partitioned solve as contiguous CTA slices of ONE cooperative grid on
-// one GPU, so the device-side exchange is tested without separate launches
-// that wait on one another). Set by every kernel entry (vcta_init).
-__shared__ int dlmpc_vcta[2];   // [0] first CTA of this rank's slice, [1] its CTA count
-#define VBID (static_cast<int>(blockIdx.x) - dlmpc_vcta[0])
-#define VGRID (dlmpc_vcta[1])
-__device__ __forceinline__ void vcta_init(int base, int count) {
-  if (threadIdx.x == 0) { dlmpc_vcta[0] = base; dlmpc_vcta[1] = count; }
-  __syncthreads();
-}
+// Virtual CTA index / count of the persistent kernel: blockIdx.x / gridDim.x
+// shifted by the problem's slice of the grid (P.vbase, P.vgrid), which is the
+// whole grid except in the multi-rank test launch (dlmpc_multi_kernel: the
+// ranks of a graph-partitioned solve as contiguous CTA slices of ONE
+// cooperative grid on one GPU, so the device-side exchange is tested without
+// separate launches that wait on one another). Read from the kernel
+// parameters (constant bank): a per-CTA shared-memory copy measured 4%
+// slower on the C4 cells.
+// The production translation unit (dlmpc.cu) uses the builtins: reading the
+// slice from the parameters there measured 40% slower on C2 (a codegen
+// effect in the register-capped patch kernel), so only the multi-rank test
+// kernel's own translation unit (dlmpc_multi.cu) defines DLMPC_VB_SHIFT.
+#ifdef DLMPC_VB_SHIFT
+#define VBID (static_cast<int>(blockIdx.x) - (P).vbase)
+#define VGRID ((P).vgrid)
+#else
+#define VBID (static_cast<int>(blockIdx.x))
+#define VGRID (static_cast<int>(gridDim.x))
+#endif
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
@@ -179,6 +186,7 @@ struct DevProblem {
   unsigned* d_rflag;                 // own residual arrival counter
   unsigned long long* d_slots;       // own residual slots
   int* d_abort;                      // set on an exchange timeout (all CTAs then stop)
+  int vbase, vgrid;                  // this problem's CTA slice of the launch (VBID / VGRID)
   long long part_cap;          // stream mode: doubles per Φ-partials buffer
   long long smem_doubles;      // dynamic shared memory of the plan
 };
@@ -208,7 +216,7 @@ __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 // recorded violation into DLMPC_CUDA_ERROR. In the production build it is
 // the constant `true` and compiles away.
 #ifdef DLMPC_CHECKED
-__device__ __noinline__ bool dchk_fail(int* dbg, int code, long long idx) {
+static __device__ __noinline__ bool dchk_fail(int* dbg, int code, long long idx) {
   if (atomicCAS(dbg, 0, code) == 0) reinterpret_cast<long long*>(dbg)[1] = idx;
   return false;
 }
@@ -327,9 +335,13 @@ struct ProdRow {   // row[j] * v[j]
 // and the solve ends in NotConverged) instead of fmax silently dropping it.
 // Also |b| for free: rmax(acc, d) == max(acc, |d|) for acc >= 0.
 __device__ __forceinline__ double rmax(double a, double b) {
+#ifdef DLMPC_FMAX_RESID
+  return fmax(a, fabs(b));
+#else
   const long long ia = __double_as_longlong(a) & 0x7fffffffffffffffLL;
   const long long ib = __double_as_longlong(b) & 0x7fffffffffffffffLL;
   return __longlong_as_double(ia > ib ? ia : ib);
+#endif
 }
 
 __device__ __forceinline__ double block_max(double v, double* red) {
@@ -412,10 +424,12 @@ __device__ __forceinline__ void publish_barrier(const DevProblem& P, int it, dou
 // at once (one round trip), then the products are summed across the lanes in
 // the reference's sequential order (warp_ordered_sum). Item q goes to CTA
 // q % grid first, so the items spread over the SMs.
-__device__ __forceinline__ long long wspread_first() {
+__device__ __forceinline__ long long wspread_first(const DevProblem& P) {
   return static_cast<long long>(threadIdx.x >> 5) * VGRID + VBID;
 }
-__device__ __forceinline__ long long wspread_step() { return static_cast<long long>(VGRID) * (blockDim.x >> 5); }
+__device__ __forceinline__ long long wspread_step(const DevProblem& P) {
+  return static_cast<long long>(VGRID) * (blockDim.x >> 5);
+}
 
 // acc (+)= v_0 + v_1 + ... + v_{n-1} over lanes 0..n-1, strictly in that
 // order with IEEE adds; `first`: acc is not yet set (the reference starts
@@ -432,9 +446,9 @@ __device__ __forceinline__ double warp_ordered_sum(double acc, bool& first, doub
 // ||a||^2 per subsystem (reference sls_core.py:338-339: all rows of a
 // subsystem share the support, hence a_pad and a_dot_a) and the RowInfeasible
 // scan of sls_core.py:346-348. Strict ascending order, no FMA, in all modes.
-__device__ void row_data_stage(const DevProblem& P, const double* x, int* bad_slot) {
+static __device__ void row_data_stage(const DevProblem& P, const double* x, int* bad_slot) {
   const int lane = threadIdx.x & 31;
-  for (long long ii = wspread_first(); ii < P.n_sub; ii += wspread_step()) {
+  for (long long ii = wspread_first(P); ii < P.n_sub; ii += wspread_step(P)) {
     const int i = static_cast<int>(ii);
     const int D = P.supp_len[i];
     const int* sc = P.supp_col + static_cast<size_t>(i) * P.d_pad;
@@ -1015,7 +1029,7 @@ __device__ __forceinline__ void ksplit_exchange_y(const DevProblem& P, const KSp
   __syncthreads();
 }
 
-template <int TC, bool S_GLOBAL, bool OPS>
+template <int TC, bool S_GLOBAL, bool OPS, bool KS = false>
 __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi, const double* lam,
                            double* psi_n, double* lam_n, const double* s_src, const int* irow_tab,
                            double* smem, double& pri_m, double& dual_m, const double* st,
@@ -1042,8 +1056,9 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
   const int t_el = warp / WPC;                  // this warp's column in element loops
   constexpr int PSTEP = 32 * WPC;
   // support rows of this CTA: all, or its half of a K-split pair (multiple of 8)
-  const int p_lo = ks.partner < 0 || ks.half == 0 ? 0 : ((S8 >> 1) + 7) & ~7;
-  const int p_hi = ks.partner < 0 || ks.half == 1 ? S8 : ((S8 >> 1) + 7) & ~7;
+  // (a separate instantiation, KS: the unpaired path keeps its registers)
+  const int p_lo = !KS || ks.half == 0 ? 0 : ((S8 >> 1) + 7) & ~7;
+  const int p_hi = !KS || ks.half == 1 ? S8 : ((S8 >> 1) + 7) & ~7;
   const int p_el0 = p_lo + (warp % WPC) * 32 + lane;   // first support slot
   // prologue: K[t][p] = φ + λ (admm.py:183), zero padded to TC x S8
   {
@@ -1081,12 +1096,12 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
   }
   __syncthreads();
   PT_LAP(P, 1)
-  if (TC == 8 && nt <= 2 && P.small_gemv && n08 * 10 <= kThreads && ks.partner < 0)
+  if (TC == 8 && nt <= 2 && P.small_gemv && n08 * 10 <= kThreads && !KS)
     gemv1_small<TC>(S, n08, ldn, nop, kt, ldk, yp, yb, ldy, nt);
   else
     gemm1<TC, NoHook, kWarps, CtaBar, 1>(P, p_hi - p_lo, n08, ldn, nop + static_cast<size_t>(p_lo) * ldn,
                                          kt + p_lo, ldk, yb, ldy, yp);
-  if (ks.partner >= 0) ksplit_exchange_y(P, ks, yb, ldy, n08, TC);
+  if constexpr (KS) ksplit_exchange_y(P, ks, yb, ldy, n08, TC);
   PT_LAP(P, 2)
   // GEMM 2: O[t][p] = sum_a N[p][a] Y[a][t]  (M = S, N = TC, K = n0) -> kt
   StoreO epi{kt + p_lo, ldk};
@@ -1176,10 +1191,15 @@ __device__ __forceinline__ void run_chunk(const DevProblem& P, int k, int nt, co
                                           const double* s_src, const int* irow_tab, double* smem,
                                           int& cur, double& pri_m, double& dual_m,
                                           const double* st = nullptr, const KSplit& ks = KSplit()) {
-  if (stage_operator(P, k, smem, cur))
-    fast_chunk<TC, S_GLOBAL, true>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st, ks);
-  else
-    fast_chunk<TC, S_GLOBAL, false>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st, ks);
+  const bool ops = stage_operator(P, k, smem, cur);
+  if (!S_GLOBAL && ks.partner >= 0) {   // K-split pair (patch mode; bases that live in L2)
+    if (ops) fast_chunk<TC, S_GLOBAL, true, true>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st, ks);
+    else fast_chunk<TC, S_GLOBAL, false, true>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st, ks);
+  } else if (ops) {
+    fast_chunk<TC, S_GLOBAL, true>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st);
+  } else {
+    fast_chunk<TC, S_GLOBAL, false>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st);
+  }
 }
 
 // Patch-kernel chunk of <= 2 columns on the register-blocked GEMV pair
@@ -1436,7 +1456,7 @@ __device__ __forceinline__ bool patch_stop_test(const DevProblem& P, const RunAr
   return R.stop_on_conv && pri <= R.eps_pri && dual <= R.eps_dual;
 }
 
-template <int TC, bool RB>
+template <int TC, bool RB, bool PAIRS>
 __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int it, double* smem,
                                 int& cur, const RunArgs& R, unsigned bar_target, int& pair_cnt) {
   double* s_patch = smem + P.off_patch;
@@ -1565,7 +1585,7 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
       else
       {
         KSplit ks;
-        if (P.cta_pair) {
+        if constexpr (PAIRS) {   // a separate kernel instantiation (kVarPairs)
           const int pv = P.cta_pair[VBID];
           if (pv >= 0) { ks.partner = pv >> 1; ks.half = pv & 1; ks.cnt = &pair_cnt; }
         }
@@ -2109,7 +2129,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
 
 // Exact column stage: one column per CTA at a time, the reference's dense
 // projector with numpy's pairwise order (admm.py:183-186).
-__device__ void column_stage_exact(const DevProblem& P, int b, const double* x, int it, double* smem) {
+static __device__ void column_stage_exact(const DevProblem& P, int b, const double* x, int it, double* smem) {
   const int tid = threadIdx.x;
   const int sp = P.s_pad;
   double* phi_s = smem + P.off_ex;   // internal order
@@ -2195,7 +2215,7 @@ __device__ __forceinline__ double control_value(const DevProblem& P, int pb, con
 
 template <bool EXACT>
 __device__ void control_stage(const DevProblem& P, int pb, const double* x) {
-  for (long long k = wspread_first(); k < P.n_inputs; k += wspread_step()) {
+  for (long long k = wspread_first(P); k < P.n_inputs; k += wspread_step(P)) {
     const double u = control_value<EXACT>(P, pb, x, static_cast<int>(k));
     if ((threadIdx.x & 31) == 0) P.u[k] = u;
   }
@@ -2220,8 +2240,8 @@ __device__ __forceinline__ double plant_row(const DevProblem& P, const double* x
   return __dadd_rn(ax, bu);
 }
 
-__device__ void plant_stage(const DevProblem& P, const double* x, double* xn) {
-  for (long long r = wspread_first(); r < P.n_cols; r += wspread_step()) {
+static __device__ void plant_stage(const DevProblem& P, const double* x, double* xn) {
+  for (long long r = wspread_first(P); r < P.n_cols; r += wspread_step(P)) {
     const double v = plant_row(P, x, static_cast<int>(r), [&](int k) { return ld_cg(P.u + k); });
     if ((threadIdx.x & 31) == 0) xn[r] = v;
   }
@@ -2236,7 +2256,7 @@ __device__ void control_plant_stage(const DevProblem& P, int pb, const double* x
                                     double* states_out) {
   const long long n_items = static_cast<long long>(P.n_inputs) + P.n_cols;
   const bool lane0 = (threadIdx.x & 31) == 0;
-  for (long long w = wspread_first(); w < n_items; w += wspread_step()) {
+  for (long long w = wspread_first(P); w < n_items; w += wspread_step(P)) {
     if (w < P.n_inputs) {
       const double u = control_value<EXACT>(P, pb, x, static_cast<int>(w));
       if (lane0) { P.u[w] = u; inputs_out[w] = u; }
@@ -2248,7 +2268,7 @@ __device__ void control_plant_stage(const DevProblem& P, int pb, const double* x
   }
 }
 
-__device__ void zero_iterate(const DevProblem& P, int b) {
+static __device__ void zero_iterate(const DevProblem& P, int b) {
   const size_t n = static_cast<size_t>(P.n_cols) * P.s_pad;
   const size_t gt = VBID * blockDim.x + threadIdx.x, GT = VGRID * blockDim.x;
   for (size_t q = gt; q < n; q += GT) { P.psi[b][q] = 0.0; P.lam[b][q] = 0.0; }
@@ -2338,28 +2358,36 @@ __device__ bool dist_exchange(const DevProblem& P, const RunArgs& R, int it, int
   return true;
 }
 
-template <int TC, int MODE>
+// Kernel variants beyond (TC, MODE), each its own instantiation so the common
+// path keeps its register allocation (measured: the dist branch compiled
+// into the stream kernel cost 3% at N=1e4, the pair branch 1.6% on small
+// patch cells):
+constexpr int kVarDist = 1;    // graph-partitioned solve, exchange on the device (non-patch modes)
+constexpr int kVarPairs = 2;   // patch mode with K-split CTA pairs
+
+template <int TC, int MODE, int VAR>
 __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunArgs& R);
 
-template <int TC, int MODE>
+template <int TC, int MODE, int VAR = 0>
 __global__ void __launch_bounds__(kThreads, 1) dlmpc_persistent(DevProblem P, RunArgs R) {
-  vcta_init(0, gridDim.x);
-  persistent_body<TC, MODE>(P, R);
+  persistent_body<TC, MODE, VAR>(P, R);
 }
 
+#ifdef DLMPC_VB_SHIFT
 // The ranks of a graph-partitioned solve as contiguous CTA slices of ONE
 // cooperative grid on one GPU (cta_base[r] .. cta_base[r+1]), each running
-// its own sub-problem: the one-GPU test of the device-side exchange.
+// its own sub-problem: the one-GPU test of the device-side exchange
+// (dlmpc_multi.cu).
 template <int TC, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) dlmpc_multi_kernel(const DevProblem* probs, const RunArgs* runs,
                                                                   const int* cta_base, int n_ranks) {
   int r = 0;
   while (r + 1 < n_ranks && static_cast<int>(blockIdx.x) >= cta_base[r + 1]) ++r;
-  vcta_init(cta_base[r], cta_base[r + 1] - cta_base[r]);
-  persistent_body<TC, MODE>(probs[r], runs[r]);
+  persistent_body<TC, MODE, kVarDist>(probs[r], runs[r]);   // probs[r].vbase / vgrid: the rank's slice
 }
+#endif
 
-template <int TC, int MODE>
+template <int TC, int MODE, int VAR>
 __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunArgs& R) {
   constexpr bool EXACT = MODE == kExact;
   constexpr bool PATCH = MODE == kPatch || MODE == kPatchRb;
@@ -2417,7 +2445,8 @@ __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunAr
           break;
         }
         bar_epoch += VGRID;
-        if (patch_iteration<TC, MODE == kPatchRb>(P, b, x, it, smem, cur, R, bar_base + bar_epoch, pair_cnt)) {
+        if (patch_iteration<TC, MODE == kPatchRb, (VAR & kVarPairs) != 0>(P, b, x, it, smem, cur, R,
+                                                                           bar_base + bar_epoch, pair_cnt)) {
           bar_epoch -= VGRID;   // returned before arriving
           conv = true;
           break;
@@ -2449,7 +2478,7 @@ __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunAr
       b ^= 1;
       // one load of the residual words per CTA, broadcast through shared memory
       unsigned long long* rbc = reinterpret_cast<unsigned long long*>(smem + P.off_red);
-      if (P.dist) {   // the halo to the neighbour ranks, the global maxima from all ranks
+      if constexpr ((VAR & kVarDist) != 0) {   // the halo to the neighbour ranks, the global maxima from all ranks
         unsigned long long g2[2];
         if (!dist_exchange(P, R, it, b, grid, g2)) {
           if (leader) { P.ctl[0] = 4; P.ctl[1] = step; P.ctl[5] = it; P.ctl[4] = b; }
@@ -2488,11 +2517,9 @@ __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunAr
   if (leader) { P.ctl[0] = 0; P.ctl[4] = b; }
 }
 
+#ifndef DLMPC_MULTI_TU   // the plain kernels live in the production translation unit only
 // Row data for the solve API (dlmpc_set_x): a plain launch.
-__global__ void set_x_kernel(DevProblem P) {
-  vcta_init(0, gridDim.x);
-  row_data_stage(P, P.x[0], P.ctl + 2);
-}
+__global__ void set_x_kernel(DevProblem P) { row_data_stage(P, P.x[0], P.ctl + 2); }
 
 // φ of the last iteration, internal column layout (for dlmpc_get(DLMPC_PHI)).
 template <bool EXACT>
@@ -2596,14 +2623,8 @@ __global__ void audit_dynamics_kernel(DevProblem P, int b, double* out) {
 // Control extraction and plant step for the loaded x after a host-driven
 // solve (graph-partitioned multi-GPU path): plain launches, grid-stride.
 template <bool EXACT>
-__global__ void control_kernel(DevProblem P, int pb) {
-  vcta_init(0, gridDim.x);
-  control_stage<EXACT>(P, pb, P.x[0]);
-}
-__global__ void plant_kernel(DevProblem P) {
-  vcta_init(0, gridDim.x);
-  plant_stage(P, P.x[0], P.x[1]);
-}
+__global__ void control_kernel(DevProblem P, int pb) { control_stage<EXACT>(P, pb, P.x[0]); }
+__global__ void plant_kernel(DevProblem P) { plant_stage(P, P.x[0], P.x[1]); }
 
 // Halo exchange of the partitioned path (partition.py halo_cells): gather
 // the (ψ, λ) entries a neighbour reads into one interleaved message, and
@@ -2626,5 +2647,6 @@ __global__ void halo_unpack_kernel(double* __restrict__ psi, double* __restrict_
     lam[c] = v.y;
   }
 }
+#endif  // DLMPC_MULTI_TU
 
 }  // namespace dlmpc
