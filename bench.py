@@ -402,13 +402,26 @@ def partitioned_c5(pb, dist, local, solves=2):
         return {"error": err or "setup failed on another rank"}
     try:
         plans = plan_partition(mask, world)
-        ex = DeviceExchangeRank(system, spec, mask, "b200", plans=plans)
+        ex = DeviceExchangeRank(system, spec, mask, "b200", plans=plans)   # raises on every rank on failure
         setup_s = time.perf_counter() - t0
-        n, _, conv = ex.solve(x0, True)                       # warm-up solve
-        ms, its = 0.0, 0
+        def solve_agreed():
+            # every rank reaches the agreement even if its own solve failed
+            # (the kernel's exchange waits are bounded, so no rank hangs)
+            try:
+                n, _, conv = ex.solve(x0, True)
+                ok = True
+            except Exception as exc:   # noqa: BLE001 -- reported in the line
+                n, conv, ok = 0, False, False
+                ex.err = repr(exc)[:300]
+            if not ex.agree(ok):
+                raise RuntimeError(getattr(ex, "err", None) or "partitioned solve failed on another rank")
+            return n, conv
+
+        solve_agreed()                                        # warm-up solve
+        ms, its, conv = 0.0, 0, True
         for _ in range(solves):
-            dist.barrier()
-            n, _, conv = ex.solve(x0, True)
+            n, c = solve_agreed()
+            conv = conv and c
             ms += ex.rk.session.last_timing()[0]
             its += n
         t = torch.tensor([its, ms, setup_s, one_ms, one_its, 0.0 if conv else 1.0], dtype=torch.float64,

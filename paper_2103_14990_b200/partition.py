@@ -520,31 +520,55 @@ class DeviceExchangeRank:
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         self.dev = torch.cuda.current_device()
         self.plans = plans if plans is not None else plan_partition(mask, self.world)
-        self.rk = rk = RankSolver(system, spec, mask, self.plans, self.rank, strategy, self.dev,
-                                  device_exchange=True)
         self._opened = []
-        bufs = rk.session.dist_alloc(self.world)
-        mine = {"ipc": [ipc_handle(p) for p in bufs], "grid": rk.session.info()["grid"],
-                "recv_from": list(rk.recv_from), "recv_cells": [np.asarray(c) for c in rk.recv_cells]}
+        self.rk = rk = None
+        # every step below is followed by an agreement on success, so a
+        # failure on one rank makes every rank raise instead of leaving the
+        # others waiting in a collective or in the kernel's arrival counters
+        err = None
+        try:
+            self.rk = rk = RankSolver(system, spec, mask, self.plans, self.rank, strategy, self.dev,
+                                      device_exchange=True)
+            bufs = rk.session.dist_alloc(self.world)
+            mine = {"ipc": [ipc_handle(p) for p in bufs], "grid": rk.session.info()["grid"],
+                    "recv_from": list(rk.recv_from), "recv_cells": [np.asarray(c) for c in rk.recv_cells]}
+        except Exception as exc:   # noqa: BLE001 -- agreed on below
+            err, mine = exc, None
         infos = [None] * self.world
         dist.all_gather_object(infos, mine, group=group)
-        all_bufs = []
-        for q in range(self.world):
-            if q == self.rank:
-                all_bufs.append(bufs)
-            else:
-                ptrs = [ipc_open(h, self.dev) for h in infos[q]["ipc"]]
-                self._opened.extend(ptrs)
-                all_bufs.append(ptrs)
-        src, dst, peer = [], [], []
-        for k, q in enumerate(rk.send_to):
-            b = infos[q]["recv_cells"][infos[q]["recv_from"].index(self.rank)]
-            src.append(rk.send_cells[k]); dst.append(b); peer.append(np.full(b.size, k, dtype=np.int32))
-        cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(0, dt)
-        rk.session.dist_setup(self.rank, self.world, cat(src, np.int64), cat(dst, np.int64), cat(peer, np.int32),
-                              [all_bufs[q] for q in rk.send_to], sum(infos[q]["grid"] for q in rk.recv_from),
-                              all_bufs)
-        dist.barrier(group=group)   # every rank's counters exist before the first push
+        if err is None and any(i is None for i in infos):
+            err = RuntimeError("device exchange: another rank failed to allocate")
+        if err is None:
+            try:
+                all_bufs = []
+                for q in range(self.world):
+                    if q == self.rank:
+                        all_bufs.append(bufs)
+                    else:
+                        ptrs = [ipc_open(h, self.dev) for h in infos[q]["ipc"]]
+                        self._opened.extend(ptrs)
+                        all_bufs.append(ptrs)
+                src, dst, peer = [], [], []
+                for k, q in enumerate(rk.send_to):
+                    b = infos[q]["recv_cells"][infos[q]["recv_from"].index(self.rank)]
+                    src.append(rk.send_cells[k]); dst.append(b); peer.append(np.full(b.size, k, dtype=np.int32))
+                cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(0, dt)
+                rk.session.dist_setup(self.rank, self.world, cat(src, np.int64), cat(dst, np.int64),
+                                      cat(peer, np.int32), [all_bufs[q] for q in rk.send_to],
+                                      sum(infos[q]["grid"] for q in rk.recv_from), all_bufs)
+            except Exception as exc:   # noqa: BLE001 -- agreed on below
+                err = exc
+        if not self.agree(err is None):   # also the barrier: every rank's counters exist before the first push
+            self.close()
+            raise err if err is not None else RuntimeError("device exchange: setup failed on another rank")
+
+    def agree(self, ok: bool) -> bool:
+        """All ranks' verdict (logical and), a collective every rank reaches."""
+        import torch
+        dev = torch.device("cuda", self.dev) if self.dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+        t = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return bool(t.item() >= 1.0)
 
     def solve(self, x, cold):
         """One MPC step's solve -> (iterations, history, converged)."""
@@ -556,7 +580,9 @@ class DeviceExchangeRank:
         for p in self._opened:
             ipc_close(p)
         self._opened = []
-        self.rk.close()
+        if self.rk is not None:
+            self.rk.close()
+            self.rk = None
 
 
 def simulate_partitioned_device(system, spec, mask, x0, t_sim, strategy="b200", warm_start=True, group=None):
