@@ -294,33 +294,71 @@ __device__ __forceinline__ double make_phi(double v, double s, double xc) {
 
 // numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
 // pairwise_sum_DOUBLE) of rounded products f(i); the reference's Ψ
-// reductions `.sum(axis=2)` (admm.py:184, 186) use it.
+// reductions `.sum(axis=2)` (admm.py:184, 186) use it. Blocks of <= 128 are
+// the 8-accumulator leaf; longer ranges split at n/2 rounded down to a
+// multiple of 8 and add the two halves.
 template <class F>
-__device__ double pairwise_sum(const F& f, int lo, int n) {
+__device__ __forceinline__ double pairwise_leaf(const F& f, int lo, int n) {
   if (n < 8) {
     double r = 0.0;
     for (int i = 0; i < n; ++i) r = __dadd_rn(r, f(lo + i));
     return r;
   }
-  if (n <= 128) {
-    double r0 = f(lo), r1 = f(lo + 1), r2 = f(lo + 2), r3 = f(lo + 3);
-    double r4 = f(lo + 4), r5 = f(lo + 5), r6 = f(lo + 6), r7 = f(lo + 7);
-    int i = 8;
-    const int stop = n - (n % 8);
-    for (; i < stop; i += 8) {
-      r0 = __dadd_rn(r0, f(lo + i));     r1 = __dadd_rn(r1, f(lo + i + 1));
-      r2 = __dadd_rn(r2, f(lo + i + 2)); r3 = __dadd_rn(r3, f(lo + i + 3));
-      r4 = __dadd_rn(r4, f(lo + i + 4)); r5 = __dadd_rn(r5, f(lo + i + 5));
-      r6 = __dadd_rn(r6, f(lo + i + 6)); r7 = __dadd_rn(r7, f(lo + i + 7));
-    }
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
-                           __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
-    for (; i < n; ++i) res = __dadd_rn(res, f(lo + i));
-    return res;
+  double r0 = f(lo), r1 = f(lo + 1), r2 = f(lo + 2), r3 = f(lo + 3);
+  double r4 = f(lo + 4), r5 = f(lo + 5), r6 = f(lo + 6), r7 = f(lo + 7);
+  int i = 8;
+  const int stop = n - (n % 8);
+  for (; i < stop; i += 8) {
+    r0 = __dadd_rn(r0, f(lo + i));     r1 = __dadd_rn(r1, f(lo + i + 1));
+    r2 = __dadd_rn(r2, f(lo + i + 2)); r3 = __dadd_rn(r3, f(lo + i + 3));
+    r4 = __dadd_rn(r4, f(lo + i + 4)); r5 = __dadd_rn(r5, f(lo + i + 5));
+    r6 = __dadd_rn(r6, f(lo + i + 6)); r7 = __dadd_rn(r7, f(lo + i + 7));
   }
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(pairwise_sum(f, lo, n2), pairwise_sum(f, lo + n2, n - n2));
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < n; ++i) res = __dadd_rn(res, f(lo + i));
+  return res;
+}
+
+// The recursion as an explicit post-order walk (no device recursion: its
+// stack depth is not statically bounded, and n >= ~900 -- the d=5, T=30
+// supports -- overflowed the default per-thread stack). Depth <= 24 covers
+// n < 128 * 2^23.
+template <class F>
+__device__ double pairwise_sum(const F& f, int lo, int n) {
+  if (n <= 128) return pairwise_leaf(f, lo, n);
+  int st_lo[24], st_n[24];
+  double st_left[24];
+  bool st_right[24];
+  int top = 0;
+  st_lo[0] = lo; st_n[0] = n; st_right[0] = false;
+  double ret = 0.0;
+  for (;;) {
+    const int cl = st_lo[top], cn = st_n[top];
+    if (cn > 128 && !st_right[top]) {   // descend into the left half
+      int n2 = cn / 2;
+      n2 -= n2 % 8;
+      st_right[top] = true;
+      ++top;
+      st_lo[top] = cl; st_n[top] = n2; st_right[top] = false;
+      continue;
+    }
+    ret = pairwise_leaf(f, cl, cn);     // a leaf: unwind
+    for (;;) {
+      if (top == 0) return ret;
+      --top;
+      const int pn = st_n[top];
+      int n2 = pn / 2;
+      n2 -= n2 % 8;
+      if (st_lo[top + 1] == st_lo[top]) {   // came back from the left half: start the right one
+        st_left[top] = ret;
+        ++top;
+        st_lo[top] = st_lo[top - 1] + n2; st_n[top] = pn - n2; st_right[top] = false;
+        break;
+      }
+      ret = __dadd_rn(st_left[top], ret);   // came back from the right half: combine
+    }
+  }
 }
 
 struct ProdRow {   // row[j] * v[j]
@@ -2152,10 +2190,12 @@ static __device__ void column_stage_exact(const DevProblem& P, int b, const doub
     const double* rhs = P.rhs_pool + static_cast<size_t>(P.col_vec[c]) * P.m_pad;
     const int* rp = P.ref_pos + static_cast<size_t>(owner) * sp;
     const double xc = ld_cg(x + c);
+    if (!DCHK(P, S <= sp && m <= P.m_pad && k >= 0 && k < P.n_classes, 20, c)) continue;
     for (int p = tid; p < S; p += kThreads) {
       const size_t pos = static_cast<size_t>(c) * sp + p;
       const double ps = ld_cg(psi + pos), lm = ld_cg(lam + pos);
       const long long ir = P.contiguous ? P.col_rowbase[c] + p : P.col_irow[static_cast<size_t>(owner) * sp + p];
+      if (!DCHK_ROW(P, ir, 21) || !DCHK(P, rp[p] >= 0 && rp[p] < S, 22, p)) continue;
       phi_s[p] = make_phi<true>(__dsub_rn(ps, lm), ld_cg(P.s_row + ir), xc);
       lam_s[p] = lm;
       psi_s[p] = ps;
