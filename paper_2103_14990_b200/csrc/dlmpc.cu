@@ -1454,10 +1454,11 @@ int dlmpc_multi_solve(dlmpc_handle* const* hs, int n, int max_iters, double eps_
   CUDA_OR_FAIL(h0, cudaMalloc(&dprobs, sizeof(DevProblem) * n));
   CUDA_OR_FAIL(h0, cudaMalloc(&druns, sizeof(RunArgs) * n));
   CUDA_OR_FAIL(h0, cudaMalloc(&dbase, sizeof(int) * (n + 1)));
-  cudaMemcpy(dprobs, probs.data(), sizeof(DevProblem) * n, cudaMemcpyHostToDevice);
-  cudaMemcpy(druns, runs.data(), sizeof(RunArgs) * n, cudaMemcpyHostToDevice);
-  cudaMemcpy(dbase, base.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice);
-  cudaError_t e = launch_multi_kernel(h0->mode, h0->P.tile_cols, dprobs, druns, dbase, n, base[n], smem, h0->stream);
+  cudaError_t e = cudaMemcpy(dprobs, probs.data(), sizeof(DevProblem) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(druns, runs.data(), sizeof(RunArgs) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dbase, base.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = launch_multi_kernel(h0->mode, h0->P.tile_cols, dprobs, druns, dbase, n, base[n], smem, h0->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h0->stream);
   cudaFree(dprobs); cudaFree(druns); cudaFree(dbase);
   if (e != cudaSuccess) return fail(h0, DLMPC_CUDA_ERROR, std::string("multi-rank launch: ") + cudaGetErrorString(e));
