@@ -248,6 +248,10 @@ int dlmpc_phase_times(dlmpc_handle* h, uint64_t* out, int reset);
 /* Shape info: n_rows, n_cols, s_pad, n_sub, grid CTAs, tile_cols, smem bytes,
  * kernel mode (0 patch, 1 two-phase, 2 exact, 3 stream), work units. */
 int dlmpc_info(const dlmpc_handle* h, int64_t* out9);
+/* Kernel plan flags, the first n of: Φ metadata cached per CTA, fused
+ * MPC-step transitions (closed loops), register-blocked GEMV pair, ψ/λ
+ * staging buffers, K-split CTA pairs. No reference counterpart. */
+int dlmpc_plan_flags(const dlmpc_handle* h, int64_t* out, int n);
 
 /* ------------------------------------------------------------------------
  * The reference's device schedules (strategies.py:44-314: naive, padded,

@@ -103,6 +103,8 @@ KernelFn pick_kernel(int mode, int tc, int rb = 0) {
 KernelFn pick_kernel_var(int mode, int tc, int var) {
   if (var == kVarPairs && mode == kPatch)
     return tc == 16 ? dlmpc_persistent<16, kPatch, kVarPairs> : dlmpc_persistent<8, kPatch, kVarPairs>;
+  if (var == kVarFuse && mode == kPatch) return tc == 16 ? dlmpc_persistent<16, kPatch, kVarFuse> : dlmpc_persistent<8, kPatch, kVarFuse>;
+  if (var == kVarFuse && mode == kPatchRb) return dlmpc_persistent<8, kPatchRb, kVarFuse>;
   if (var == kVarDist) {
     if (mode == kExact) return dlmpc_persistent<8, kExact, kVarDist>;
     if (mode == kStream) return tc == 16 ? dlmpc_persistent<16, kStream, kVarDist> : dlmpc_persistent<8, kStream, kVarDist>;
@@ -130,7 +132,8 @@ int ensure_run_buffers(dlmpc_handle* h, int max_iters, int t_sim) {
   if (max_iters > h->max_iters_cap) {
     double* hist = nullptr; unsigned long long* resid = nullptr;
     cudaError_t e = cudaMalloc(&hist, sizeof(double) * 2 * max_iters);
-    if (e == cudaSuccess) e = cudaMalloc(&resid, sizeof(unsigned long long) * 2 * max_iters);
+    // three regions of 2 * max_iters words (fused MPC-step transitions rotate over them)
+    if (e == cudaSuccess) e = cudaMalloc(&resid, sizeof(unsigned long long) * 6 * max_iters);
     if (e != cudaSuccess) {
       if (hist) cudaFree(hist);
       return fail(h, DLMPC_CUDA_ERROR, std::string("run buffers: ") + cudaGetErrorString(e));
@@ -160,7 +163,8 @@ int ensure_run_buffers(dlmpc_handle* h, int max_iters, int t_sim) {
 int launch(dlmpc_handle* h, const RunArgs& R, int var = 0) {
   KernelFn fn = pick_kernel(h->mode, h->P.tile_cols, h->P.rb_gemv);
   if (h->P.cta_pair && h->mode == kPatch) var |= kVarPairs;
-  if (var) fn = pick_kernel_var(h->mode, h->P.tile_cols, var);
+  if (h->P.fuse_steps && R.closed_loop && R.warm_start && R.t_sim > 1) var |= kVarFuse;
+  if (var) fn = pick_kernel_var(var == kVarFuse && h->P.rb_gemv ? kPatchRb : h->mode, h->P.tile_cols, var);
   if (!fn) return fail(h, DLMPC_BAD_ARGUMENT, "no kernel variant for this mode");
   // the shared-memory limit is a per-function attribute: sessions of one
   // instantiation with different plans (the ranks of a partitioned solve in
@@ -724,12 +728,120 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       }
       ch_cls.swap(nc_cls); ch_c0.swap(nc_c0); ch_n.swap(nc_n); u_chunk.swap(nu);
     }
+    // closed loops with the Φ cache of one unit per CTA: the MPC-step
+    // transition inside each CTA (fused_transition) over its window, from
+    // step-invariant tables (layout: FuseTab in dlmpc_device.cuh)
+    std::vector<int> ft_iptr(1, 0), ft_int, ft_dptr(1, 0);
+    std::vector<double> ft_dbl;
+    P.fuse_steps = 0;
+    {
+      // on by default for the register-blocked GEMV plans (C2-sized networks:
+      // measured +3.1% on the C2 closed loops; N=1000 d=3 T=10 even, N=300
+      // d=2 T=5 -2%: the fused kernel of the DMMA plans spills);
+      // DLMPC_FUSE_STEPS=1 forces it for any eligible plan, =0 disables it
+      const char* e = getenv("DLMPC_FUSE_STEPS");
+      const bool force = e && e[0] == '1', off_env = e && e[0] == '0';
+      const bool want = h->mode == kPatch && P.cache_phi && cta_pair.empty() && P.own_sub_lo == 0 &&
+                        P.own_sub_hi == pr->n_sub && pr->a_ptr && pr->b_ptr && !off_env &&
+                        (P.rb_gemv || force) &&
+                        (long long)pr->n_cols * pr->s_pad < INT_MAX && pr->row_start[pr->n_sub] < INT_MAX &&
+                        pr->n_cols < (1 << 29) && pr->n_inputs < (1 << 29);
+      if (want) {
+        long long imax = 0, dmax = 0, w2max = 0, wmax = 0, umax = 0;
+        std::vector<int> wl, ul, w2, blob;
+        std::vector<double> dbl;
+        auto idx = [](const std::vector<int>& v, int x) { return (int)(std::lower_bound(v.begin(), v.end(), x) - v.begin()); };
+        for (size_t u = 0; u < u_lo.size(); ++u) {
+          const int ulo = u_lo[u], uhi = u_hi[u];
+          wl.clear(); ul.clear(); w2.clear(); blob.assign(FuseTab::kHeader, 0); dbl.clear();
+          for (int i = p_lo[u]; i < p_hi[u]; ++i)
+            for (int k = 0; k < pr->supp_len[i]; ++k) wl.push_back(pr->supp_col[(size_t)i * pr->d_pad + k]);
+          std::sort(wl.begin(), wl.end());
+          wl.erase(std::unique(wl.begin(), wl.end()), wl.end());
+          for (int r : wl) {
+            for (int64_t q = pr->b_ptr[r]; q < pr->b_ptr[r + 1]; ++q) ul.push_back(pr->b_idx[q]);
+            for (int64_t q = pr->a_ptr[r]; q < pr->a_ptr[r + 1]; ++q) w2.push_back(pr->a_idx[q]);
+          }
+          for (int k = 0; k < pr->n_inputs; ++k)
+            if (pr->input_owner[k] >= ulo && pr->input_owner[k] < uhi) ul.push_back(k);
+          for (auto* v : {&ul, &w2}) { std::sort(v->begin(), v->end()); v->erase(std::unique(v->begin(), v->end()), v->end()); }
+          const int nw = (int)wl.size(), nu = (int)ul.size(), nw2 = (int)w2.size();
+          blob[FuseTab::kNw] = nw; blob[FuseTab::kNu] = nu; blob[FuseTab::kNw2] = nw2;
+          blob[FuseTab::kWcol] = (int)blob.size();      // window states: r * 2 + own
+          for (int r : wl) blob.push_back(r * 2 + (pr->col_owner[r] >= ulo && pr->col_owner[r] < uhi ? 1 : 0));
+          blob[FuseTab::kW2] = (int)blob.size();        // states whose x the window's A rows read
+          blob.insert(blob.end(), w2.begin(), w2.end());
+          blob[FuseTab::kSupp] = (int)blob.size();      // per patch-subsystem support slot: window index
+          for (int i = p_lo[u]; i < p_hi[u]; ++i)
+            for (int k = 0; k < pr->d_pad; ++k)
+              blob.push_back(k < pr->supp_len[i] ? idx(wl, pr->supp_col[(size_t)i * pr->d_pad + k]) : 0);
+          blob[FuseTab::kMx] = (int)blob.size();        // the single chunk's columns: window index
+          if (u_chunk[u + 1] - u_chunk[u] == 1)
+            for (int t = 0; t < ch_n[u_chunk[u]]; ++t) blob.push_back(idx(wl, ch_c0[u_chunk[u]] + t));
+          blob[FuseTab::kUhead] = (int)blob.size();     // per input: k * 2 + own, s_row index, support length, entry offset
+          const int uh = (int)blob.size();
+          blob.resize(blob.size() + 4 * (size_t)nu);
+          blob[FuseTab::kUent] = (int)blob.size();      // per support slot of an input's row: ψ/λ position, column
+          for (int j = 0; j < nu; ++j) {
+            const int k = ul[j], i = pr->input_owner[k], l = pr->input_local[k];
+            blob[uh + 4 * j] = k * 2 + (i >= ulo && i < uhi ? 1 : 0);
+            blob[uh + 4 * j + 1] = (int)(pr->row_start[i] + l);
+            blob[uh + 4 * j + 2] = pr->supp_len[i];
+            blob[uh + 4 * j + 3] = (int)blob.size() - blob[FuseTab::kUent];
+            for (int q = 0; q < pr->supp_len[i]; ++q) {
+              const size_t e2 = (size_t)i * pr->d_pad + q;
+              blob.push_back((int)((long long)pr->supp_col[e2] * pr->s_pad + pr->supp_off[e2] + l));
+              blob.push_back(pr->supp_col[e2]);
+            }
+          }
+          blob[FuseTab::kAoff] = (int)blob.size();      // per window state: A entries [aoff, aoff+1), B entries likewise
+          const int ao = (int)blob.size();
+          blob.resize(blob.size() + 2 * ((size_t)nw + 1));
+          blob[FuseTab::kAent] = (int)blob.size();      // A entry: index into W2 (values: doubles [0, na))
+          int na = 0;
+          for (int j = 0; j < nw; ++j) {
+            blob[ao + j] = na;
+            for (int64_t q = pr->a_ptr[wl[j]]; q < pr->a_ptr[wl[j] + 1]; ++q, ++na) {
+              blob.push_back(idx(w2, pr->a_idx[q])); dbl.push_back(pr->a_val[q]);
+            }
+          }
+          blob[ao + nw] = na;
+          blob[FuseTab::kBent] = (int)blob.size();      // B entry: index into U (values: doubles [na, na+nb))
+          int nb = 0;
+          for (int j = 0; j < nw; ++j) {
+            blob[ao + nw + 1 + j] = nb;
+            for (int64_t q = pr->b_ptr[wl[j]]; q < pr->b_ptr[wl[j] + 1]; ++q, ++nb) {
+              blob.push_back(idx(ul, pr->b_idx[q])); dbl.push_back(pr->b_val[q]);
+            }
+          }
+          blob[ao + 2 * nw + 1] = nb;
+          blob[FuseTab::kNa] = na;
+          blob[FuseTab::kNint] = (int)blob.size();
+          ft_int.insert(ft_int.end(), blob.begin(), blob.end());
+          ft_dbl.insert(ft_dbl.end(), dbl.begin(), dbl.end());
+          ft_iptr.push_back((int)ft_int.size()); ft_dptr.push_back((int)ft_dbl.size());
+          imax = std::max<long long>(imax, (long long)blob.size());
+          dmax = std::max<long long>(dmax, (long long)dbl.size());
+          w2max = std::max<long long>(w2max, nw2); wmax = std::max<long long>(wmax, nw); umax = std::max<long long>(umax, nu);
+        }
+        // shared memory: table doubles | x of W2 | x+ of W | u of U | row weights of the patch | table ints
+        const long long need = dmax + w2max + wmax + umax + prows_max + (imax + 1) / 2 + 2;
+        const long long off = (P.off_ex + 1) & ~1LL;
+        if (off + need <= limit) {
+          P.fuse_steps = 1;
+          P.off_fw = (int)off;
+          P.ft_dcap = (int)dmax; P.ft_w2cap = (int)w2max; P.ft_wcap = (int)wmax; P.ft_ucap = (int)umax;
+          P.off_ex = (int)(off + need);
+          h->smem_bytes = (int)(P.off_ex * 8);
+        }
+      }
+    }
     // patch mode, C2-sized networks: the register-blocked GEMV pair when every
     // chunk has <= 2 columns and every class operator fits its thread blocking
     // (measured on C2: GEMV pair 1.3 us vs 2.1 us for the DFMA GEMV + DMMA GEMM)
     if (getenv("DLMPC_DEBUG_PLAN"))
-      fprintf(stderr, "plan: mode %d tc %d stash %d opr %d split %d n08 %d ldy %d rb %d chunks %zu cache %d smem %d\n", h->mode,
-              P.tile_cols, P.stash_bufs, P.opr_cap, P.split_max, P.n08_max, P.ldy, P.rb_gemv, ch_n.size(), P.cache_phi, h->smem_bytes);
+      fprintf(stderr, "plan: mode %d tc %d stash %d opr %d split %d n08 %d ldy %d rb %d chunks %zu cache %d fuse %d smem %d\n", h->mode,
+              P.tile_cols, P.stash_bufs, P.opr_cap, P.split_max, P.n08_max, P.ldy, P.rb_gemv, ch_n.size(), P.cache_phi, P.fuse_steps, h->smem_bytes);
     if (h->mode == kPatch || h->mode == kStream) {
       int rc;
       if ((rc = upload(h, cta_ptr.data(), cta_ptr.size(), &P.cta_unit_ptr)) ||
@@ -743,6 +855,14 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
           (rc = upload(h, ch_n.data(), ch_n.size(), &P.chunk_n)))
         return rc;
       if (h->mode == kPatch && (rc = alloc(h, 1, &P.gbar))) return rc;
+      if (P.fuse_steps) {
+        if (ft_dbl.empty()) ft_dbl.push_back(0.0);
+        if ((rc = upload(h, ft_iptr.data(), ft_iptr.size(), &P.ft_iptr)) ||
+            (rc = upload(h, ft_int.data(), ft_int.size(), &P.ft_int)) ||
+            (rc = upload(h, ft_dptr.data(), ft_dptr.size(), &P.ft_dptr)) ||
+            (rc = upload(h, ft_dbl.data(), ft_dbl.size(), &P.ft_dbl)))
+          return rc;
+      }
       if (h->mode == kPatch && !cta_pair.empty()) {
         if ((rc = upload(h, cta_pair.data(), cta_pair.size(), &P.cta_pair)) ||
             (rc = alloc(h, (size_t)G, &P.pair_flag)) ||
@@ -1550,6 +1670,13 @@ int dlmpc_info(const dlmpc_handle* h, int64_t* out) {
   out[0] = h->P.n_rows; out[1] = h->P.n_cols; out[2] = h->P.s_pad; out[3] = h->P.n_sub;
   out[4] = h->grid; out[5] = h->P.tile_cols; out[6] = h->smem_bytes;
   out[7] = h->mode; out[8] = h->n_units;
+  return DLMPC_OK;
+}
+
+int dlmpc_plan_flags(const dlmpc_handle* h, int64_t* out, int n) {
+  if (!h || !out || n < 0) return DLMPC_BAD_ARGUMENT;
+  const int64_t v[5] = {h->P.cache_phi, h->P.fuse_steps, h->P.rb_gemv, h->P.stash_bufs, h->P.cta_pair ? 1 : 0};
+  for (int i = 0; i < n && i < 5; ++i) out[i] = v[i];
   return DLMPC_OK;
 }
 

@@ -189,6 +189,34 @@ struct DevProblem {
   int vbase, vgrid;                  // this problem's CTA slice of the launch (VBID / VGRID)
   long long part_cap;          // stream mode: doubles per Φ-partials buffer
   long long smem_doubles;      // dynamic shared memory of the plan
+  // patch mode, cached single unit: the closed loop's MPC-step transition
+  // inside each CTA, without grid barriers (fused_transition), from per-unit
+  // step-invariant tables (FuseTab) staged in shared memory at launch
+  int fuse_steps;
+  const int* ft_iptr; const int* ft_int;       // [n_units+1] offsets, int tables
+  const int* ft_dptr; const double* ft_dbl;    // [n_units+1] offsets, A / B values
+  int off_fw, ft_dcap, ft_w2cap, ft_wcap, ft_ucap;   // shared memory region and its section capacities
+};
+
+// A unit's window for fused_transition: W = the states of its patch
+// subsystems' supports, U = the inputs W's B rows reference plus the unit's
+// own inputs, W2 = the states W's A rows read (all ascending). Int table:
+// a header of offsets (kHeader ints), then the sections below; the double
+// table holds the A values (in CSR order, per W state) then the B values.
+struct FuseTab {
+  enum {
+    kNw, kNu, kNw2, kNa, kNint,
+    kWcol,    // [nw]     r * 2 + (r is an own state)
+    kW2,      // [nw2]    state
+    kSupp,    // [np * d_pad] window index of each patch-subsystem support slot
+    kMx,      // [nt]     window index of the single chunk's columns
+    kUhead,   // [nu][4]  k * 2 + own, s_row index, support length D, entry offset
+    kUent,    // [..][2]  per support slot of input k's row: ψ/λ position, column
+    kAoff,    // [nw+1]   A entries of W state j, then [nw+1] its B entries
+    kAent,    // [na]     W2 index
+    kBent,    // [nb]     U index
+    kHeader = 16
+  };
 };
 
 struct RunArgs {
@@ -432,8 +460,8 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 // has arrived `target` times in total (wrap-safe compare). One block barrier
 // less per iteration than publish_residuals + grid.sync(); the grid barrier
 // itself costs ~1.2 us either way on B200 (tools/microbench/barrier_bench.cu).
-__device__ __forceinline__ void publish_barrier(const DevProblem& P, int it, double pri_m, double dual_m,
-                                                double* red, unsigned target) {
+__device__ __forceinline__ void publish_barrier(const DevProblem& P, unsigned long long* rs, double pri_m,
+                                                double dual_m, double* red, unsigned target) {
   for (int o = 16; o > 0; o >>= 1) {
     pri_m = rmax(pri_m, __shfl_xor_sync(0xffffffffu, pri_m, o));
     dual_m = rmax(dual_m, __shfl_xor_sync(0xffffffffu, dual_m, o));
@@ -448,8 +476,8 @@ __device__ __forceinline__ void publish_barrier(const DevProblem& P, int it, dou
       d = rmax(d, __shfl_xor_sync(0xffffffffu, d, o));
     }
     if (lane == 0) {
-      atomicMax(P.resid + 2 * it, static_cast<unsigned long long>(__double_as_longlong(p)));
-      atomicMax(P.resid + 2 * it + 1, static_cast<unsigned long long>(__double_as_longlong(d)));
+      atomicMax(rs, static_cast<unsigned long long>(__double_as_longlong(p)));
+      atomicMax(rs + 1, static_cast<unsigned long long>(__double_as_longlong(d)));
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" :: "l"(P.gbar) : "memory");
       while (static_cast<int>(ld_acquire_u32(P.gbar) - target) < 0) {}
     }
@@ -1360,6 +1388,16 @@ __device__ void column_stage_tiles(const DevProblem& P, int b, const double* x, 
 // positions and lengths, row bounds, unit block, row info, the single
 // chunk's column positions); later steps refresh only what depends on x
 // (x of the supports and of the chunk's columns, 1/||a||², 1/(ρ + 2w·||a||²)).
+// The x-dependent scales of patch subsystem q's rows from its ||a||^2 (one
+// warp): 1/||a||^2 and 1/(ρ + 2w·||a||^2) per row (shared by cache_phi_meta
+// and fused_transition, so both produce the same bits).
+__device__ __forceinline__ void phi_cache_scales(const DevProblem& P, double a, int2 ri, const double* w,
+                                                 double* ada_q, double* rw) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) *ada_q = a > 0.0 ? 1.0 / a : 0.0;
+  for (int l = lane; l < ri.y; l += 32) rw[ri.x + l] = 1.0 / (P.rho + 2.0 * w[ri.x + l] * a);
+}
+
 template <int TC>
 __device__ void cache_phi_meta(const DevProblem& P, const double* x, double* smem, bool full) {
   const int un0 = P.cta_unit_ptr[VBID];
@@ -1425,11 +1463,7 @@ __device__ void cache_phi_meta(const DevProblem& P, const double* x, double* sme
     const int i = plo + q;
     const int D = len[q];
     for (int k = lane; k < D; k += 32) xk[q * P.d_pad + k] = ld_cg(x + P.supp_col[static_cast<size_t>(i) * P.d_pad + k]);
-    const double a = ld_cg(P.ada + i);
-    if (lane == 0) ada[q] = a > 0.0 ? 1.0 / a : 0.0;
-    const int2 ri = rinfo[q];
-    for (int l = lane; l < ri.y; l += 32)
-      rw[ri.x + l] = 1.0 / (P.rho + 2.0 * P.row_w[prow0 + ri.x + l] * a);
+    phi_cache_scales(P, ld_cg(P.ada + i), rinfo[q], P.row_w + prow0, ada + q, rw);
   }
   if (one_chunk && threadIdx.x < TC) {
     const int t = threadIdx.x;
@@ -1494,9 +1528,18 @@ __device__ __forceinline__ bool patch_stop_test(const DevProblem& P, const RunAr
   return R.stop_on_conv && pri <= R.eps_pri && dual <= R.eps_dual;
 }
 
-template <int TC, bool RB, bool PAIRS>
+// roff: this MPC step's residual region (word offset in P.resid). pre_target
+// (fused step transitions, iteration 0 only; 0 = none): the split barrier of
+// the previous step's transition -- every CTA has finished reading the final
+// iterate (buffer b ^ 1, s_row) once the counter reaches it; waited for by
+// the last warp under the Φ stage, before the first store into b ^ 1 or s_row.
+// FUSE (kVarFuse kernels only; measured: the extra state compiled into the
+// plain kernel made ptxas interleave the Φ loads with the dot product, +47%
+// per C2 iteration, so the plain path keeps its original form):
+template <int TC, bool RB, bool PAIRS, bool FUSE>
 __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int it, double* smem,
-                                int& cur, const RunArgs& R, unsigned bar_target, int& pair_cnt) {
+                                int& cur, const RunArgs& R, unsigned bar_target, int& pair_cnt, int roff,
+                                unsigned pre_target) {
   double* s_patch = smem + P.off_patch;
   long long* m_pos = reinterpret_cast<long long*>(smem + P.off_meta);
   double* m_x = smem + P.off_meta + 3 * TC;
@@ -1505,12 +1548,20 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
   const double* lam = P.lam[b];
   double pri_m = 0.0, dual_m = 0.0;
   bool tested = it == 0;
+  // FUSE, iteration 0: the own rows' s reach s_row after the Φ barrier (and the split-barrier wait)
+  const bool defer0 = FUSE && pre_target != 0u;
   // the two residual words: one load per CTA (thread 0), broadcast through
   // shared memory at the Φ barrier -- every thread of every CTA loading the
   // same L2 line is a hot spot of ~5k requests per iteration
   unsigned long long rp = 0, rd = 0;
   unsigned long long* rbc = reinterpret_cast<unsigned long long*>(smem + P.off_red);
-  if (!tested && threadIdx.x == 0) { rp = __ldcg(P.resid + 2 * (it - 1)); rd = __ldcg(P.resid + 2 * (it - 1) + 1); }
+  if (!tested && threadIdx.x == 0) {
+    rp = __ldcg(P.resid + roff + 2 * (it - 1)); rd = __ldcg(P.resid + roff + 2 * (it - 1) + 1);
+  }
+  if constexpr (FUSE) {
+    if (pre_target != 0u && threadIdx.x == kThreads - 32)
+      while (static_cast<int>(ld_acquire_u32(P.gbar) - pre_target) < 0) {}
+  }
   PT_DECL
   const int un_a = P.cta_unit_ptr[VBID];
   if (un_a == P.cta_unit_ptr[VBID + 1] && !tested) {
@@ -1556,7 +1607,7 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
       if (rinfo) { const int2 ri = rinfo[i - plo]; r_off = ri.x; nrow = ri.y; }
       else { r_off = static_cast<int>(P.row_start[i] - prow0); nrow = static_cast<int>(P.row_start[i + 1] - P.row_start[i]); }
       double* dst = s_patch + r_off;
-      double* gdst = (tested && i >= own_lo && i < own_hi) ? P.s_row + prow0 + r_off : nullptr;
+      double* gdst = (tested && !defer0 && i >= own_lo && i < own_hi) ? P.s_row + prow0 + r_off : nullptr;
       auto out = [dst, gdst](int l, double s) {
         dst[l] = s;
         if (gdst) gdst[l] = s;
@@ -1581,6 +1632,10 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
         cp_async_wait<0>();
         return true;
       }
+      for (int r = threadIdx.x; r < o_n; r += kThreads)
+        if (DCHK_ROW(P, prow0 + o_off + r, 5) && DCHK(P, o_off + r < P.patch_cap, 6, o_off + r))
+          P.s_row[prow0 + o_off + r] = s_patch[o_off + r];
+    } else if (defer0) {
       for (int r = threadIdx.x; r < o_n; r += kThreads)
         if (DCHK_ROW(P, prow0 + o_off + r, 5) && DCHK(P, o_off + r < P.patch_cap, 6, o_off + r))
           P.s_row[prow0 + o_off + r] = s_patch[o_off + r];
@@ -1635,7 +1690,7 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
     }
   }
   PT_START
-  publish_barrier(P, it, pri_m, dual_m, smem + P.off_red, bar_target);
+  publish_barrier(P, P.resid + roff + 2 * it, pri_m, dual_m, smem + P.off_red, bar_target);
   PT_LAP(P, 5)
   return false;
 }
@@ -2308,6 +2363,163 @@ __device__ void control_plant_stage(const DevProblem& P, int pb, const double* x
   }
 }
 
+// Closed loop, patch mode with the Φ cache of one unit per CTA
+// (P.fuse_steps): the end of an MPC step inside each CTA, with no grid
+// barrier. Replaces control_plant_stage + grid barrier + row_data_stage +
+// grid barrier + cache_phi_meta. Every CTA can read the final iterate
+// (buffer pb, s_row) and x once the last iteration barrier has passed, so
+// the CTA computes what its unit needs itself, over its window (FuseTab,
+// staged in shared memory by fused_tables_load):
+//  1. u of the window inputs (as control_value: the same bits as the input's
+//     owner computes; the owners store P.u and the trajectory's inputs) --
+//     the one global round trip of the transition: ψ, λ, x, s of the inputs'
+//     rows, with x of W2 for the plant rows loaded under it; then the CTA
+//     arrives on the split barrier (P.gbar), which the next step's first
+//     iteration waits for before its first store into pb / s_row;
+//  2. x+ of the window states (as plant_row, from shared memory); the owners
+//     store x+ and the trajectory's states;
+//  3. (refresh: a next step follows) the x-dependent Φ cache from the
+//     window: x on the supports, ||a||^2 in ascending order as
+//     row_data_stage (the owners store P.ada), 1/||a||^2, 1/(ρ + 2w·||a||^2),
+//     x of the single chunk's columns. RowInfeasible (sls_core.py:346-348)
+//     goes into next_bad; the next step tests it after its first iteration
+//     barrier.
+struct FuseSmem {
+  double* fd; double* xo; double* xw; double* uw; double* wrow; int* fi;
+  __device__ FuseSmem(const DevProblem& P, double* smem) {
+    fd = smem + P.off_fw;
+    xo = fd + P.ft_dcap;
+    xw = xo + P.ft_w2cap;
+    uw = xw + P.ft_wcap;
+    wrow = uw + P.ft_ucap;
+    fi = reinterpret_cast<int*>(wrow + P.patch_cap);
+  }
+};
+
+// The unit's FuseTab and its patch rows' Φ weights into shared memory (once
+// per launch; read after the next block barrier).
+static __device__ void fused_tables_load(const DevProblem& P, double* smem) {
+  const int un = P.cta_unit_ptr[VBID];
+  if (un == P.cta_unit_ptr[VBID + 1]) return;
+  FuseSmem f(P, smem);
+  const int i0 = P.ft_iptr[un], ni = P.ft_iptr[un + 1] - i0;
+  const int d0 = P.ft_dptr[un], nd = P.ft_dptr[un + 1] - d0;
+  for (int q = threadIdx.x; q < ni; q += kThreads) f.fi[q] = P.ft_int[i0 + q];
+  for (int q = threadIdx.x; q < nd; q += kThreads) f.fd[q] = P.ft_dbl[d0 + q];
+  const long long prow0 = P.row_start[P.unit_patch_lo[un]];
+  const int prows = static_cast<int>(P.row_start[P.unit_patch_hi[un]] - prow0);
+  for (int q = threadIdx.x; q < prows; q += kThreads) f.wrow[q] = P.row_w[prow0 + q];
+}
+
+template <int TC>
+__device__ void fused_transition(const DevProblem& P, int pb, const double* x, double* xn, double* inputs_out,
+                                 double* states_out, double* smem, bool refresh, int* next_bad) {
+  const int un = P.cta_unit_ptr[VBID];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  if (un == P.cta_unit_ptr[VBID + 1]) {   // no unit: only the split-barrier arrival
+    if (refresh && t == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" :: "l"(P.gbar) : "memory");
+    return;
+  }
+  const FuseSmem f(P, smem);
+  const int* fi = f.fi;
+  const int nw = fi[FuseTab::kNw], nu = fi[FuseTab::kNu], nw2 = fi[FuseTab::kNw2], na = fi[FuseTab::kNa];
+  const int* w2 = fi + fi[FuseTab::kW2];
+  const double xr = t < nw2 ? ld_cg(x + w2[t]) : 0.0;   // stored after stage 1
+  // 1. inputs
+  const double* psi = P.psi[pb];
+  const double* lam = P.lam[pb];
+  for (int j = warp; j < nu; j += kWarps) {
+    const int* hd = fi + fi[FuseTab::kUhead] + 4 * j;
+    const int kf = hd[0], D = hd[2];
+    const int* ue = fi + fi[FuseTab::kUent] + hd[3];
+    const double s = ld_cg(P.s_row + hd[1]);
+    double acc = 0.0;
+    bool first = true;
+    for (int q0 = 0; q0 < D; q0 += 32) {
+      const int kn = min(32, D - q0);
+      double pr = 0.0;
+      if (lane < kn) {
+        const int pos = ue[2 * (q0 + lane)], c = ue[2 * (q0 + lane) + 1];
+        const double xc = ld_cg(x + c);
+        const double phi = make_phi<false>(__dsub_rn(ld_cg(psi + pos), ld_cg(lam + pos)), s, xc);
+        pr = __dmul_rn(phi, xc);
+      }
+      acc = warp_ordered_sum(acc, first, pr, kn);
+    }
+    if (lane == 0) {
+      f.uw[j] = acc;
+      if (kf & 1) { P.u[kf >> 1] = acc; inputs_out[kf >> 1] = acc; }
+    }
+  }
+  if (t < nw2) f.xo[t] = xr;
+  for (int q = t + kThreads; q < nw2; q += kThreads) f.xo[q] = ld_cg(x + w2[q]);
+  __syncthreads();
+  if (refresh && t == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" :: "l"(P.gbar) : "memory");
+  // 2. states (csr_matvec order: from 0, no FMA; then + Bu)
+  const int* aoff = fi + fi[FuseTab::kAoff];
+  const int* boff = aoff + nw + 1;
+  const int* aent = fi + fi[FuseTab::kAent];
+  const int* bent = fi + fi[FuseTab::kBent];
+  const int* wcol = fi + fi[FuseTab::kWcol];
+  for (int j = warp; j < nw; j += kWarps) {
+    double ax = 0.0, bu = 0.0;
+    bool first = false;
+    const int a0 = aoff[j], a1 = aoff[j + 1];
+    for (int q0 = a0; q0 < a1; q0 += 32) {
+      const int kn = min(32, a1 - q0);
+      const double pr = lane < kn ? __dmul_rn(f.fd[q0 + lane], f.xo[aent[q0 + lane]]) : 0.0;
+      ax = warp_ordered_sum(ax, first, pr, kn);
+    }
+    for (int q = boff[j]; q < boff[j + 1]; ++q) bu = __dadd_rn(bu, __dmul_rn(f.fd[na + q], f.uw[bent[q]]));
+    const double v = __dadd_rn(ax, bu);
+    if (lane == 0) {
+      f.xw[j] = v;
+      const int wf = wcol[j];
+      if (wf & 1) { xn[wf >> 1] = v; states_out[wf >> 1] = v; }
+    }
+  }
+  __syncthreads();
+  if (!refresh) return;
+  // 3. the next step's Φ cache (layout: cache_phi_meta)
+  const int* ublk = reinterpret_cast<const int*>(smem + P.off_ublk);
+  const int2* rinfo = reinterpret_cast<const int2*>(smem + P.off_ublk + 8);
+  const int own_lo = ublk[1], own_hi = ublk[2], plo = ublk[3], np = ublk[4] - plo, prows = ublk[5];
+  double* base = smem + P.off_phimeta;
+  double* xk = base + static_cast<size_t>(np) * P.d_pad;
+  double* ada = xk + static_cast<size_t>(np) * P.d_pad;
+  double* rw = ada + np;
+  const int* len = reinterpret_cast<const int*>(rw + 3 * prows);
+  const int* fsup = fi + fi[FuseTab::kSupp];
+  for (int q = warp; q < np; q += kWarps) {
+    const int i = plo + q;
+    const int D = len[q];
+    double acc = 0.0;
+    bool firstp = true;
+    for (int k0 = 0; k0 < D; k0 += 32) {
+      const int kn = min(32, D - k0);
+      double xc = 0.0;
+      if (lane < kn) {
+        xc = f.xw[fsup[q * P.d_pad + k0 + lane]];
+        xk[q * P.d_pad + k0 + lane] = xc;
+      }
+      acc = warp_ordered_sum(acc, firstp, __dmul_rn(xc, xc), kn);
+    }
+    if (D < P.d_row) acc = __dadd_rn(acc, 0.0);   // as row_data_stage
+    if (lane == 0 && i >= own_lo && i < own_hi) {
+      P.ada[i] = acc;
+      if (acc == 0.0 && P.sub_first_bad[i] >= 0 && i >= P.own_sub_lo && i < P.own_sub_hi)
+        atomicMin(next_bad, P.sub_first_bad[i]);
+    }
+    phi_cache_scales(P, acc, rinfo[q], f.wrow, ada + q, rw);
+  }
+  const int ch_a = ublk[8], ch_b = ublk[9];
+  if (ch_b - ch_a == 1 && t < TC) {   // the single chunk's columns (own states: in the window)
+    const int* mx = fi + fi[FuseTab::kMx];
+    (smem + P.off_meta + 3 * TC)[t] = t < ublk[12] ? f.xw[mx[t]] : 0.0;
+  }
+  __syncthreads();
+}
+
 static __device__ void zero_iterate(const DevProblem& P, int b) {
   const size_t n = static_cast<size_t>(P.n_cols) * P.s_pad;
   const size_t gt = VBID * blockDim.x + threadIdx.x, GT = VGRID * blockDim.x;
@@ -2404,6 +2616,7 @@ __device__ bool dist_exchange(const DevProblem& P, const RunArgs& R, int it, int
 // patch cells):
 constexpr int kVarDist = 1;    // graph-partitioned solve, exchange on the device (non-patch modes)
 constexpr int kVarPairs = 2;   // patch mode with K-split CTA pairs
+constexpr int kVarFuse = 4;    // patch mode closed loops, warm-started: fused MPC-step transitions (P.fuse_steps)
 
 template <int TC, int MODE, int VAR>
 __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunArgs& R);
@@ -2443,34 +2656,54 @@ __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunAr
     __syncthreads();
   }
   const size_t gt = VBID * blockDim.x + tid, GT = VGRID * blockDim.x;
+  // fused MPC-step transitions (fused_transition; the host launches this
+  // variant only for warm-started closed loops of more than one step with
+  // P.fuse_steps): from step 1 on, no grid barrier between steps. A step's
+  // residual words then rotate over three regions and its RowInfeasible slot
+  // over three (ctl 2, 3, 6): a region is zeroed one step ahead, when every
+  // CTA has passed the first iteration barrier of the step after its last
+  // reader's.
+  constexpr bool fuse = PATCH && (VAR & kVarFuse) != 0;
   // patch modes: the iteration barrier's counter value at launch (stable: the
-  // previous launch has ended, and no CTA arrives before the first grid.sync)
-  const unsigned bar_base = (PATCH && tid == 0) ? ld_acquire_u32(P.gbar) : 0u;
+  // previous launch has ended, and no CTA arrives before the first grid.sync);
+  // fused: also read by the last warp, which waits on the split barriers
+  const unsigned bar_base = (PATCH && (tid == 0 || (fuse && tid == kThreads - 32))) ? ld_acquire_u32(P.gbar) : 0u;
   unsigned bar_epoch = 0;
   int pair_cnt = 0;   // K-split pairs: partial-Y publications of this CTA in this launch
+  unsigned pre_target = 0u;   // fused: the split barrier the next step's first iteration waits for
+  if constexpr (fuse) fused_tables_load(P, smem);   // read after step 0's grid barrier
   for (int step = 0; step < R.t_sim; ++step) {
     PT_DECL
     PT_START
     const double* x = P.x[R.closed_loop ? (step & 1) : 0];
-    int* bad_slot = P.ctl + 2 + (step & 1);
-    for (size_t q = gt; q < static_cast<size_t>(2 * R.max_iters); q += GT) P.resid[q] = 0ull;
-    if (R.closed_loop) {
-      row_data_stage(P, x, bad_slot);
-      if ((R.cold_start && step == 0) || !R.warm_start) zero_iterate(P, b);
-    }
-    if (MODE == kStream) fence_proxy_async_global();   // zeroed ψ, λ are read by TMA
-    grid.sync();
-    if (R.closed_loop) {
-      const int bad = *reinterpret_cast<volatile int*>(bad_slot);
-      if (bad != kBadNone) {
-        if (leader) { P.ctl[0] = 2; P.ctl[1] = step; P.ctl[5] = 0; P.ctl[4] = b; }
-        return;
+    const int roff = fuse ? (step % 3) * 2 * R.max_iters : 0;
+    if (!fuse || step == 0) {
+      int* bad_slot = P.ctl + 2 + (step & 1);
+      for (size_t q = gt; q < static_cast<size_t>((fuse ? 4 : 2) * R.max_iters); q += GT) P.resid[q] = 0ull;
+      if (R.closed_loop) {
+        row_data_stage(P, x, bad_slot);
+        if ((R.cold_start && step == 0) || !R.warm_start) zero_iterate(P, b);
       }
-      if (leader) P.ctl[2 + ((step + 1) & 1)] = kBadNone;
+      if (MODE == kStream) fence_proxy_async_global();   // zeroed ψ, λ are read by TMA
+      grid.sync();
+      if (R.closed_loop) {
+        const int bad = *reinterpret_cast<volatile int*>(bad_slot);
+        if (bad != kBadNone) {
+          if (leader) { P.ctl[0] = 2; P.ctl[1] = step; P.ctl[5] = 0; P.ctl[4] = b; }
+          return;
+        }
+        if (leader) {
+          P.ctl[2 + ((step + 1) & 1)] = kBadNone;
+          if (fuse) P.ctl[6] = kBadNone;
+        }
+      }
+      PT_LAP(P, 8)
+      if (PATCH && P.cache_phi) cache_phi_meta<TC>(P, x, smem, step == 0);
+      PT_LAP(P, 9)
+    } else {   // the Φ cache came from the previous step's transition
+      const size_t z = static_cast<size_t>(((step + 1) % 3) * 2 * R.max_iters);
+      for (size_t q = gt; q < static_cast<size_t>(2 * R.max_iters); q += GT) P.resid[z + q] = 0ull;
     }
-    PT_LAP(P, 8)
-    if (PATCH && P.cache_phi) cache_phi_meta<TC>(P, x, smem, step == 0);
-    PT_LAP(P, 9)
     int it = 0;
     bool conv = false;
     if (PATCH) {
@@ -2479,20 +2712,33 @@ __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunAr
         PT_DECL
         if (it == R.max_iters) {
           if (it > 0) {
-            const unsigned long long rp = __ldcg(P.resid + 2 * (it - 1)), rd = __ldcg(P.resid + 2 * (it - 1) + 1);
+            const unsigned long long rp = __ldcg(P.resid + roff + 2 * (it - 1));
+            const unsigned long long rd = __ldcg(P.resid + roff + 2 * (it - 1) + 1);
             conv = patch_stop_test(P, R, it, rp, rd);
           }
           break;
         }
         bar_epoch += VGRID;
-        if (patch_iteration<TC, MODE == kPatchRb, (VAR & kVarPairs) != 0>(P, b, x, it, smem, cur, R,
-                                                                           bar_base + bar_epoch, pair_cnt)) {
+        if (patch_iteration<TC, MODE == kPatchRb, (VAR & kVarPairs) != 0, fuse>(
+                P, b, x, it, smem, cur, R, bar_base + bar_epoch, pair_cnt, roff, it == 0 ? pre_target : 0u)) {
           bar_epoch -= VGRID;   // returned before arriving
           conv = true;
           break;
         }
         b ^= 1;
         ++it;
+        if (fuse && step > 0 && it == 1) {   // the RowInfeasible test of this step's transition
+          int* slot = (step % 3) == 2 ? P.ctl + 6 : P.ctl + 2 + step % 3;
+          const int bad = *reinterpret_cast<volatile int*>(slot);
+          if (bad != kBadNone) {   // the step's iterate in b ^ 1 is untouched
+            if (leader) { P.ctl[2 + (step & 1)] = bad; P.ctl[0] = 2; P.ctl[1] = step; P.ctl[5] = 0; P.ctl[4] = b ^ 1; }
+            return;
+          }
+          if (leader) {   // the slot of step + 2; its last reader has passed this barrier
+            const int j = (step + 2) % 3;
+            *(j == 2 ? P.ctl + 6 : P.ctl + 2 + j) = kBadNone;
+          }
+        }
       }
     }
     while (!PATCH && it < R.max_iters) {
@@ -2547,11 +2793,21 @@ __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunAr
         for (size_t q = gt; q < static_cast<size_t>(P.n_cols); q += GT) R.states[q] = x[q];
       }
       double* xn = P.x[(step + 1) & 1];
-      control_plant_stage<EXACT>(P, b ^ 1, x, xn, R.inputs + static_cast<size_t>(step) * P.n_inputs,
-                                 R.states + static_cast<size_t>(step + 1) * P.n_cols);
-      PT_LAP(P, 10)
-      grid.sync();
-      PT_LAP(P, 11)
+      if (fuse) {
+        const bool refresh = step + 1 < R.t_sim;
+        const int j = (step + 1) % 3;
+        fused_transition<TC>(P, b ^ 1, x, xn, R.inputs + static_cast<size_t>(step) * P.n_inputs,
+                             R.states + static_cast<size_t>(step + 1) * P.n_cols, smem, refresh,
+                             j == 2 ? P.ctl + 6 : P.ctl + 2 + j);
+        if (refresh) { bar_epoch += VGRID; pre_target = bar_base + bar_epoch; }
+        PT_LAP(P, 10)
+      } else {
+        control_plant_stage<EXACT>(P, b ^ 1, x, xn, R.inputs + static_cast<size_t>(step) * P.n_inputs,
+                                   R.states + static_cast<size_t>(step + 1) * P.n_cols);
+        PT_LAP(P, 10)
+        grid.sync();
+        PT_LAP(P, 11)
+      }
     }
   }
   if (leader) { P.ctl[0] = 0; P.ctl[4] = b; }

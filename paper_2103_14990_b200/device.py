@@ -57,7 +57,7 @@ class _Problem(C.Structure):
 EXPORTS = ("dlmpc_create", "dlmpc_destroy", "dlmpc_last_error", "dlmpc_global_error",
            "dlmpc_set_x", "dlmpc_solve", "dlmpc_iterate", "dlmpc_simulate",
            "dlmpc_simulate_device", "dlmpc_get", "dlmpc_put", "dlmpc_zero",
-           "dlmpc_last_timing", "dlmpc_stream", "dlmpc_synchronize", "dlmpc_info",
+           "dlmpc_last_timing", "dlmpc_stream", "dlmpc_synchronize", "dlmpc_info", "dlmpc_plan_flags",
            "dlmpc_phase_times", "dlmpc_audit", "dlmpc_get_cols", "dlmpc_put_cols",
            "dlmpc_finish_step", "dlmpc_set_halo", "dlmpc_halo_pack", "dlmpc_halo_unpack",
            "dlmpc_iterate_async", "dlmpc_halo_pack_async", "dlmpc_halo_unpack_async", "dlmpc_set_stream",
@@ -123,6 +123,7 @@ def load_library():
     lib.dlmpc_stream.restype = vp
     lib.dlmpc_synchronize.argtypes = [vp]
     lib.dlmpc_info.argtypes = [vp, _i64p]
+    lib.dlmpc_plan_flags.argtypes = [vp, _i64p, C.c_int]
     lib.dlmpc_phase_times.argtypes = [vp, _P(C.c_uint64), C.c_int]
     lib.dlmpc_audit.argtypes = [vp, _f64p, _f64p]
     lib.dlmpc_get_cols.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp]
@@ -499,4 +500,7 @@ class DeviceSession:
         keys = ("n_rows", "n_cols", "s_pad", "n_sub", "grid", "tile_cols", "smem_bytes", "mode", "units")
         d = dict(zip(keys, (int(v) for v in out)))
         d["mode"] = ("patch", "twophase", "exact", "stream")[d["mode"]]
+        fl = np.zeros(5, dtype=np.int64)
+        self._lib.dlmpc_plan_flags(self._h, _ptr(fl, C.c_int64), 5)
+        d.update(zip(("cache_phi", "fuse_steps", "rb_gemv", "stash_bufs", "pairs"), (int(v) for v in fl)))
         return d
