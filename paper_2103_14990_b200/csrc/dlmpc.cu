@@ -46,6 +46,7 @@ struct dlmpc_handle {
   int64_t* d_recv_cells = nullptr; int64_t n_recv = 0;
   double* d_halo = nullptr;
   char* h_stage = nullptr; size_t stage_cap = 0;   // pinned staging of dlmpc_simulate's host copies
+  char* d_stage = nullptr;                          // its device mirror: one D2H copy per closed loop
   cudaStream_t own_stream = nullptr;   // the handle's stream; `stream` may be an external one (dlmpc_set_stream)
   int cur_b = 0, b_valid = 1;          // current ψ/λ buffer as known on the host (ctl[4])
   int dist_world = 0;                  // > 0 once dlmpc_dist_alloc ran
@@ -1019,6 +1020,7 @@ void dlmpc_destroy(dlmpc_handle* h) {
   if (h->d_halo) cudaFree(h->d_halo);
   if (h->P.resid) cudaFree(h->P.resid);
   if (h->h_stage) cudaFreeHost(h->h_stage);
+  if (h->d_stage) cudaFree(h->d_stage);
   if (h->d_step_iters) cudaFree(h->d_step_iters);
   if (h->d_states) cudaFree(h->d_states);
   if (h->d_inputs) cudaFree(h->d_inputs);
@@ -1077,14 +1079,11 @@ int dlmpc_iterate(dlmpc_handle* h, int n, double* hist) {
   return run_iterations(h, n, 0.0, 0.0, 0, &it, hist);
 }
 
-int dlmpc_simulate_device(dlmpc_handle* h, const double* x0_dev, int t_sim, int warm_start, int cold_start,
-                          int max_iters, double eps_pri, double eps_dual, double* states_dev,
-                          double* inputs_dev, int* step_iters_dev, int* status_dev) {
-  if (h) h->it_cont = 0;
-  if (!h || !x0_dev || t_sim < 1 || max_iters < 1) return fail(h, DLMPC_BAD_ARGUMENT, "bad argument");
-  cudaSetDevice(h->device);
-  if (int rc = ensure_run_buffers(h, max_iters, t_sim)) return rc;
-  CUDA_OR_FAIL(h, cudaMemcpyAsync(h->P.x[0], x0_dev, sizeof(double) * h->P.n_cols, cudaMemcpyDeviceToDevice, h->stream));
+namespace {
+// The closed-loop launch with x0 already in P.x[0].
+int launch_closed_loop(dlmpc_handle* h, int t_sim, int warm_start, int cold_start, int max_iters, double eps_pri,
+                       double eps_dual, double* states_dev, double* inputs_dev, int* step_iters_dev,
+                       int* status_dev) {
   CUDA_OR_FAIL(h, cudaMemsetAsync(h->P.ctl + 2, 0x7f, sizeof(int) * 2, h->stream));
   RunArgs R{};
   R.t_sim = t_sim; R.closed_loop = 1; R.warm_start = warm_start; R.cold_start = cold_start;
@@ -1098,12 +1097,25 @@ int dlmpc_simulate_device(dlmpc_handle* h, const double* x0_dev, int t_sim, int 
   CUDA_OR_FAIL(h, cudaGetLastError());
   return DLMPC_OK;
 }
+}  // namespace
+
+int dlmpc_simulate_device(dlmpc_handle* h, const double* x0_dev, int t_sim, int warm_start, int cold_start,
+                          int max_iters, double eps_pri, double eps_dual, double* states_dev,
+                          double* inputs_dev, int* step_iters_dev, int* status_dev) {
+  if (h) h->it_cont = 0;
+  if (!h || !x0_dev || t_sim < 1 || max_iters < 1) return fail(h, DLMPC_BAD_ARGUMENT, "bad argument");
+  cudaSetDevice(h->device);
+  if (int rc = ensure_run_buffers(h, max_iters, t_sim)) return rc;
+  CUDA_OR_FAIL(h, cudaMemcpyAsync(h->P.x[0], x0_dev, sizeof(double) * h->P.n_cols, cudaMemcpyDeviceToDevice, h->stream));
+  return launch_closed_loop(h, t_sim, warm_start, cold_start, max_iters, eps_pri, eps_dual, states_dev, inputs_dev,
+                            step_iters_dev, status_dev);
+}
 
 int dlmpc_simulate(dlmpc_handle* h, const double* x0, int t_sim, int warm_start, int cold_start,
                    int max_iters, double eps_pri, double eps_dual, double* states, double* inputs,
                    int* step_iters, int* fail_step, int64_t* bad_row, int* fail_iters, double* fail_hist) {
   if (h) h->it_cont = 0;
-  if (!h || !x0 || t_sim < 1) return fail(h, DLMPC_BAD_ARGUMENT, "bad argument");
+  if (!h || !x0 || t_sim < 1 || max_iters < 1) return fail(h, DLMPC_BAD_ARGUMENT, "bad argument");
   cudaSetDevice(h->device);
   if (int rc = ensure_run_buffers(h, max_iters, t_sim)) return rc;
   // pinned staging: x0 in, then status, iteration counts, trajectory out in
@@ -1113,19 +1125,23 @@ int dlmpc_simulate(dlmpc_handle* h, const double* x0, int t_sim, int warm_start,
   const size_t o_in = o_st + (size_t)(t_sim + 1) * nc * 8, need = o_in + (size_t)t_sim * ni * 8 + 8;
   if (need > h->stage_cap) {
     if (h->h_stage) cudaFreeHost(h->h_stage);
-    h->h_stage = nullptr; h->stage_cap = 0;
+    if (h->d_stage) cudaFree(h->d_stage);
+    h->h_stage = nullptr; h->d_stage = nullptr; h->stage_cap = 0;
     CUDA_OR_FAIL(h, cudaMallocHost(reinterpret_cast<void**>(&h->h_stage), need));
+    CUDA_OR_FAIL(h, cudaMalloc(reinterpret_cast<void**>(&h->d_stage), need));
     h->stage_cap = need;
   }
+  // the kernel writes iteration counts, states and inputs straight into the
+  // device mirror of the staging layout and the status joins them with one
+  // small D2D copy, so the results come back in a single D2H copy
   char* hs = h->h_stage;
+  char* ds = h->d_stage;
   std::memcpy(hs, x0, nc * 8);
-  CUDA_OR_FAIL(h, cudaMemcpyAsync(h->d_states, hs, nc * 8, cudaMemcpyHostToDevice, h->stream));
-  if (int rc = dlmpc_simulate_device(h, h->d_states, t_sim, warm_start, cold_start, max_iters, eps_pri, eps_dual,
-                                     nullptr, nullptr, nullptr, nullptr)) return rc;
-  CUDA_OR_FAIL(h, cudaMemcpyAsync(hs + o_ctl, h->P.ctl, sizeof(int) * 8, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_OR_FAIL(h, cudaMemcpyAsync(hs + o_it, h->d_step_iters, sizeof(int) * t_sim, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_OR_FAIL(h, cudaMemcpyAsync(hs + o_st, h->d_states, (size_t)(t_sim + 1) * nc * 8, cudaMemcpyDeviceToHost, h->stream));
-  if (ni) CUDA_OR_FAIL(h, cudaMemcpyAsync(hs + o_in, h->d_inputs, (size_t)t_sim * ni * 8, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_OR_FAIL(h, cudaMemcpyAsync(h->P.x[0], hs, nc * 8, cudaMemcpyHostToDevice, h->stream));
+  if (int rc = launch_closed_loop(h, t_sim, warm_start, cold_start, max_iters, eps_pri, eps_dual,
+                                  reinterpret_cast<double*>(ds + o_st), reinterpret_cast<double*>(ds + o_in),
+                                  reinterpret_cast<int*>(ds + o_it), reinterpret_cast<int*>(ds + o_ctl))) return rc;
+  CUDA_OR_FAIL(h, cudaMemcpyAsync(hs + o_ctl, ds + o_ctl, need - o_ctl, cudaMemcpyDeviceToHost, h->stream));
   CUDA_OR_FAIL(h, cudaStreamSynchronize(h->stream));
   CUDA_OR_FAIL(h, cudaEventElapsedTime(&h->last_ms, h->ev0, h->ev1));
   int ctl[8];
@@ -1135,7 +1151,10 @@ int dlmpc_simulate(dlmpc_handle* h, const double* x0, int t_sim, int warm_start,
   if (fail_step) *fail_step = ctl[0] == DLMPC_OK ? -1 : ctl[1];
   if (bad_row) *bad_row = ctl[0] == DLMPC_ROW_INFEASIBLE ? ctl[2 + (ctl[1] & 1)] : -1;
   if (fail_iters) *fail_iters = ctl[0] == DLMPC_NOT_CONVERGED ? ctl[5] : 0;
-  if (states) std::memcpy(states, hs + o_st, (size_t)(done + 1) * nc * 8);
+  if (states) {   // row 0 is x0 (the kernel stores it only once step 0 has been solved)
+    std::memcpy(states, x0, nc * 8);
+    if (done > 0) std::memcpy(states + nc, hs + o_st + nc * 8, (size_t)done * nc * 8);
+  }
   if (inputs && done > 0 && ni) std::memcpy(inputs, hs + o_in, (size_t)done * ni * 8);
   if (step_iters && done > 0) std::memcpy(step_iters, hs + o_it, sizeof(int) * done);
   if (fail_hist && ctl[0] == DLMPC_NOT_CONVERGED && ctl[5] > 0)
