@@ -627,9 +627,19 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         }
       }
       h->n_units = (int)u_lo.size();
+      // patch mode: trailing CTAs without a unit would only join the barriers
+      // (C2: 100 units on 148 SMs); the launch leaves them out (tools/grid_ab.py,
+      // C2 closed loops: 14.62 -> 14.74 M subsystem-iters/s, bitwise the same)
+      const char* keep = getenv("DLMPC_KEEP_IDLE_CTAS");
+      if (h->mode == kPatch && cta_pair.empty() && !(keep && keep[0] == '1')) {
+        int gl = G;
+        while (gl > 1 && cta_ptr[gl - 1] == cta_ptr[gl]) --gl;
+        cta_ptr.resize(gl + 1);
+        h->grid = gl;
+      }
     }
     bool one_unit = true;
-    for (int q = 0; q < G; ++q) one_unit = one_unit && (cta_ptr[q + 1] - cta_ptr[q] <= 1);
+    for (int q = 0; q < h->grid; ++q) one_unit = one_unit && (cta_ptr[q + 1] - cta_ptr[q] <= 1);
     bool rb_off = false;   // the register-blocked GEMV pair was planned but did not fit
     for (; h->mode != kStream;) {
       const int ldk = ld_frag(s8_max), ldy = ld_frag(tc);
