@@ -45,19 +45,29 @@ namespace dlmpc {
 #endif
 
 // Optional per-phase timers (profiling build only: -DDLMPC_PHASE_TIMING).
-// Thread 0 of every CTA accumulates SM-cycle deltas per phase into
-// P.phase_ns[blockIdx.x * 16 + phase] (0-7 per iteration, 8-15 per MPC step).
+// Thread 0 of every CTA accumulates SM-cycle deltas per phase in shared
+// memory and adds them to P.phase_ns[blockIdx.x * 16 + phase] (0-7 per
+// iteration, 8-15 per MPC step) when the kernel ends (round 1 added them to
+// global memory at every lap: the read-modify-write put an L2 round trip into
+// the next lap's interval).
 #ifdef DLMPC_PHASE_TIMING
 __device__ __forceinline__ unsigned long long gtimer() {   // SM cycles (globaltimer is too coarse)
   return static_cast<unsigned long long>(clock64());
 }
+__shared__ unsigned long long pt_sh[16];
 #define PT_DECL unsigned long long pt_t0 = 0;
 #define PT_START if (threadIdx.x == 0) pt_t0 = gtimer();
-#define PT_LAP(P, ph) if (threadIdx.x == 0) { unsigned long long t1_ = gtimer(); (P).phase_ns[VBID * 16 + (ph)] += t1_ - pt_t0; pt_t0 = t1_; }
+#define PT_LAP(P, ph) if (threadIdx.x == 0) { unsigned long long t1_ = gtimer(); pt_sh[(ph)] += t1_ - pt_t0; pt_t0 = t1_; }
+#define PT_ADD(ph, v) if (threadIdx.x == 0) pt_sh[(ph)] += (v);
+#define PT_INIT if (threadIdx.x == 0) for (int q_ = 0; q_ < 16; ++q_) pt_sh[q_] = 0ull;
+#define PT_FLUSH(P) if (threadIdx.x == 0) for (int q_ = 0; q_ < 16; ++q_) (P).phase_ns[VBID * 16 + q_] += pt_sh[q_];
 #else
 #define PT_DECL
 #define PT_START
 #define PT_LAP(P, ph)
+#define PT_ADD(ph, v)
+#define PT_INIT
+#define PT_FLUSH(P)
 #endif
 
 // Virtual CTA index / count of the persistent kernel: blockIdx.x / gridDim.x
@@ -1616,6 +1626,7 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
     double* stash = smem + P.off_stash;
     const int stash_stride = 2 * P.stash_cols * P.ldk;
     if (P.stash_bufs > 0 && ch_a < ch_b) stash_issue(P, c00, nt0, S0, psi, lam, stash);
+    PT_LAP(P, 12)   // timing build, patch modes: thread 0's view of the Φ stage in slots 12-15
     // Φ scale of every row the unit's columns touch (own rows + d-hop halo);
     // before the stop test the own rows' s goes to shared memory only
     for (int i = plo + warp; i < phi_; i += kWarps) {
@@ -1633,12 +1644,15 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
       else
         phi_rows_of<false>(P, i, psi, lam, x, out);
     }
+    PT_LAP(P, 13)
     if (!tested && threadIdx.x == 0) { rbc[0] = rp; rbc[1] = rd; }
+    PT_LAP(P, 14)
     // a unit of one chunk with cached metadata: its staged ψ, λ (issued
     // before Φ) are waited for here, so this barrier also publishes them and
     // the chunk needs no barrier of its own
     const bool one_chunk = P.cache_phi && ch_b - ch_a == 1 && P.stash_bufs > 0;
     if (one_chunk) cp_async_wait<0>();
+    PT_LAP(P, 15)
     __syncthreads();
     PT_LAP(P, 0)
     if (!tested) {
@@ -2145,8 +2159,8 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
           pri_m = epi.pri_m; dual_m = epi.dual_m;
 #ifdef DLMPC_PHASE_TIMING
           if (tid == 0) {
-            P.phase_ns[VBID * 16 + 9] += epi.t_kloop - pt_t0;
-            P.phase_ns[VBID * 16 + 10] += epi.t_lam - epi.t_kloop;
+            pt_sh[9] += epi.t_kloop - pt_t0;
+            pt_sh[10] += epi.t_lam - epi.t_kloop;
             pt_t0 = epi.t_lam;
           }
 #endif
@@ -2672,6 +2686,7 @@ __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunAr
     __syncthreads();
   }
   const size_t gt = VBID * blockDim.x + tid, GT = VGRID * blockDim.x;
+  PT_INIT
   // fused MPC-step transitions (fused_transition; the host launches this
   // variant only for warm-started closed loops of more than one step with
   // P.fuse_steps): from step 1 on, no grid barrier between steps. A step's
@@ -2801,6 +2816,7 @@ __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunAr
     PT_START
     if (leader) R.step_iters[step] = it;
     if (R.stop_on_conv && !conv) {
+      PT_FLUSH(P)
       if (leader) { P.ctl[0] = 1; P.ctl[1] = step; P.ctl[5] = it; P.ctl[4] = b; }
       return;
     }
@@ -2826,6 +2842,7 @@ __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunAr
       }
     }
   }
+  PT_FLUSH(P)
   if (leader) { P.ctl[0] = 0; P.ctl[4] = b; }
 }
 
