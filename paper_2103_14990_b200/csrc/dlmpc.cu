@@ -243,6 +243,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
   int optin = 0;
   CUDA_OR_FAIL(h, cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
   const long long limit = (optin - 1024) / 8;   // doubles
+  P.off_ctab = -1;   // patch plans set it
   const int G = pr->grid_ctas > 0 ? std::min(pr->grid_ctas, h->sm_count) : h->sm_count;
   h->grid = G;
   {
@@ -677,7 +678,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       auto part = [&](int sp) { return std::max<long long>(sp > 1 ? (long long)sp * n08_max * tc : 0, rb_part); };
       auto total = [&](long long opr, int sp, bool cache) {
         return opr + (long long)kt_cols * ldk + (long long)n08_max * ldy + part(sp)
-               + 32 + 4 * tc + prows_max + (cache ? meta_phi : 0) + 4;
+               + 34 + 4 * tc + prows_max + (cache ? meta_phi : 0) + 4;
       };
       while (split_max > 1 && total(0, split_max, false) > limit) split_max >>= 1;
       if (total(0, split_max, false) > limit) {
@@ -709,7 +710,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         const char* e = getenv("DLMPC_SMALL_GEMV");
         P.small_gemv = (split_max > 1 && (long long)split_max * tc >= 10 && !(e && e[0] == '0')) ? 1 : 0;
       }
-      P.off_red = (int)off; off += 32;
+      P.off_red = (int)off; off += 34;   // + the CTA's unit range (2 ints, patch_iteration)
       P.off_meta = (int)off; off += 4 * tc;
       P.off_patch = (int)off; off += (prows_max + 1) & ~1LL;
       P.patch_cap = (int)prows_max;
@@ -721,6 +722,13 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       P.stash_bufs = stash_bufs;
       P.stash_cols = st_cols;
       P.rb_gemv = rb ? 1 : 0;
+      // patch plans (the DMMA chunks read them; the two-phase kernel shares
+      // this planner but not the table): class sizes in shared memory
+      // (class_dims), 3 doubles per class
+      if (h->mode == kPatch && !rb && pr->n_classes <= 256 && off + 3LL * pr->n_classes <= limit) {
+        P.off_ctab = (int)off;
+        off += 3LL * pr->n_classes;
+      }
       P.off_ex = (int)off;
       h->smem_bytes = (int)(off * 8);
       P.tile_cols = tc;

@@ -206,6 +206,9 @@ struct DevProblem {
   const int* ft_iptr; const int* ft_int;       // [n_units+1] offsets, int tables
   const int* ft_dptr; const double* ft_dbl;    // [n_units+1] offsets, A / B values
   int off_fw, ft_dcap, ft_w2cap, ft_wcap, ft_ucap;   // shared memory region and its section capacities
+  // patch modes: the class sizes in shared memory (class_dims), staged at
+  // launch; -1: none (other modes, or too many classes)
+  int off_ctab;
 };
 
 // A unit's window for fused_transition: W = the states of its patch
@@ -247,6 +250,30 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+// A class's sizes and basis offset: from the shared-memory table of the patch
+// modes (P.off_ctab, staged at launch), else from the global tables. The
+// iteration barrier's acquire invalidates L1, so right after it every global
+// table load is an L2 round trip on the chunk's critical path.
+struct ClassDims { int s, n0, ldn; long long off; };
+__device__ __forceinline__ ClassDims class_dims(const DevProblem& P, const double* smem, int k) {
+  if (P.off_ctab >= 0) {
+    const int* ci = reinterpret_cast<const int*>(smem + P.off_ctab) + 4 * k;
+    const long long* co = reinterpret_cast<const long long*>(smem + P.off_ctab + 2 * P.n_classes);
+    return {ci[0], ci[1], ci[2], co[k]};
+  }
+  return {P.class_s[k], P.class_n0[k], P.class_ldn[k], P.class_null_off[k]};
+}
+__device__ __forceinline__ void class_table_load(const DevProblem& P, double* smem) {   // all threads
+  if (P.off_ctab < 0) return;
+  int* ci = reinterpret_cast<int*>(smem + P.off_ctab);
+  long long* co = reinterpret_cast<long long*>(smem + P.off_ctab + 2 * P.n_classes);
+  for (int k = threadIdx.x; k < P.n_classes; k += kThreads) {
+    ci[4 * k] = P.class_s[k]; ci[4 * k + 1] = P.class_n0[k]; ci[4 * k + 2] = P.class_ldn[k]; ci[4 * k + 3] = 0;
+    co[k] = P.class_null_off[k];
+  }
+}
+
 
 // Bounds checks of the checked build (there is no compute-sanitizer on the
 // GPU pool): DCHK(P, cond, code, idx) records the first failing (code, idx)
@@ -1122,11 +1149,12 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
   const long long* m_q = m_pos + 2 * TC;
   const double* m_x = smem + P.off_meta + 3 * TC;
   const int ldk = P.ldk, ldy = P.ldy;
-  const int S = P.class_s[k], S8 = (S + 7) & ~7;
-  const int n0 = P.class_n0[k], n08 = (n0 + 7) & ~7;
-  const int ldn = P.class_ldn[k];
+  const ClassDims cd = class_dims(P, smem, k);
+  const int S = cd.s, S8 = (S + 7) & ~7;
+  const int n0 = cd.n0, n08 = (n0 + 7) & ~7;
+  const int ldn = cd.ldn;
   // the class operator: staged at smem offset 0 (LDS) or read from global
-  const double* nop = OPS ? smem : P.null_pool + P.class_null_off[k];
+  const double* nop = OPS ? smem : P.null_pool + cd.off;
   PT_DECL
   PT_START
   const int t_el = warp / WPC;                  // this warp's column in element loops
@@ -1235,11 +1263,12 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
 // (cooperative copy, once per class change -- with the class-aware CTA
 // assignment, once per launch). Returns whether it is in shared memory.
 __device__ __forceinline__ bool stage_operator(const DevProblem& P, int k, double* smem, int& cur) {
-  const long long n = static_cast<long long>((P.class_s[k] + 7) & ~7) * P.class_ldn[k];
+  const ClassDims cd = class_dims(P, smem, k);
+  const long long n = static_cast<long long>((cd.s + 7) & ~7) * cd.ldn;
   if (n > P.opr_cap) return false;
   if (k != cur) {
     __syncthreads();
-    const double2* src = reinterpret_cast<const double2*>(P.null_pool + P.class_null_off[k]);
+    const double2* src = reinterpret_cast<const double2*>(P.null_pool + cd.off);
     double2* dst = reinterpret_cast<double2*>(smem);
     for (long long q = threadIdx.x; q < n / 2; q += kThreads) dst[q] = __ldg(src + q);
     __syncthreads();
@@ -1286,8 +1315,9 @@ __device__ __forceinline__ void run_chunk(const DevProblem& P, int k, int nt, co
 // 216-217); the operator is staged thread-major once per class.
 constexpr int kRbTag = 1 << 24;   // `cur` = k + AL * kRbTag: a thread-major staged operator
 template <int TC, int RB_AL>
-__device__ void rb_chunk_al(const DevProblem& P, int k, int nt, double* psi_n, double* lam_n, const double* s_src,
-                         double* smem, int& cur, double& pri_m, double& dual_m, const double* st) {
+__device__ void rb_chunk_al(const DevProblem& P, int k, int S, int nt, double* psi_n, double* lam_n,
+                            const double* s_src, double* smem, int& cur, double& pri_m, double& dual_m,
+                            const double* st) {
   if (cur != k + RB_AL * kRbTag) {
     __syncthreads();
     stage_operator_rb<RB_AL>(P, k, smem);
@@ -1298,7 +1328,7 @@ __device__ void rb_chunk_al(const DevProblem& P, int k, int nt, double* psi_n, d
   const long long* m_s = m_pos + TC;
   const long long* m_q = m_pos + 2 * TC;
   const double* m_x = smem + P.off_meta + 3 * TC;
-  const int S = P.class_s[k], ldk = P.ldk;
+  const int ldk = P.ldk;
   const int l = threadIdx.x & 31, w = threadIdx.x >> 5, h = l >> 4, j = l & 15;
   const int PB = (((S + 7) & ~7) + 15) >> 4;
   const int prow0 = w * PB + h * RB_PL;
@@ -1344,11 +1374,13 @@ __device__ void rb_chunk_al(const DevProblem& P, int k, int nt, double* psi_n, d
 // One blocking (RB_AL = 4, n0 <= 64) for every class: a second, narrower
 // instantiation for the d=3 interior class (n0 = 47) saves its idle FMAs but
 // doubles the hot loop's code, and measured 10.6 vs 8.4 us/iteration on C2.
+// S: the class's support length (the caller has it: no global table load
+// after the iteration barrier, whose acquire invalidates L1).
 template <int TC>
-__device__ __forceinline__ void rb_chunk(const DevProblem& P, int k, int nt, double* psi_n, double* lam_n,
+__device__ __forceinline__ void rb_chunk(const DevProblem& P, int k, int S, int nt, double* psi_n, double* lam_n,
                                          const double* s_src, double* smem, int& cur, double& pri_m,
                                          double& dual_m, const double* st) {
-  rb_chunk_al<TC, RB_AL_MAX>(P, k, nt, psi_n, lam_n, s_src, smem, cur, pri_m, dual_m, st);
+  rb_chunk_al<TC, RB_AL_MAX>(P, k, S, nt, psi_n, lam_n, s_src, smem, cur, pri_m, dual_m, st);
 }
 
 // Column stage of the two-phase fast kernel (class-sorted tiles, generic graphs).
@@ -1589,15 +1621,19 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
       while (static_cast<int>(ld_acquire_u32(P.gbar) - pre_target) < 0) {}
   }
   PT_DECL
-  const int un_a = P.cta_unit_ptr[VBID];
-  if (un_a == P.cta_unit_ptr[VBID + 1] && !tested) {
+  // the CTA's unit range, staged in shared memory at launch: the iteration
+  // barrier's acquire invalidates L1, so a table load here would be an L2
+  // round trip at the start of every iteration
+  const int* urange = reinterpret_cast<const int*>(smem + P.off_red + 32);
+  const int un_a = urange[0], un_b = urange[1];
+  if (un_a == un_b && !tested) {
     if (threadIdx.x == 0) { rbc[0] = rp; rbc[1] = rd; }
     __syncthreads();
     rp = rbc[0]; rd = rbc[1];
     __syncthreads();   // every warp has read the slots before the publish reuses them
     if (patch_stop_test(P, R, it, rp, rd)) return true;
   }
-  for (int un = un_a; un < P.cta_unit_ptr[VBID + 1]; ++un) {
+  for (int un = un_a; un < un_b; ++un) {
     PT_START
     int own_lo, own_hi, plo, phi_, prows, ch_a, ch_b, k0 = 0, c00 = 0, nt0 = 0, S0 = 0, o_off, o_n;
     long long prow0;
@@ -1703,8 +1739,8 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
         __syncthreads();
       }
       if constexpr (RB)
-        rb_chunk<TC>(P, k, nt, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, smem, cur, pri_m, dual_m,
-                     stash + sb * stash_stride);
+        rb_chunk<TC>(P, k, ch == ch_a ? S0 : P.class_s[k], nt, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, smem, cur,
+                     pri_m, dual_m, stash + sb * stash_stride);
       else
       {
         KSplit ks;
@@ -2687,6 +2723,12 @@ __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunAr
   }
   const size_t gt = VBID * blockDim.x + tid, GT = VGRID * blockDim.x;
   PT_INIT
+  if (MODE == kPatch) class_table_load(P, smem);   // DMMA patch chunks; read after step 0's grid barrier
+  if (PATCH && tid == 0) {   // patch modes: the unit range (patch_iteration; read after step 0's grid barrier)
+    int* ur = reinterpret_cast<int*>(smem + P.off_red + 32);
+    ur[0] = P.cta_unit_ptr[VBID];
+    ur[1] = P.cta_unit_ptr[VBID + 1];
+  }
   // fused MPC-step transitions (fused_transition; the host launches this
   // variant only for warm-started closed loops of more than one step with
   // P.fuse_steps): from step 1 on, no grid barrier between steps. A step's
