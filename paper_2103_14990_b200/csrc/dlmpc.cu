@@ -473,7 +473,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         int ldl = P.s_pad;
         while ((2 * ldl) % 16 != 4 && (2 * ldl) % 16 != 12) ldl += 2;
         const long long fixed = ((opr_main + 1) & ~1LL) + 2LL * tc * ldk + (long long)tc * ldl + (long long)n08_max * ldy +
-                                (sp_max > 1 ? (long long)sp_max * n08_max * tc : 0) + 32 + 8 * tc + 8;
+                                (sp_max > 1 ? (long long)sp_max * n08_max * tc : 0) + 34 + 8 * tc + 8;
         // patch rows per unit: 2048 measured 1.3% faster than 4096 at N=1e6
         // (fewer, better-balanced units once the tables fit at the first try)
         long long cap = std::min<long long>(2048, (limit - fixed) / 2);
@@ -586,7 +586,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
             }
             P.off_y = (int)off; off += (long long)n08_max * ldy;
             P.off_yp = (int)off; off += sp_max > 1 ? (long long)sp_max * n08_max * tc : 0;
-            P.off_red = (int)off; off += 32;
+            P.off_red = (int)off; off += 34;   // + the CTA's unit range (2 ints, stream_iteration)
             P.off_meta = (int)off; off += 8 * tc;
             P.off_patch = (int)off; off += (cap + 1) & ~1LL;
             P.off_cpatch = (int)off; off += (cap + 1) & ~1LL;

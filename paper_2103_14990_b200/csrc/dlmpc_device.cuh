@@ -1911,8 +1911,13 @@ struct LamWait {
 // instantiation and read the basis from L2 -- a separate instantiation, so
 // the common path keeps shared-memory fragment loads.
 template <int TC, bool OPS>
+// keep_tab: an earlier iteration of this launch left this CTA's control
+// tables in shared memory (reused when the CTA has a single unit: the tables
+// are invariant, and a reload would cost dependent L2 round trips after the
+// grid barrier, whose acquire invalidates L1); keep_pada: the same for the
+// 1/||a||^2 of the patch subsystems (constant within an MPC step).
 __device__ void stream_iteration(const DevProblem& P, int b, const double* x, int it, int itg, double* smem,
-                                 int& cur, unsigned& ph) {
+                                 int& cur, unsigned& ph, bool keep_tab, bool keep_pada) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* s_patch = smem + P.off_patch;
   double* c_patch = smem + P.off_cpatch;
@@ -1940,8 +1945,12 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
   // unit descriptors, double-buffered in shared memory: the next unit's is
   // fetched (cp.async) while the current unit runs
   int* udesc = reinterpret_cast<int*>(smem + P.off_udesc);   // [2][16]
-  const int un_a = P.cta_unit_ptr[VBID], un_b = P.cta_unit_ptr[VBID + 1];
-  if (un_a < un_b && tid < 4)
+  const int* urange = reinterpret_cast<const int*>(smem + P.off_red + 32);   // staged at launch
+  const int un_a = urange[0], un_b = urange[1];
+  const bool single = un_b - un_a == 1;
+  keep_tab = keep_tab && single;
+  keep_pada = keep_pada && single;
+  if (un_a < un_b && tid < 4 && !keep_tab)
     reinterpret_cast<int4*>(udesc)[tid] = __ldg(reinterpret_cast<const int4*>(P.unit_desc) + 4 * un_a + tid);
   __syncthreads();
   for (int un = un_a; un < un_b; ++un) {
@@ -1976,15 +1985,19 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
     int* chtab = chtab0 + 2 * tb * P.tab_alt;
     double* ptab = ptab0 + tb * P.tab_alt;
     if (un == un_a) {
-      const int4* src = reinterpret_cast<const int4*>(P.chunk_desc + static_cast<size_t>(ch_a) * CHW);
-      int4* dst = reinterpret_cast<int4*>(chtab);
-      for (int q = tid; q < nch * CHW / 4; q += kThreads) dst[q] = __ldg(src + q);
-      const double2* ps = reinterpret_cast<const double2*>(P.unit_ptab + static_cast<size_t>(pt_off) * 6);
-      double2* pd = reinterpret_cast<double2*>(ptab);
-      for (int q = tid; q < npq * 3; q += kThreads) pd[q] = __ldg(ps + q);
-      for (int q = tid; q < npq; q += kThreads) {
-        const double a = ld_cg(P.ada + plo + q);
-        pada0[q] = a > 0.0 ? 1.0 / a : 0.0;   // only read in iterations >= 1 (reciprocal form)
+      if (!keep_tab) {
+        const int4* src = reinterpret_cast<const int4*>(P.chunk_desc + static_cast<size_t>(ch_a) * CHW);
+        int4* dst = reinterpret_cast<int4*>(chtab);
+        for (int q = tid; q < nch * CHW / 4; q += kThreads) dst[q] = __ldg(src + q);
+        const double2* ps = reinterpret_cast<const double2*>(P.unit_ptab + static_cast<size_t>(pt_off) * 6);
+        double2* pd = reinterpret_cast<double2*>(ptab);
+        for (int q = tid; q < npq * 3; q += kThreads) pd[q] = __ldg(ps + q);
+      }
+      if (!keep_pada) {
+        for (int q = tid; q < npq; q += kThreads) {
+          const double a = ld_cg(P.ada + plo + q);
+          pada0[q] = a > 0.0 ? 1.0 / a : 0.0;   // only read in iterations >= 1 (reciprocal form)
+        }
       }
     } else {
       const double* raw = pada0 + P.np_cap + tb * P.tab_alt + (plo & 1);
@@ -2724,7 +2737,8 @@ __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunAr
   const size_t gt = VBID * blockDim.x + tid, GT = VGRID * blockDim.x;
   PT_INIT
   if (MODE == kPatch) class_table_load(P, smem);   // DMMA patch chunks; read after step 0's grid barrier
-  if (PATCH && tid == 0) {   // patch modes: the unit range (patch_iteration; read after step 0's grid barrier)
+  int lit = 0;   // stream mode: iterations run in this launch (table reuse, stream_iteration)
+  if ((PATCH || MODE == kStream) && tid == 0) {   // the unit range (read after step 0's grid barrier)
     int* ur = reinterpret_cast<int*>(smem + P.off_red + 32);
     ur[0] = P.cta_unit_ptr[VBID];
     ur[1] = P.cta_unit_ptr[VBID + 1];
@@ -2818,8 +2832,9 @@ __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunAr
       PT_DECL
       if (MODE == kStream) {
         const int itg = it + (R.closed_loop ? 0 : R.it_base);
-        if (P.cta_gop && P.cta_gop[VBID]) stream_iteration<TC, false>(P, b, x, it, itg, smem, cur, ph);
-        else stream_iteration<TC, true>(P, b, x, it, itg, smem, cur, ph);
+        if (P.cta_gop && P.cta_gop[VBID]) stream_iteration<TC, false>(P, b, x, it, itg, smem, cur, ph, lit > 0, lit > 0 && it > 0);
+        else stream_iteration<TC, true>(P, b, x, it, itg, smem, cur, ph, lit > 0, lit > 0 && it > 0);
+        ++lit;
         fence_proxy_async_global();
         PT_START
       } else {
