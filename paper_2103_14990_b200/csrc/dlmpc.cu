@@ -104,6 +104,11 @@ KernelFn pick_kernel(int mode, int tc, int rb = 0) {
 KernelFn pick_kernel_var(int mode, int tc, int var) {
   if (var == kVarPairs && mode == kPatch)
     return tc == 16 ? dlmpc_persistent<16, kPatch, kVarPairs> : dlmpc_persistent<8, kPatch, kVarPairs>;
+  if (var == kVarPcache && mode == kPatch)
+    return tc == 16 ? dlmpc_persistent<16, kPatch, kVarPcache> : dlmpc_persistent<8, kPatch, kVarPcache>;
+  if (var == (kVarPairs | kVarPcache) && mode == kPatch)
+    return tc == 16 ? dlmpc_persistent<16, kPatch, kVarPairs | kVarPcache>
+                    : dlmpc_persistent<8, kPatch, kVarPairs | kVarPcache>;
   if (var == kVarFuse && mode == kPatch) return tc == 16 ? dlmpc_persistent<16, kPatch, kVarFuse> : dlmpc_persistent<8, kPatch, kVarFuse>;
   if (var == kVarFuse && mode == kPatchRb) return dlmpc_persistent<8, kPatchRb, kVarFuse>;
   if (var == kVarDist) {
@@ -164,6 +169,7 @@ int ensure_run_buffers(dlmpc_handle* h, int max_iters, int t_sim) {
 int launch(dlmpc_handle* h, const RunArgs& R, int var = 0) {
   KernelFn fn = pick_kernel(h->mode, h->P.tile_cols, h->P.rb_gemv);
   if (h->P.cta_pair && h->mode == kPatch) var |= kVarPairs;
+  if (h->P.cache_phi == 2 && h->mode == kPatch) var |= kVarPcache;
   if (h->P.fuse_steps && R.closed_loop && R.warm_start && R.t_sim > 1) var |= kVarFuse;
   if (var) fn = pick_kernel_var(var == kVarFuse && h->P.rb_gemv ? kPatchRb : h->mode, h->P.tile_cols, var);
   if (!fn) return fail(h, DLMPC_BAD_ARGUMENT, "no kernel variant for this mode");
@@ -676,18 +682,26 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       const long long rb_part = rb ? 2LL * 16 * rb_al * kWarps : 0;
       const int kt_cols = rb ? 0 : tc, st_cols = rb ? 2 : tc;
       auto part = [&](int sp) { return std::max<long long>(sp > 1 ? (long long)sp * n08_max * tc : 0, rb_part); };
-      auto total = [&](long long opr, int sp, bool cache) {
+      // partial Φ cache (no per-row scales and bounds; phi_rows_pcached)
+      const long long meta_part = meta_phi - 3 * prows_max;
+      auto total = [&](long long opr, int sp, long long meta) {
         return opr + (long long)kt_cols * ldk + (long long)n08_max * ldy + part(sp)
-               + 34 + 4 * tc + prows_max + (cache ? meta_phi : 0) + 4;
+               + 34 + 4 * tc + prows_max + meta + 4;
       };
-      while (split_max > 1 && total(0, split_max, false) > limit) split_max >>= 1;
-      if (total(0, split_max, false) > limit) {
+      while (split_max > 1 && total(0, split_max, 0) > limit) split_max >>= 1;
+      if (total(0, split_max, 0) > limit) {
         if (tc == 16) { tc = 8; continue; }
         return fail(h, DLMPC_BAD_ARGUMENT, "column tile does not fit in shared memory");
       }
-      long long opr = total(opr_need, split_max, false) <= limit ? opr_need : 0;
-      if (rb && opr > 0 && opr < rb_opr && total(rb_opr, split_max, false) <= limit) opr = rb_opr;
-      const bool cache = h->mode == kPatch && one_unit && total(opr, split_max, true) <= limit;
+      long long opr = total(opr_need, split_max, 0) <= limit ? opr_need : 0;
+      if (rb && opr > 0 && opr < rb_opr && total(rb_opr, split_max, 0) <= limit) opr = rb_opr;
+      const bool cache = h->mode == kPatch && one_unit && total(opr, split_max, meta_phi) <= limit;
+      // where the full cache does not fit (the largest C4 cells), the partial
+      // one: d=6, T=30 at N=1000 (measured in DESIGN §5)
+      const char* epc = getenv("DLMPC_PARTIAL_PHI");
+      const bool pcache = !cache && !rb && h->mode == kPatch && one_unit && !(epc && epc[0] == '0') &&
+                          total(opr, split_max, meta_part) <= limit;
+      const long long meta_sz = cache ? meta_phi : (pcache ? meta_part : 0);
       // cp.async staging buffers for chunk ψ,λ (patch mode): 2 if they fit, else 1, else none
       const long long stash_one = 2LL * st_cols * ldk;
       int stash_bufs = 0;
@@ -695,7 +709,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         // staging buffers within ~200 KB of shared memory in all: a larger
         // carveout leaves too little L1 for the kernel's table loads (d=3,
         // T=10 at N=1000: 1.4% slower with a buffer that took it to 208 KB)
-        const long long base = total(opr, split_max, cache);
+        const long long base = total(opr, split_max, meta_sz);
         const long long lim = std::min<long long>(limit, (no_split ? 200LL * 1024 : 1LL << 40) / 8);
         stash_bufs = base + 2 * stash_one + 2 <= lim ? 2 : (base + stash_one + 2 <= lim ? 1 : 0);
       }
@@ -714,9 +728,9 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       P.off_meta = (int)off; off += 4 * tc;
       P.off_patch = (int)off; off += (prows_max + 1) & ~1LL;
       P.patch_cap = (int)prows_max;
-      P.off_phimeta = (int)off; off += cache ? meta_phi : 0;
+      P.off_phimeta = (int)off; off += meta_sz;
       P.off_ublk = (int)(off - (np_max + 8 + 2));   // tail of the Φ metadata block (cache only)
-      P.cache_phi = cache ? 1 : 0;
+      P.cache_phi = cache ? 1 : (pcache ? 2 : 0);
       off = (off + 1) & ~1LL;   // 16-byte alignment for cp.async
       P.off_stash = (int)off; off += stash_bufs * stash_one;
       P.stash_bufs = stash_bufs;
@@ -760,7 +774,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       // DLMPC_FUSE_STEPS=1 forces it for any eligible plan, =0 disables it
       const char* e = getenv("DLMPC_FUSE_STEPS");
       const bool force = e && e[0] == '1', off_env = e && e[0] == '0';
-      const bool want = h->mode == kPatch && P.cache_phi && cta_pair.empty() && P.own_sub_lo == 0 &&
+      const bool want = h->mode == kPatch && P.cache_phi == 1 && cta_pair.empty() && P.own_sub_lo == 0 &&
                         P.own_sub_hi == pr->n_sub && pr->a_ptr && pr->b_ptr && !off_env &&
                         (P.rb_gemv || force) &&
                         (long long)pr->n_cols * pr->s_pad < INT_MAX && pr->row_start[pr->n_sub] < INT_MAX &&

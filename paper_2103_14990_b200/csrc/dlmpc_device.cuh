@@ -1454,7 +1454,8 @@ __device__ void cache_phi_meta(const DevProblem& P, const double* x, double* sme
   double* xk = base + static_cast<size_t>(np) * P.d_pad;
   double* ada = xk + static_cast<size_t>(np) * P.d_pad;
   double* rw = ada + np;
-  int* len = reinterpret_cast<int*>(rw + 3 * prows);
+  const bool part = P.cache_phi == 2;   // partial cache: no per-row scales and bounds, raw ||a||^2
+  int* len = reinterpret_cast<int*>(rw + (part ? 0 : 3 * prows));
   int* ublk = reinterpret_cast<int*>(smem + P.off_ublk);
   int2* rinfo = reinterpret_cast<int2*>(smem + P.off_ublk + 8);
   const int ch_a = P.unit_chunk_ptr[un0], ch_b = P.unit_chunk_ptr[un0 + 1];
@@ -1474,7 +1475,7 @@ __device__ void cache_phi_meta(const DevProblem& P, const double* x, double* sme
       rinfo[q] = make_int2(static_cast<int>(P.row_start[plo + q] - prow0),
                            static_cast<int>(P.row_start[plo + q + 1] - P.row_start[plo + q]));
     }
-    for (int q = threadIdx.x; q < prows; q += kThreads) {
+    for (int q = threadIdx.x; q < (part ? 0 : prows); q += kThreads) {
       rw[prows + q] = P.row_lo[prow0 + q]; rw[2 * prows + q] = P.row_hi[prow0 + q];
     }
     const int own_lo = P.unit_sub_lo[un0], own_hi = P.unit_sub_hi[un0];
@@ -1505,7 +1506,8 @@ __device__ void cache_phi_meta(const DevProblem& P, const double* x, double* sme
     const int i = plo + q;
     const int D = len[q];
     for (int k = lane; k < D; k += 32) xk[q * P.d_pad + k] = ld_cg(x + P.supp_col[static_cast<size_t>(i) * P.d_pad + k]);
-    phi_cache_scales(P, ld_cg(P.ada + i), rinfo[q], P.row_w + prow0, ada + q, rw);
+    if (part) { if (lane == 0) ada[q] = ld_cg(P.ada + i); }
+    else phi_cache_scales(P, ld_cg(P.ada + i), rinfo[q], P.row_w + prow0, ada + q, rw);
   }
   if (one_chunk && threadIdx.x < TC) {
     const int t = threadIdx.x;
@@ -1571,6 +1573,54 @@ __device__ __forceinline__ void phi_rows_cached(const DevProblem& P, int q, int 
   }
 }
 
+// Φ scale of the rows of patch subsystem q from the partial cache
+// (P.cache_phi == 2: the support descriptors, x on the support and the raw
+// ||a||^2 in shared memory; a plan whose per-row scales and bounds do not fit
+// shared memory). The row weight and bounds come from global memory with the
+// row's ψ, λ (one round trip); the two reciprocals are formed as
+// phi_cache_scales forms them.
+template <class Out>
+__device__ __forceinline__ void phi_rows_pcached(const DevProblem& P, int q, int np, long long prow0, int r_off,
+                                                 int nr, const double* psi, const double* lam, const double* smem,
+                                                 const Out& out) {
+  const int lane = threadIdx.x & 31;
+  const double* base = smem + P.off_phimeta;
+  const long long* bk = reinterpret_cast<const long long*>(base) + static_cast<size_t>(q) * P.d_pad;
+  const double* xk = base + static_cast<size_t>(np) * P.d_pad + static_cast<size_t>(q) * P.d_pad;
+  const double* ada_p = base + 2 * static_cast<size_t>(np) * P.d_pad;
+  const int D = reinterpret_cast<const int*>(ada_p + np)[q];
+  const double a = ada_p[q];
+  const double inv_ada = a > 0.0 ? 1.0 / a : 0.0;
+  const double rho = P.rho;
+  for (int l0 = 0; l0 < nr; l0 += 32) {
+    const int l = l0 + lane;
+    if (l >= nr) break;
+    const long long gr = prow0 + r_off + l;
+    const double w = P.row_w[gr], lo = P.row_lo[gr], hi = P.row_hi[gr];
+    double acc = 0.0;
+    for (int k0 = 0; k0 < D; k0 += 16) {
+      double pv[16], lv[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        pv[u] = lv[u] = 0.0;
+        if (k0 + u < D) {
+          const long long b = bk[k0 + u] + l;
+          if (DCHK(P, b >= 0 && b < static_cast<long long>(P.n_cols) * P.s_pad, 10, b)) {
+            pv[u] = ld_cg(psi + b);
+            lv[u] = ld_cg(lam + b);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (k0 + u < D) acc = fma(__dsub_rn(pv[u], lv[u]), xk[k0 + u], acc);
+    }
+    const double inv_den = 1.0 / (P.rho + 2.0 * w * a);
+    const double y = fmin(fmax(rho * acc * inv_den, lo), hi);
+    out(l, (y - acc) * inv_ada);
+  }
+}
+
 // One ADMM iteration of the patch kernel for this CTA's units.
 // The stop test of iteration it-1 (global residual maxima, published before
 // the grid barrier) is overlapped with iteration it's first Φ stage: the two
@@ -1594,7 +1644,7 @@ __device__ __forceinline__ bool patch_stop_test(const DevProblem& P, const RunAr
 // FUSE (kVarFuse kernels only; measured: the extra state compiled into the
 // plain kernel made ptxas interleave the Φ loads with the dot product, +47%
 // per C2 iteration, so the plain path keeps its original form):
-template <int TC, bool RB, bool PAIRS, bool FUSE>
+template <int TC, bool RB, bool PAIRS, bool FUSE, bool PCACHE>
 __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int it, double* smem,
                                 int& cur, const RunArgs& R, unsigned bar_target, int& pair_cnt, int roff,
                                 unsigned pre_target) {
@@ -1675,7 +1725,9 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
         dst[l] = s;
         if (gdst) gdst[l] = s;
       };
-      if (P.cache_phi)
+      if constexpr (PCACHE)   // the partial cache (kVarPcache kernels: P.cache_phi == 2)
+        phi_rows_pcached(P, i - plo, phi_ - plo, prow0, r_off, nrow, psi, lam, smem, out);
+      else if (P.cache_phi)
         phi_rows_cached<RB>(P, i - plo, phi_ - plo, prows, r_off, nrow, psi, lam, smem, out);
       else
         phi_rows_of<false>(P, i, psi, lam, x, out);
@@ -2696,6 +2748,8 @@ __device__ bool dist_exchange(const DevProblem& P, const RunArgs& R, int it, int
 constexpr int kVarDist = 1;    // graph-partitioned solve, exchange on the device (non-patch modes)
 constexpr int kVarPairs = 2;   // patch mode with K-split CTA pairs
 constexpr int kVarFuse = 4;    // patch mode closed loops, warm-started: fused MPC-step transitions (P.fuse_steps)
+constexpr int kVarPcache = 8;  // patch mode with the partial Φ cache (P.cache_phi == 2; compiled into the
+                               // common kernel it spilled and cost the other C4 cells 4%)
 
 template <int TC, int MODE, int VAR>
 __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunArgs& R);
@@ -2806,7 +2860,7 @@ __device__ __forceinline__ void persistent_body(const DevProblem& P, const RunAr
           break;
         }
         bar_epoch += VGRID;
-        if (patch_iteration<TC, MODE == kPatchRb, (VAR & kVarPairs) != 0, fuse>(
+        if (patch_iteration<TC, MODE == kPatchRb, (VAR & kVarPairs) != 0, fuse, PATCH && (VAR & kVarPcache) != 0>(
                 P, b, x, it, smem, cur, R, bar_base + bar_epoch, pair_cnt, roff, it == 0 ? pre_target : 0u)) {
           bar_epoch -= VGRID;   // returned before arriving
           conv = true;

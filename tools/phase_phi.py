@@ -1,4 +1,4 @@
-"""Thread 0's view of the patch Φ stage (timing build, slots 12-15 and 0):
+"""Thread 0's view of the patch Φ stage (timing build, slots 12-15 and 0; locality and horizon from DLMPC_PP_D / DLMPC_PP_T):
 DLMPC_LIB=paper_2103_14990_b200/libdlmpc_timing.so python tools/phase_phi.py [N] [t_sim]"""
 import os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
@@ -6,7 +6,8 @@ import numpy as np
 import paper_2103_14990_b200 as pb
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 100
 t_sim = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=n, d=3, horizon=10, t_sim=t_sim, seed=1))
+system, spec, mask, x0 = pb.scenario_problem(pb.Scenario(n=n, d=int(os.environ.get("DLMPC_PP_D", 3)),
+                                                      horizon=int(os.environ.get("DLMPC_PP_T", 10)), t_sim=t_sim, seed=1))
 sess = pb.DlmpcSession(system, spec, mask, "b200")
 sess.simulate(x0, t_sim)
 sess.device.phase_times(reset=True)
