@@ -115,3 +115,24 @@ def test_row_infeasible_at_a_later_step(variant):
         pb.dlmpc_simulate(system, spec, mask, x0, 4, variant)
     assert exc.value.step == 1
     assert exc.value.row == ref["at"][1]
+
+
+@pytest.mark.parametrize("n,d,t,expect", [
+    (100, 3, 10, {"grid": 100, "cache_phi": 1, "fuse_steps": 1, "rb_gemv": 1, "pairs": 0}),   # C2
+    (1000, 3, 10, {"grid": 148, "cache_phi": 1, "fuse_steps": 0, "rb_gemv": 0}),
+    (1000, 6, 30, {"cache_phi": 2, "pairs": 1}),                                               # partial Φ cache
+])
+def test_plan_choices_of_the_timed_configs(n, d, t, expect):
+    """The kernel plans the bench and the C4 sweep time: C2
+    launches only the CTAs that own a unit and fuses its step transitions;
+    the largest C4 cell takes the partial Φ cache and K-split pairs."""
+    system = pb.build_chain_network(n)
+    spec = pb.make_benchmark_spec(system, t)
+    mask = pb.build_locality_mask(system, d, t)
+    sess = pb.DlmpcSession(system, spec, mask, FAST)
+    try:
+        info = sess.device.info()
+    finally:
+        sess.close()
+    for k, v in expect.items():
+        assert info[k] == v, (k, info)
