@@ -710,7 +710,9 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
         // carveout leaves too little L1 for the kernel's table loads (d=3,
         // T=10 at N=1000: 1.4% slower with a buffer that took it to 208 KB)
         const long long base = total(opr, split_max, meta_sz);
-        const long long lim = std::min<long long>(limit, (no_split ? 200LL * 1024 : 1LL << 40) / 8);
+        const char* esl = getenv("DLMPC_STASH_LIM_KB");   // A/B of the carveout rule
+        const long long lim_kb = esl ? atoll(esl) : 200;
+        const long long lim = std::min<long long>(limit, (no_split ? lim_kb * 1024 : 1LL << 40) / 8);
         stash_bufs = base + 2 * stash_one + 2 <= lim ? 2 : (base + stash_one + 2 <= lim ? 1 : 0);
       }
       if (rb && (stash_bufs == 0 || opr < rb_opr)) { rb_off = true; continue; }
