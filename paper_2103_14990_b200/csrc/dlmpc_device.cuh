@@ -43,6 +43,12 @@ namespace dlmpc {
 #ifndef DLMPC_STREAM_MROW
 #define DLMPC_STREAM_MROW 0
 #endif
+#ifndef DLMPC_STREAM_KRB
+// stream Φ: patch rows per thread whose loads are in flight together; 4
+// covers a unit's <= 2048 patch rows in one round trip (N=1e5 642.4 -> 632.9
+// us/iter against 3, bitwise the same; 2 is slower)
+#define DLMPC_STREAM_KRB 4
+#endif
 
 // Optional per-phase timers (profiling build only: -DDLMPC_PHASE_TIMING).
 // Thread 0 of every CTA accumulates SM-cycle deltas per phase in shared
@@ -2103,7 +2109,7 @@ __device__ void stream_iteration(const DevProblem& P, int b, const double* x, in
       }
       // from the per-unit dot partials of the last iteration (slot order);
       // every thread issues the loads of up to kRB rows before using any
-      constexpr int kRB = 3;
+      constexpr int kRB = DLMPC_STREAM_KRB;
       for (int r0 = tid; r0 < prows; r0 += kRB * kThreads) {
         double w[kRB], lo[kRB], hi[kRB], c[kRB], ada[kRB];
         long long grow[kRB];
