@@ -327,12 +327,16 @@ class DeviceSession:
         or raises NotConverged / RowInfeasible with the failing step."""
         L = self.layout
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
-        states = np.zeros((t_sim + 1, L.n_cols))
-        inputs = np.zeros((t_sim, L.n_inputs))
-        iters = np.zeros(t_sim, dtype=np.int32)
+        states = np.empty((t_sim + 1, L.n_cols))     # every row written on success
+        inputs = np.empty((t_sim, L.n_inputs))
+        iters = np.empty(t_sim, dtype=np.int32)
         fstep, fit = C.c_int32(-1), C.c_int32(0)
         bad = C.c_int64(-1)
-        fhist = np.zeros(2 * max_iters)
+        # the failing step's residual history (written on NotConverged only):
+        # one buffer per session instead of a fresh 2 * max_iters array per call
+        fhist = getattr(self, "_fhist", None)
+        if fhist is None or fhist.size < 2 * max_iters:
+            fhist = self._fhist = np.zeros(2 * max_iters)
         rc = self._check(self._lib.dlmpc_simulate(
             self._h, _ptr(x0, C.c_double), int(t_sim), int(bool(warm_start)), int(bool(cold_start)),
             int(max_iters), float(eps_pri), float(eps_dual), _ptr(states, C.c_double),
