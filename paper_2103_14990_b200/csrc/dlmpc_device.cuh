@@ -2551,9 +2551,10 @@ static __device__ void fused_tables_load(const DevProblem& P, double* smem) {
 template <int TC>
 __device__ void fused_transition(const DevProblem& P, int pb, const double* x, double* xn, double* inputs_out,
                                  double* states_out, double* smem, bool refresh, int* next_bad) {
-  const int un = P.cta_unit_ptr[VBID];
+  const int* urange = reinterpret_cast<const int*>(smem + P.off_red + 32);   // staged at launch
+  const int un = urange[0];
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  if (un == P.cta_unit_ptr[VBID + 1]) {   // no unit: only the split-barrier arrival
+  if (un == urange[1]) {   // no unit: only the split-barrier arrival
     if (refresh && t == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" :: "l"(P.gbar) : "memory");
     return;
   }
