@@ -358,6 +358,21 @@ __device__ __forceinline__ void stash_issue(const DevProblem& P, int c0, int nt,
   cp_async_commit();
 }
 
+// Patch mode without staging buffers: the first chunk's ψ, λ lines into L1
+// under the Φ stage (no registers held); the chunk's prologue and epilogue
+// read them with plain loads. Legal right after the iteration barrier: its
+// acquire invalidated L1, and buffer b is read-only until the next barrier.
+__device__ __forceinline__ void chunk_prefetch_l1(const double* psi, const double* lam, int c0, int nt, int s_pad) {
+  const long long n = static_cast<long long>(nt) * s_pad;   // doubles per array
+  const long long lines = (n + 15) / 16;                    // 128-byte lines
+  const double* b0 = psi + static_cast<long long>(c0) * s_pad;
+  const double* b1 = lam + static_cast<long long>(c0) * s_pad;
+  for (long long q = threadIdx.x; q < 2 * lines; q += kThreads) {
+    const double* a = (q < lines ? b0 : b1) + 16 * (q < lines ? q : q - lines);
+    asm volatile("prefetch.global.L1 [%0];\n" :: "l"(a));
+  }
+}
+
 template <bool EXACT>
 __device__ __forceinline__ double make_phi(double v, double s, double xc) {
   return EXACT ? __dadd_rn(v, __dmul_rn(s, xc)) : fma(s, xc, v);
@@ -1138,7 +1153,11 @@ __device__ __forceinline__ void ksplit_exchange_y(const DevProblem& P, const KSp
   __syncthreads();
 }
 
-template <int TC, bool S_GLOBAL, bool OPS, bool KS = false>
+// L1LD (the partial-cache patch kernels, kVarPcache): ψ, λ of the chunk with
+// plain loads, prefetched into L1 under the Φ stage (chunk_prefetch_l1):
+// the epilogue's second read of them hits L1 (d=6, T=30: 190.7 -> 185.5
+// us/iter; in the other patch kernels it measured up to 2% slower).
+template <int TC, bool S_GLOBAL, bool OPS, bool KS = false, bool L1LD = false>
 __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi, const double* lam,
                            double* psi_n, double* lam_n, const double* s_src, const int* irow_tab,
                            double* smem, double& pri_m, double& dual_m, const double* st,
@@ -1186,6 +1205,9 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
           if (st) {
             ps[u] = st[(2 * t) * ldk + p];
             lm[u] = st[(2 * t + 1) * ldk + p];
+          } else if (L1LD) {   // partial-cache patch kernels: L1 hits after chunk_prefetch_l1
+            ps[u] = psi[pos0 + p];
+            lm[u] = lam[pos0 + p];
           } else {
             ps[u] = ld_cg(psi + pos0 + p);
             lm[u] = ld_cg(lam + pos0 + p);
@@ -1235,6 +1257,9 @@ __device__ void fast_chunk(const DevProblem& P, int k, int nt, const double* psi
             if (st) {
               ps[u] = st[(2 * t) * ldk + p];
               lm[u] = st[(2 * t + 1) * ldk + p];
+            } else if (L1LD) {
+              ps[u] = psi[pos0 + p];
+              lm[u] = lam[pos0 + p];
             } else {
               ps[u] = ld_cg(psi + pos0 + p);
               lm[u] = ld_cg(lam + pos0 + p);
@@ -1296,7 +1321,7 @@ __device__ __forceinline__ void stage_operator_sized(const DevProblem& P, int k,
   cur = k;
 }
 
-template <int TC, bool S_GLOBAL>
+template <int TC, bool S_GLOBAL, bool L1LD = false>
 __device__ __forceinline__ void run_chunk(const DevProblem& P, int k, int nt, const double* psi,
                                           const double* lam, double* psi_n, double* lam_n,
                                           const double* s_src, const int* irow_tab, double* smem,
@@ -1304,12 +1329,12 @@ __device__ __forceinline__ void run_chunk(const DevProblem& P, int k, int nt, co
                                           const double* st = nullptr, const KSplit& ks = KSplit()) {
   const bool ops = stage_operator(P, k, smem, cur);
   if (!S_GLOBAL && ks.partner >= 0) {   // K-split pair (patch mode; bases that live in L2)
-    if (ops) fast_chunk<TC, S_GLOBAL, true, true>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st, ks);
-    else fast_chunk<TC, S_GLOBAL, false, true>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st, ks);
+    if (ops) fast_chunk<TC, S_GLOBAL, true, true, L1LD>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st, ks);
+    else fast_chunk<TC, S_GLOBAL, false, true, L1LD>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st, ks);
   } else if (ops) {
-    fast_chunk<TC, S_GLOBAL, true>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st);
+    fast_chunk<TC, S_GLOBAL, true, false, L1LD>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st);
   } else {
-    fast_chunk<TC, S_GLOBAL, false>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st);
+    fast_chunk<TC, S_GLOBAL, false, false, L1LD>(P, k, nt, psi, lam, psi_n, lam_n, s_src, irow_tab, smem, pri_m, dual_m, st);
   }
 }
 
@@ -1718,6 +1743,7 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
     double* stash = smem + P.off_stash;
     const int stash_stride = 2 * P.stash_cols * P.ldk;
     if (P.stash_bufs > 0 && ch_a < ch_b) stash_issue(P, c00, nt0, S0, psi, lam, stash);
+    else if (PCACHE && ch_a < ch_b) chunk_prefetch_l1(psi, lam, c00, nt0, P.s_pad);
     PT_LAP(P, 12)   // timing build, patch modes: thread 0's view of the Φ stage in slots 12-15
     // Φ scale of every row the unit's columns touch (own rows + d-hop halo);
     // before the stop test the own rows' s goes to shared memory only
@@ -1806,7 +1832,7 @@ __device__ bool patch_iteration(const DevProblem& P, int b, const double* x, int
           const int pv = P.cta_pair[VBID];
           if (pv >= 0) { ks.partner = pv >> 1; ks.half = pv & 1; ks.cnt = &pair_cnt; }
         }
-        run_chunk<TC, false>(P, k, nt, psi, lam, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, nullptr, smem, cur,
+        run_chunk<TC, false, PCACHE>(P, k, nt, psi, lam, P.psi[b ^ 1], P.lam[b ^ 1], s_patch, nullptr, smem, cur,
                              pri_m, dual_m, P.stash_bufs > 0 ? stash + sb * stash_stride : nullptr, ks);
       }
       if (P.stash_bufs == 1 && ch + 1 < ch_b)   // single buffer: refill after the chunk is done
