@@ -698,10 +698,13 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       const bool cache = h->mode == kPatch && one_unit && total(opr, split_max, meta_phi) <= limit;
       // where the full cache does not fit (the largest C4 cells), the partial
       // one: d=6, T=30 at N=1000 (measured in DESIGN §5)
+      // (DLMPC_PARTIAL_PHI=0 disables it, =2 takes it in place of the full
+      // cache -- tests: the partial-cache kernels on small problems)
       const char* epc = getenv("DLMPC_PARTIAL_PHI");
-      const bool pcache = !cache && !rb && h->mode == kPatch && one_unit && !(epc && epc[0] == '0') &&
+      const bool force_pc = epc && epc[0] == '2' && !rb;
+      const bool pcache = (!cache || force_pc) && !rb && h->mode == kPatch && one_unit && !(epc && epc[0] == '0') &&
                           total(opr, split_max, meta_part) <= limit;
-      const long long meta_sz = cache ? meta_phi : (pcache ? meta_part : 0);
+      const long long meta_sz = pcache ? meta_part : (cache ? meta_phi : 0);
       // cp.async staging buffers for chunk ψ,λ (patch mode): 2 if they fit, else 1, else none
       const long long stash_one = 2LL * st_cols * ldk;
       int stash_bufs = 0;
@@ -732,7 +735,7 @@ int plan(dlmpc_handle* h, const dlmpc_problem* pr) {
       P.patch_cap = (int)prows_max;
       P.off_phimeta = (int)off; off += meta_sz;
       P.off_ublk = (int)(off - (np_max + 8 + 2));   // tail of the Φ metadata block (cache only)
-      P.cache_phi = cache ? 1 : (pcache ? 2 : 0);
+      P.cache_phi = pcache ? 2 : (cache ? 1 : 0);
       off = (off + 1) & ~1LL;   // 16-byte alignment for cp.async
       P.off_stash = (int)off; off += stash_bufs * stash_one;
       P.stash_bufs = stash_bufs;

@@ -136,3 +136,41 @@ def test_plan_choices_of_the_timed_configs(n, d, t, expect):
         sess.close()
     for k, v in expect.items():
         assert info[k] == v, (k, info)
+
+
+@pytest.mark.parametrize("n,d,t", [(300, 2, 5), (1000, 3, 10), (1000, 4, 20)])
+def test_partial_phi_cache_matches_full_cache(n, d, t):
+    """The partial Φ cache (kVarPcache kernels, with the L1-prefetched chunk;
+    taken by the largest C4 cells) forced on small plans: the same iteration
+    counts as the full-cache plan and the oracle, states within the fast
+    path's tolerance."""
+    system = pb.build_chain_network(n)
+    spec = pb.make_benchmark_spec(system, t)
+    mask = pb.build_locality_mask(system, d, t)
+    old = os.environ.get("DLMPC_PARTIAL_PHI")
+    os.environ["DLMPC_PARTIAL_PHI"] = "2"
+    try:
+        os.environ["DLMPC_FUSE_STEPS"] = "0"
+        part = pb.DlmpcSession(system, spec, mask, FAST)
+    finally:
+        os.environ.pop("DLMPC_FUSE_STEPS", None)
+        if old is None:
+            os.environ.pop("DLMPC_PARTIAL_PHI", None)
+        else:
+            os.environ["DLMPC_PARTIAL_PHI"] = old
+    full = _session(system, spec, mask, False)
+    try:
+        info = part.device.info()
+        if info["rb_gemv"]:
+            pytest.skip("GEMV-pair plan (the partial cache is for the DMMA plans)")
+        assert info["cache_phi"] == 2, info
+        assert full.device.info()["cache_phi"] == 1
+        for seed in (1, 2):
+            x0 = pb.sample_initial_state(system.partition, np.random.default_rng(seed))
+            ta, _ = full.simulate(x0, 4)
+            tb, _ = part.simulate(x0, 4)
+            assert list(ta.step_iterations) == list(tb.step_iterations)
+            scale = np.max(np.abs(ta.states))
+            assert np.max(np.abs(ta.states - tb.states)) <= 1e-12 * scale
+    finally:
+        part.close(); full.close()
