@@ -34,6 +34,7 @@ def _session(system, spec, mask, fuse, variant=FAST):
 
 @pytest.mark.parametrize("n,d,t,eps,max_iters,t_sim", [
     (100, 3, 10, 1e-4, 5000, 20),    # C2, the bench workload
+    (100, 3, 10, 1e-4, 5000, 150),   # a long loop: the residual regions and RowInfeasible slots wrap many times
     (12, 2, 4, 1e-4, 5000, 9),       # fewer units than CTAs (idle CTAs on the split barrier)
     (40, 1, 3, 1e6, 1, 7),           # one iteration per step: the max_iters stop test path
     (300, 2, 5, 1e-4, 5000, 6),      # two subsystems per unit
